@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the cell-list force path (arXiv 1412.3784) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 4] [--variant do|ds]
+
+A step is one SLLOD step of the whole hot path (box update and
+remap, wrap + cell keys, counting sort, neighborhood + pair kernel, reduction,
+kick/drift) on the resident state of BASELINE configs[4] (67,108,864 LJ
+particles, planar-elongation KR box, fp32).  Prints ONE JSON line (rank 0).
+
+metric = pair interactions/s (unordered physical pairs |P|/2 per force
+evaluation / step time); particle-steps/s is reported beside it.  The timed
+region is bracketed by barrier + synchronize, timed with CUDA events on the
+library's stream, max over ranks.  Inputs (~100 B/particle, 7 GB) are far
+larger than L2 (126 MB), so no L2 flush is needed.
+
+--impl reference times the CPU oracle (oracle/, fp64, the box's host cores)
+on the same config and metric, each step a bounded particle sample with the
+O(N) cell build amortized per particle.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "force-step throughput: pair interactions/s and particle-steps/s per GPU, % roofline"
+UNIT = "pair interactions/s"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
+
+
+def dist_setup(backend):
+    import torch.distributed as dist
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend)
+    return rank, lrank, ws
+
+
+def workload(k: int):
+    from paper_1412_3784_b200 import workloads as W
+
+    return W.make(k)
+
+
+def oracle_sample(w, q32, sample: int, seed: int = 0):
+    """The CPU oracle as it stands on a bounded sample of the workload: full O(N)
+    DO cell-list build, pair loop for `sample` random particles; extrapolated to
+    one full force evaluation.  Returns (interactions/s unordered, seconds per
+    full evaluation, sample description, threads)."""
+    import oracle
+
+    qo = oracle.wrap(q32.astype(np.float64), w.L, "f32")
+    rng = np.random.default_rng(seed)
+    idx = np.sort(rng.choice(len(qo), size=sample, replace=False))
+    r = oracle.evaluate(oracle.DO, qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx, want=())
+    n = len(qo)
+    t_full = r.t_build + r.t_eval * (n / sample)
+    inter_full = r.interactions * (n / sample) / 2.0
+    return inter_full / t_full, t_full, r, oracle.num_threads()
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    w = workload(args.config)
+    from paper_1412_3784_b200 import workloads as W
+
+    q = W.positions(w, dtype=np.float32, k=args.config)
+    sample = args.ref_sample
+    vals, times = [], []
+    for s in range(args.warmup + args.steps):
+        v, tf, r, thr = oracle_sample(w, q, sample, seed=s)
+        if s >= args.warmup:
+            vals.append(v)
+            times.append(tf)
+    value = len(vals) / sum(1.0 / v for v in vals)  # harmonic mean = total work / total time
+    ms = 1e3 * statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
+        "config": {"workload": f"C{args.config}", "n": w.n, "variant": "do", "box": "KR planar elongation"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+                         "sample": f"per step: full O(N) DO cell build + pair loop of {sample} random particles, "
+                                   f"extrapolated to one force evaluation of all {w.n}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    rank, lrank, ws = dist_setup("nccl")
+    torch.cuda.set_device(lrank)
+    from paper_1412_3784_b200 import workloads as W
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = workload(args.config)
+    peaks = load_peaks()
+    # the same seeded workload per rank (independent replicas; slab decomposition is the next row)
+    q = W.positions(w, dtype=np.float32, k=args.config, r=0)
+    p = W.momenta(w, dtype=np.float32, k=args.config, r=0)
+    stream = torch.cuda.Stream(lrank)
+    cl = CellList(args.variant, "f32", rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
+                  capacity=w.n, max_cells=int(2.5 * w.n / 13) + 65536, device=lrank, stream=stream.cuda_stream)
+    kw = dict(L0=w.L0)
+    if w.policy == "kr":
+        kw["tstar"] = w.extra["tstar"]
+    if w.policy == "gkr":
+        kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
+    cl.set_flow(w.A, w.policy, w.t0, **kw)
+    qd = torch.from_numpy(q).to(f"cuda:{lrank}")
+    pd = torch.from_numpy(p).to(f"cuda:{lrank}")
+    cl.set_state(qd, pd)
+    del qd, pd
+    dt = w.dt
+    for _ in range(args.warmup):
+        cl.step(dt, 1, want_uw=False)
+    torch.cuda.synchronize()
+
+    import torch.distributed as dist
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    sampler = ClockSampler(lrank)
+    cl.profile(True)
+    l0 = cl.launches()
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        cl.step(dt, 1, want_uw=False)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = cl.launches() - l0
+    prof = cl.profile_read()
+    cl.profile(False)
+    st = cl.stats()
+    if ws > 1:
+        t = torch.tensor([ms_total], device=f"cuda:{lrank}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        tot = torch.tensor([st["acc_interactions"], st["acc_candidates"]], dtype=torch.float64, device=f"cuda:{lrank}")
+        dist.all_reduce(tot)
+        acc_inter, acc_cand = float(tot[0]), float(tot[1])
+    else:
+        acc_inter, acc_cand = st["acc_interactions"], st["acc_candidates"]
+    evals = st["acc_evals"]
+    secs = ms_total * 1e-3
+    value = (acc_inter / 2.0) / secs
+    psteps = w.n * ws * args.steps / secs
+
+    # roofline of the dominant kernel (pair kernel), from live per-launch event times
+    pairs_ms, pairs_n = prof["pairs"]
+    pairs_ms_avg = pairs_ms / max(pairs_n, 1)
+    cand = st["acc_candidates"] / max(evals, 1)
+    inter = st["acc_interactions"] / max(evals, 1)
+    nsm = torch.cuda.get_device_properties(lrank).multi_processor_count
+    fmax = (peaks.get("sm_max_mhz") or 1965.0) * 1e6
+    p32 = nsm * 128 * 2 * fmax                      # FP32 FMA lanes x 2 flops x clock
+    p64 = p32 / 2.0                                 # B200 FP64 = 1/2 FP32
+    flops = 9.0 * cand + 30.0 * inter               # SURVEY 8(d3) work model (algorithmic)
+    t_bound = 9.0 * cand / p32 + 30.0 * inter / p64  # filter in fp32, interactions in fp64
+    achieved = flops / (pairs_ms_avg * 1e-3) / 1e12
+    peak = flops / t_bound / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(f"C{args.config}-{args.variant}", {}).get("pairs_dram_bytes")
+        except Exception:
+            traffic = None
+    kernel_ms = {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]}
+
+    # e2e: the same metric through the C-ABI with HOST (pinned) buffers, copies inside the timed region
+    e2e = None
+    if rank == 0 or True:
+        qh = torch.from_numpy(q).pin_memory()
+        Fh = torch.empty_like(qh).pin_memory()
+        cl.set_box(cl_box(cl))
+        cl.compute_forces(qh, Fh)  # warm-up
+        torch.cuda.synchronize()
+        reps = max(1, min(3, args.steps))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            _, Ue, _ = cl.compute_forces(qh, Fh)
+        t1 = time.perf_counter()
+        se = cl.stats()
+        e2e = {"value": (se["interactions"] / 2.0) / ((t1 - t0) / reps), "unit": UNIT,
+               "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(Fh.numel() * 4 + 8 + 48),
+               "call": "nc_compute_forces(host q -> host F, U, W)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, tf, r, thr = oracle_sample(w, q, args.ref_sample)
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+               "sample": f"full O(N) DO cell build + pair loop of {args.ref_sample} random particles of C{args.config}, "
+                         f"extrapolated to one force evaluation ({tf:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
+            "config": {"workload": f"C{args.config}", "n_per_gpu": w.n, "variant": args.variant,
+                       "box": "KR planar elongation, eps=0.1, dt=0.002", "potential": "LJ rc=2.5 shifted",
+                       "precision": "fp32 storage + fp32 filter, fp64 interactions",
+                       "l2": "inputs (~7 GB) >> L2 (126 MB); no flush", "parallelism": f"replicas x{ws}"},
+            "particle_steps_per_s": psteps,
+            "interactions_per_particle": inter / w.n, "candidates_per_particle": cand / w.n,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_pairs",
+                         "kernel_ms": pairs_ms_avg,
+                         "peak_note": f"blend of FP32 {p32/1e12:.1f} and FP64 {p64/1e12:.1f} TFLOP/s at "
+                                      f"{fmax/1e6:.0f} MHz x {nsm} SMs for 9 flop/candidate (fp32) + 30 "
+                                      f"flop/interaction (fp64)"},
+            "kernel_ms_per_step": kernel_ms,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    cl.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def cl_box(cl):
+    n, L, t, _ = cl.get_state()
+    return L
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--variant", default="do", choices=["do", "ds"])
+    ap.add_argument("--ref-sample", type=int, default=200000)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

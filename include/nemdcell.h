@@ -1,0 +1,210 @@
+/*
+ * nemdcell.h -- C-ABI of the B200 (sm_100a) cell-list force path for
+ * nonequilibrium MD in a periodic box that deforms with a homogeneous
+ * linear flow, after arXiv 1412.3784 (Dobson, Fox, Saracino: "Cell list
+ * algorithms for nonequilibrium molecular dynamics").
+ *
+ * Library: paper_1412_3784_b200/libnemdcell.so.  Every entry point is
+ * extern "C", takes plain pointers and sizes, and returns an nc_status; no
+ * call throws or aborts across the ABI.  nc_last_error() gives the text of
+ * the last failure on a context.
+ *
+ * Citations: P:n = line n of the paper text; Eq. (k) numbered as
+ * in DESIGN.md section 1; Rn = reading n in DESIGN.md section 3 (where the
+ * paper is silent or ambiguous).
+ *
+ * Conventions shared by all calls
+ *  - Box matrix L: double[9], ROW-major, whose COLUMNS are the box vectors
+ *    v1, v2, v3 (Eq. 1).  det L > 0 is required.
+ *  - Positions q, momenta p, forces F: n x 3 contiguous, row-major, element
+ *    type float (NC_F32) or double (NC_F64) as chosen in nc_config.prec.
+ *    Pointers may be DEVICE memory (e.g. torch CUDA tensors; used in place)
+ *    or HOST memory (pageable or pinned; the library copies through its own
+ *    device buffers on cfg.stream).  The kind is detected per pointer.
+ *  - Arrays are in particle-id (gid) order at the ABI; internally the
+ *    library keeps particles sorted by (cell, gid) (R27).
+ *  - All GPU work is enqueued on cfg.stream (a cudaStream_t; NULL = the
+ *    legacy default stream).  Calls that return host values synchronize that
+ *    stream only.  One context per host thread; calls are not re-entrant.
+ *  - Ownership: the caller owns every pointer it passes; the library owns
+ *    all scratch and the resident particle state for the context lifetime.
+ *  - Units: epsilon = sigma = m = 1 are the usual choice; any positive
+ *    values are accepted.
+ */
+#ifndef NEMDCELL_H
+#define NEMDCELL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nc_ctx nc_ctx;
+
+/* The paper's two cell-list variants. */
+typedef enum {
+    NC_DS = 0, /* dynamic size: cells congruent to the box, c_k = floor(h_k/d_cut), 27 cells */
+    NC_DO = 1  /* dynamic offset: QR-rotated rectangular cells, l_k = floor(r_kk/d_cut), 27/30/34/36 */
+} nc_variant;
+
+/* Storage and pair-arithmetic precision.  NC_F32 keeps fp32 positions and
+ * evaluates pairs in fp32 with an fp64 re-check of every candidate whose
+ * fp32 r^2 lies within a relative band of r_c^2, so the pair SET is the
+ * canonical fp64 one (R16).  NC_F64 does everything in fp64. */
+typedef enum { NC_F32 = 0, NC_F64 = 1 } nc_prec;
+
+typedef enum {
+    NC_OK = 0,
+    NC_E_ARG = 1,        /* null pointer, n out of range, bad enum, unsupported pointer */
+    NC_E_BOX = 2,        /* det L <= 0 or a non-finite entry */
+    NC_E_DEGENERATE = 3, /* DS: some c_k < 3; DO: l1 < 4, l2 < 4 or l3 < 3 (R9).  No fallback. */
+    NC_E_FLOW = 4,       /* |tr A| > 1e-12 max(1, max|A_ij|): flow not incompressible */
+    NC_E_STATE = 5,      /* call order: no box / flow / state set yet */
+    NC_E_CUDA = 6,       /* a CUDA runtime error (text in nc_last_error) */
+    NC_E_NCCL = 7,       /* reserved for the multi-GPU slab path */
+    NC_E_OOM = 8,        /* n or the cell count exceeds what was allocated */
+    NC_E_NONFINITE = 9   /* a non-finite force, energy or virial was produced */
+} nc_status;
+
+/* Lattice remapping policies. */
+typedef enum {
+    NC_REMAP_NONE = 0, /* L_t = e^{At} L0 (Eq. 5) */
+    NC_REMAP_LE = 1,   /* Lees-Edwards: shear A = eps e1 e2^T, tilt kept in [-1/2,1/2) by M of Eq. (8) */
+    NC_REMAP_KR = 2,   /* Kraynik-Reinelt planar: L~ = e^{A (t mod t*)} L0 with e^{At*}L0 = L0 M (Eq. 9) */
+    NC_REMAP_GKR = 3   /* generalized KR, diagonal A: L~ = exp(diag(f1 w1 + f2 w2)) L0 (Eq. 10; R23) */
+} nc_remap_kind;
+
+typedef struct {
+    nc_remap_kind kind;
+    double L0[9];      /* reference basis at t = 0 (row-major, columns = box vectors) */
+    double tstar;      /* KR: period t* (> 0) */
+    double omega1[3];  /* GKR: log-eigenvalues of the first automorphism, in the axis order of L0 */
+    double omega2[3];  /* GKR: log-eigenvalues of the second automorphism */
+    double beta[2];    /* GKR: alpha_k(t) = beta_k * eps * t; f_k = alpha_k - floor(alpha_k + 1/2) */
+    double eps;        /* GKR: rate scale eps of A = eps diag(a) */
+} nc_remap;
+
+typedef struct {
+    nc_variant variant;
+    nc_prec prec;
+    double rc;         /* cutoff d_cut; the pair test is r^2 < rc^2 strictly (R10) */
+    double eps, sigma; /* LJ 12-6 parameters (R11) */
+    double u_shift;    /* energy shift: phi(r) = 4 eps((s/r)^12-(s/r)^6) - u_shift for r < rc.
+                          LJ: u_shift = phi_LJ(rc); WCA (rc = 2^(1/6) sigma): u_shift = -eps */
+    double mass;       /* particle mass m (SLLOD) */
+    int device;        /* CUDA device ordinal */
+    void *stream;      /* cudaStream_t for all work (NULL = default stream) */
+    int64_t capacity;  /* maximum particle count; buffers are allocated once in nc_create */
+    int64_t max_cells; /* maximum cell count over the run (0 = derive from capacity: 2*capacity + 4096) */
+} nc_config;
+
+/* Per-evaluation instrumentation (R28): from the last force evaluation. */
+typedef struct {
+    int64_t n;                 /* particles */
+    int32_t dims[3];           /* grid: c (DS) or l (DO) */
+    int64_t ncells;
+    double candidates;         /* (i, j, image) triples distance-checked, self excluded */
+    double interactions;       /* ordered pairs with r < rc (|P| in DESIGN.md) */
+    double stencil_cells;      /* sum over cells of the neighborhood size (mean = / ncells) */
+    double rechecks;           /* fp32 candidates re-decided in canonical fp64 (R16) */
+    double U;                  /* total potential energy */
+    double W[6];               /* configurational virial 1/2 sum fr d(x)d: xx,yy,zz,xy,xz,yz (R12) */
+    double acc_evals;          /* force evaluations since the last nc_profile(ctx, 1) */
+    double acc_interactions;   /* their summed interactions */
+    double acc_candidates;     /* their summed candidates */
+} nc_stats;
+
+/* Create a context on cfg->device; allocates all buffers for cfg->capacity
+ * particles.  *out receives the context (NULL on failure).  Errors: NC_E_ARG,
+ * NC_E_CUDA, NC_E_OOM. */
+nc_status nc_create(const nc_config *cfg, nc_ctx **out);
+
+/* Free the context and all device memory it owns (synchronizes its stream). */
+void nc_destroy(nc_ctx *ctx);
+
+/* Set the box L_t.  Recomputes the host geometry: L^{-1},
+ * heights h_k, DS counts c_k or the QR factor R,
+ * counts l_k and widths.  Errors: NC_E_BOX,
+ * NC_E_DEGENERATE, NC_E_OOM (more cells than max_cells). */
+nc_status nc_set_box(nc_ctx *ctx, const double L[9]);
+
+/* Set the flow matrix A (row-major) and the remap policy at time t;
+ * also sets the box to the policy's L~_t.  pol may be NULL (NC_REMAP_NONE
+ * with L0 = current box).  Errors: NC_E_FLOW, NC_E_ARG, NC_E_BOX,
+ * NC_E_DEGENERATE. */
+nc_status nc_set_flow(nc_ctx *ctx, const double A[9], const nc_remap *pol, double t);
+
+/* Wrap q into the unit cell Omega (R14, R15), compute cell keys
+ * and sort particles into cells by (cell, gid) (R27).
+ * q: n x 3 positions (device or host), read only -- the wrapped copy is kept
+ * internally and returned by nc_get_cells / nc_get_wrapped.  Errors:
+ * NC_E_ARG, NC_E_STATE (no box), NC_E_OOM, NC_E_CUDA. */
+nc_status nc_build_cells(nc_ctx *ctx, const void *q, int64_t n);
+
+/* One force evaluation (implies nc_build_cells): pair set by the chosen
+ * cell list, F_i = -sum fr d, U, W (R11, R12).
+ * F: n x 3 output (device or host), gid order, lab frame.  U, W: host
+ * outputs (may be NULL).  Synchronizes the stream.  Errors: as
+ * nc_build_cells, plus NC_E_NONFINITE. */
+nc_status nc_compute_forces(nc_ctx *ctx, const void *q, int64_t n, void *F, double *U, double W[6]);
+
+/* Load the resident particle state: positions q and PECULIAR momenta p
+ * (n x 3, device or host, R19), particle ids gid (int64, may be NULL for
+ * 0..n-1).  Computes the initial forces.  Errors: as nc_compute_forces. */
+nc_status nc_set_state(nc_ctx *ctx, const void *q, const void *p, const int64_t *gid, int64_t n);
+
+/* Advance the resident state by nsteps SLLOD velocity-Verlet steps of size
+ * dt (R19): kick + flow factor, drift with e^{A dt}, box update and remap
+ * (P:342, 349, 380, 428, 433), rewrap, cell rebuild, forces, flow
+ * factor + kick.  U, W (host, may be NULL) receive the values after the
+ * last step.  Errors: NC_E_STATE, NC_E_DEGENERATE, NC_E_NONFINITE,
+ * NC_E_CUDA. */
+nc_status nc_step_sllod(nc_ctx *ctx, double dt, int nsteps, double *U, double W[6]);
+
+/* Copy the resident state out in gid order: q, p (n x 3, device or host,
+ * may be NULL), gid (int64 host, may be NULL), the box L (host double[9],
+ * may be NULL) and time t (may be NULL).  *n receives the count. */
+nc_status nc_get_state(nc_ctx *ctx, void *q, void *p, int64_t *gid, int64_t *n, double L[9], double *t);
+
+/* Parity instrumentation from the last build: cell_of[gid] (int64 host, n),
+ * cell_start (int64 host, ncells+1), dims (int32[3]) and the wrapped
+ * positions in gid order (host, n x 3, storage precision).  Any may be NULL. */
+nc_status nc_get_cells(nc_ctx *ctx, int64_t *cell_of, int64_t *cell_start, int32_t dims[3], void *wrapped_q);
+
+/* Per-particle pair digests (gid order, host arrays of n): cnt_i = number
+ * of partners, hsum_i = sum mix64(key), hxor_i = xor mix64(key) with
+ * key = gid_j | (n1+8)<<32 | (n2+8)<<36 | (n3+8)<<40 and n the lattice image
+ * of the canonical displacement d = (q_j + L n) - q_i.  Runs a separate
+ * digest evaluation of the last built cells (not on the timed path). */
+nc_status nc_get_pair_digest(nc_ctx *ctx, uint32_t *cnt, uint64_t *hsum, uint64_t *hxor);
+
+/* Instrumentation of the last evaluation. */
+nc_status nc_get_stats(nc_ctx *ctx, nc_stats *out);
+
+/* Histogram of neighborhood sizes over all cells of the current box
+ * (index = size, 64 entries, host int64).  Runs a small kernel. */
+nc_status nc_get_stencil_histogram(nc_ctx *ctx, int64_t hist[64]);
+
+/* Live per-kernel timing with CUDA events recorded on cfg.stream around
+ * every launch of the path (enable = 1 starts a fresh accumulation, 0 stops).
+ * nc_profile_read synchronizes the stream and returns, per kernel id
+ * (NC_K_*), the summed device milliseconds and the launch counts. */
+enum { NC_K_WRAPKEY = 0, NC_K_SCAN = 1, NC_K_SCATTER = 2, NC_K_RANKGATHER = 3, NC_K_PAIRS = 4, NC_K_REDUCE = 5,
+       NC_K_KICK = 6, NC_K_OTHER = 7, NC_K_COUNT = 8 };
+nc_status nc_profile(nc_ctx *ctx, int enable);
+nc_status nc_profile_read(nc_ctx *ctx, double ms[8], int64_t counts[8]);
+
+/* Number of kernel launches this context has issued so far. */
+int64_t nc_launch_count(const nc_ctx *ctx);
+
+/* Text of the last error on ctx (or of the last nc_create failure if ctx is NULL). */
+const char *nc_last_error(const nc_ctx *ctx);
+
+/* Library version string. */
+const char *nc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEMDCELL_H */

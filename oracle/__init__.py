@@ -262,7 +262,7 @@ def evaluate(method: int, q, L, rc, eps=1.0, sigma=1.0, ushift=None, idx=None, p
     hxor = np.zeros(k, dtype=np.uint64) if dig else None
     pairs = np.zeros((max(pairs_cap, 1), 5), dtype=np.int32) if pairs_cap else None
     npairs = np.zeros(1, dtype=np.int64)
-    stats = np.zeros(5, dtype=np.int64)
+    stats = np.zeros(7, dtype=np.int64)
 
     def P(a):
         return _p(a) if a is not None else None
@@ -273,7 +273,8 @@ def evaluate(method: int, q, L, rc, eps=1.0, sigma=1.0, ushift=None, idx=None, p
     if st:
         raise ValueError({1: "bad box (P:32)", 2: "degenerate grid (R9)"}[st])
     r = Result(F=F, U_i=U, W_i=W, cnt=cnt, hsum=hsum, hxor=hxor, candidates=int(stats[0]),
-               interactions=int(stats[1]), dims=tuple(int(x) for x in stats[2:5]))
+               interactions=int(stats[1]), dims=tuple(int(x) for x in stats[2:5]),
+               t_build=stats[5] * 1e-9, t_eval=stats[6] * 1e-9)
     if U is not None:
         r["U"] = float(np.sum(U))
     if W is not None:

@@ -1,0 +1,925 @@
+// kernels.cuh -- sm_100a kernels of the cell-list force path (arXiv 1412.3784).
+//
+//   K1  k_wrap_key        : lambda = L^{-1} q (canonical fp64), wrap into Omega,
+//                           DS / DO cell key, fused histogram (atomic slot)
+//   K2  k_scan_*          : exclusive scan of the cell histogram -> cell_start
+//       k_scatter         : particle -> (cell, arrival slot) bucket
+//       k_rank_gather     : stable (cell, gid) order; gather q, p, gid and the
+//                           cell-local rotated coordinates u (+ DO home shift)
+//   K3  k_pairs           : warp-per-cell pair kernel: builds the 27 (DS) or
+//                           27/30/34/36 (DO) neighborhood on the fly, stages
+//                           the neighbor particles (image shift applied) in
+//                           shared memory, filters r^2 < r_c^2 into per-lane
+//                           queues, evaluates LJ/WCA for the queued pairs,
+//                           full i-side accumulation, no atomics
+//   K3r k_reduce_layers   : deterministic fixed-order reduction of partials
+//   K4  k_kick_drift_key  : SLLOD half kick + flow factor + drift, fused with K1
+//       k_kick            : SLLOD flow factor + half kick
+//
+// Canonical fp64 arithmetic (reading R16): every operation that decides an
+// integer (wrap, cell key, stencil rows/columns, pair membership in the
+// re-check band) uses explicit round-to-nearest intrinsics (__dmul_rn,
+// __dadd_rn, __ddiv_rn) in the association order of the definition, so no
+// FMA contraction can change a decision.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "geom.hpp"
+
+namespace nc {
+
+template <typename T> struct V4;
+template <> struct V4<float> { using t = float4; };
+template <> struct V4<double> { using t = double4; };
+
+__device__ __forceinline__ float4 mk4(float x, float y, float z, float w) { return make_float4(x, y, z, w); }
+__device__ __forceinline__ double4 mk4(double x, double y, double z, double w) { return make_double4(x, y, z, w); }
+
+// index <-> 4th component (bit pattern for fp32, exact value for fp64)
+__device__ __forceinline__ float idx_to_w(uint32_t i, float) { return __uint_as_float(i); }
+__device__ __forceinline__ double idx_to_w(uint32_t i, double) { return (double)i; }
+__device__ __forceinline__ uint32_t w_to_idx(float w) { return __float_as_uint(w); }
+__device__ __forceinline__ uint32_t w_to_idx(double w) { return (uint32_t)w; }
+
+__device__ __forceinline__ double round_to(double v, float) { return (double)__double2float_rn(v); }
+__device__ __forceinline__ double round_to(double v, double) { return v; }
+
+__device__ __forceinline__ int floordiv(int a, int b) {
+  int q = a / b;
+  if ((a % b) != 0 && ((a < 0) != (b < 0))) --q;
+  return q;
+}
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// canonical lambda_k = (Li_k0 q0 + Li_k1 q1) + Li_k2 q2
+__device__ __forceinline__ void frac_c(const Geom& g, double q0, double q1, double q2, double* lam) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    lam[k] = __dadd_rn(__dadd_rn(__dmul_rn(g.Li[3 * k], q0), __dmul_rn(g.Li[3 * k + 1], q1)),
+                       __dmul_rn(g.Li[3 * k + 2], q2));
+}
+
+// canonical lattice shift s_a = (L_a0 n0 + L_a1 n1) + L_a2 n2
+__device__ __forceinline__ double lshift_c(const Geom& g, int a, int n0, int n1, int n2) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(g.L[3 * a], (double)n0), __dmul_rn(g.L[3 * a + 1], (double)n1)),
+                   __dmul_rn(g.L[3 * a + 2], (double)n2));
+}
+
+// Cell of one particle from its fractional coordinates (P:668-672
+// with R1, R2, R14).  Returns the x-fastest cell id, the cell coordinates,
+// the DO home shift nh = (-kx, -ky, 0) and the rotated rearranged point.
+struct CellPos {
+  int a[3];
+  int nh0, nh1;
+  double xr[3];  // DO: rearranged rotated point (x', y', z); DS: unused
+};
+
+__device__ __forceinline__ uint32_t cell_of(const Geom& g, const double* lam, CellPos& cp) {
+  if (g.variant == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp.a[k] = clampi((int)floor(__dmul_rn(lam[k], (double)g.dims[k])), 0, g.dims[k] - 1);
+    cp.nh0 = cp.nh1 = 0;
+  } else {
+    double x = __dadd_rn(__dadd_rn(__dmul_rn(g.R[0], lam[0]), __dmul_rn(g.R[1], lam[1])), __dmul_rn(g.R[2], lam[2]));
+    double y = __dadd_rn(__dmul_rn(g.R[4], lam[1]), __dmul_rn(g.R[5], lam[2]));
+    double z = __dmul_rn(g.R[8], lam[2]);
+    double ky = floor(__ddiv_rn(y, g.R[4]));
+    double yp = __dsub_rn(y, __dmul_rn(ky, g.R[4]));
+    double xpp = __dsub_rn(x, __dmul_rn(ky, g.R[1]));
+    double kx = floor(__ddiv_rn(xpp, g.R[0]));
+    double xp = __dsub_rn(xpp, __dmul_rn(kx, g.R[0]));
+    cp.a[0] = clampi((int)floor(__ddiv_rn(xp, g.w[0])), 0, g.dims[0] - 1);
+    cp.a[1] = clampi((int)floor(__ddiv_rn(yp, g.w[1])), 0, g.dims[1] - 1);
+    cp.a[2] = clampi((int)floor(__ddiv_rn(z, g.w[2])), 0, g.dims[2] - 1);
+    cp.nh0 = -(int)kx;
+    cp.nh1 = -(int)ky;
+    cp.xr[0] = xp;
+    cp.xr[1] = yp;
+    cp.xr[2] = z;
+  }
+  return (uint32_t)cp.a[0] + (uint32_t)g.dims[0] * ((uint32_t)cp.a[1] + (uint32_t)g.dims[1] * (uint32_t)cp.a[2]);
+}
+
+// Cell-local coordinates in the QR-rotated frame (not canonical: they only
+// feed the fp32/fp64 distance filter and the forces).  DS: u = R(lambda - a/c);
+// DO: u = (x' - a0 w0, y' - a1 w1, z - a2 w2).
+__device__ __forceinline__ void local_u(const Geom& g, const double* lam, const CellPos& cp, double* u) {
+  if (g.variant == 0) {
+    double m0 = lam[0] - (double)cp.a[0] * g.cinv[0];
+    double m1 = lam[1] - (double)cp.a[1] * g.cinv[1];
+    double m2 = lam[2] - (double)cp.a[2] * g.cinv[2];
+    u[0] = g.R[0] * m0 + g.R[1] * m1 + g.R[2] * m2;
+    u[1] = g.R[4] * m1 + g.R[5] * m2;
+    u[2] = g.R[8] * m2;
+  } else {
+    u[0] = cp.xr[0] - (double)cp.a[0] * g.w[0];
+    u[1] = cp.xr[1] - (double)cp.a[1] * g.w[1];
+    u[2] = cp.xr[2] - (double)cp.a[2] * g.w[2];
+  }
+}
+
+__device__ __forceinline__ uint32_t pack_nh(int nh0, int nh1) {
+  return ((uint32_t)(nh0 & 0xffff)) | ((uint32_t)(nh1 & 0xffff) << 16);
+}
+__device__ __forceinline__ int nh_x(uint32_t p) { return (int)(int16_t)(p & 0xffff); }
+__device__ __forceinline__ int nh_y(uint32_t p) { return (int)(int16_t)(p >> 16); }
+
+// ---------------------------------------------------------------------------
+// K1: wrap + key + histogram.  qin: n x stride (stride 3 = caller layout,
+// 4 = internal).  Stored (wrapped, rounded to T) positions go to qout.
+// Wrap rule (R14, R15): if lambda outside [0,1)^3, q <- round_T(q - L floor(lambda))
+// once; keys from the stored value, clamped.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ uint32_t wrap_key_one(const Geom& g, double& q0, double& q1, double& q2) {
+  double lam[3];
+  frac_c(g, q0, q1, q2, lam);
+  if (lam[0] < 0.0 || lam[0] >= 1.0 || lam[1] < 0.0 || lam[1] >= 1.0 || lam[2] < 0.0 || lam[2] >= 1.0) {
+    int n0 = (int)floor(lam[0]), n1 = (int)floor(lam[1]), n2 = (int)floor(lam[2]);
+    q0 = round_to(__dsub_rn(q0, lshift_c(g, 0, n0, n1, n2)), T());
+    q1 = round_to(__dsub_rn(q1, lshift_c(g, 1, n0, n1, n2)), T());
+    q2 = round_to(__dsub_rn(q2, lshift_c(g, 2, n0, n1, n2)), T());
+    frac_c(g, q0, q1, q2, lam);
+  }
+  CellPos cp;
+  return cell_of(g, lam, cp);
+}
+
+template <typename T>
+__global__ void k_wrap_key(int64_t n, const T* __restrict__ qin, int stride, typename V4<T>::t* __restrict__ qout,
+                           uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
+                           const __grid_constant__ Geom g) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q0 = (double)qin[i * stride], q1 = (double)qin[i * stride + 1], q2 = (double)qin[i * stride + 2];
+  uint32_t c = wrap_key_one<T>(g, q0, q1, q2);
+  qout[i] = mk4((T)q0, (T)q1, (T)q2, (T)0);
+  key[i] = c;
+  slot[i] = atomicAdd(&counts[c], 1u);
+}
+
+// ---------------------------------------------------------------------------
+// K2: exclusive scan (3 phases, deterministic: integer counts).
+// ---------------------------------------------------------------------------
+constexpr int SCAN_T = 256, SCAN_E = 8, SCAN_TILE = SCAN_T * SCAN_E;
+
+__global__ void k_scan_reduce(const uint32_t* __restrict__ in, int64_t m, uint32_t* __restrict__ bsum) {
+  __shared__ uint32_t s[SCAN_T / 32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  uint32_t acc = 0;
+  for (int k = 0; k < SCAN_E; ++k) {
+    int64_t idx = base + (int64_t)k * SCAN_T + threadIdx.x;
+    if (idx < m) acc += in[idx];
+  }
+  acc = __reduce_add_sync(0xffffffffu, acc);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < SCAN_T / 32; ++w) t += s[w];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// single block: exclusive scan of nb block sums in place; total to *tot
+__global__ void k_scan_bsums(uint32_t* __restrict__ bsum, int64_t nb, uint32_t* __restrict__ tot) {
+  __shared__ uint32_t carry_s;
+  __shared__ uint32_t wsum[32];
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += blockDim.x) {
+    int64_t idx = base + threadIdx.x;
+    uint32_t v = idx < nb ? bsum[idx] : 0u;
+    uint32_t x = v;
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t ws = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += y;
+      }
+      wsum[lane] = ws;
+    }
+    __syncthreads();
+    uint32_t excl = carry_s + (wid > 0 ? wsum[wid - 1] : 0u) + x - v;
+    if (idx < nb) bsum[idx] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s += wsum[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *tot = carry_s;
+}
+
+// out[i] = exclusive prefix of in; out[m] = total (out has m+1 entries)
+__global__ void k_scan_apply(const uint32_t* __restrict__ in, int64_t m, const uint32_t* __restrict__ bsum,
+                             uint32_t* __restrict__ out, const uint32_t* __restrict__ tot) {
+  __shared__ uint32_t wsum[SCAN_T / 32];
+  __shared__ uint32_t carry_s;
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = bsum[blockIdx.x];
+  __syncthreads();
+  // each thread owns SCAN_E consecutive elements
+  int64_t my0 = base + (int64_t)threadIdx.x * SCAN_E;
+  uint32_t v[SCAN_E], s = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_E; ++k) {
+    v[k] = (my0 + k < m) ? in[my0 + k] : 0u;
+    s += v[k];
+  }
+  uint32_t x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < SCAN_T / 32; ++w) {
+      uint32_t c = wsum[w];
+      wsum[w] = t;
+      t += c;
+    }
+  }
+  __syncthreads();
+  uint32_t run = carry_s + wsum[wid] + x - s;
+#pragma unroll
+  for (int k = 0; k < SCAN_E; ++k) {
+    if (my0 + k < m) out[my0 + k] = run;
+    run += v[k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[m] = *tot;
+}
+
+// bucket each particle at (cell_start[key] + arrival slot); carry its gid
+__global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
+                          const uint32_t* __restrict__ cs, const uint32_t* __restrict__ gid_in,
+                          uint32_t* __restrict__ tmp, uint32_t* __restrict__ tmpgid) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t pos = cs[key[i]] + slot[i];
+  tmp[pos] = (uint32_t)i;
+  tmpgid[pos] = gid_in ? gid_in[i] : (uint32_t)i;
+}
+
+// Stable (cell, gid) order (R27): the destination of bucket entry s is
+// cell_start + #{members with smaller gid}.  Gathers q (stored), p, gid and
+// writes the cell-local rotated coordinates u (4th component = sorted index)
+// and the packed DO home shift.
+template <typename T>
+__global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ tmpgid,
+                              const uint32_t* __restrict__ key, const uint32_t* __restrict__ cs,
+                              const typename V4<T>::t* __restrict__ qw, const typename V4<T>::t* __restrict__ p_in,
+                              typename V4<T>::t* __restrict__ q_out, typename V4<T>::t* __restrict__ p_out,
+                              uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
+                              uint32_t* __restrict__ nh_out, const __grid_constant__ Geom g) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t i = tmp[s];
+  uint32_t c = key[i];
+  uint32_t c0 = cs[c], c1 = cs[c + 1];
+  uint32_t gg = tmpgid[s];
+  uint32_t rank = 0;
+  for (uint32_t t = c0; t < c1; ++t) rank += (tmpgid[t] < gg) ? 1u : 0u;
+  uint32_t dst = c0 + rank;
+  typename V4<T>::t q = qw[i];
+  double lam[3];
+  frac_c(g, (double)q.x, (double)q.y, (double)q.z, lam);
+  CellPos cp;
+  cell_of(g, lam, cp);
+  double u[3];
+  local_u(g, lam, cp, u);
+  q_out[dst] = q;
+  if (p_in) p_out[dst] = p_in[i];
+  gid_out[dst] = gg;
+  u_out[dst] = make_double4(u[0], u[1], u[2], (double)dst);
+  nh_out[dst] = pack_nh(cp.nh0, cp.nh1);
+}
+
+// ---------------------------------------------------------------------------
+// K3: the pair kernel.
+//
+// Precision design: the candidate FILTER runs in the
+// storage type T (fp32 in NC_F32 mode: ~85% of candidates are rejected there);
+// every candidate that passes is re-evaluated from fp64 cell-local coordinates
+// (error ~1e-16 |d|) and its force, energy and virial are computed and
+// accumulated in fp64.  Membership is decided by the fp64 r^2, and inside a
+// 1e-12 relative band around r_c^2 by the canonical fp64 test of R16.
+// ---------------------------------------------------------------------------
+constexpr int K3_WARPS = 4;
+constexpr int K3_CAP = 256;     // staged neighbor particles per warp per chunk
+constexpr int K3_QCAP = 24;     // per-lane queue of filter survivors
+constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
+constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, nonfinite
+constexpr double K3_BAND64 = 1e-12;
+
+template <typename T>
+struct K3Stage64 {  // fp32 mode: fp64 copy of the staged rotated cell-local coordinates
+  double x[K3_CAP], y[K3_CAP], z[K3_CAP];
+};
+template <>
+struct K3Stage64<double> {  // fp64 mode: stage holds LAB positions; packed DO home shift of each j
+  uint32_t nh[K3_CAP];
+};
+
+template <typename T>
+struct K3Smem {
+  typename V4<T>::t stage[K3_CAP];  // filter copy, .w = sorted index
+  K3Stage64<T> s64;
+  uint16_t queue[K3_QCAP][32];
+  uint8_t sent[K3_CAP];
+  uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
+  int32_t e_n[K3_MAXE][3];
+  double e_B[K3_MAXE][3];
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Build the neighborhood of center cell (a0,a1,a2) into smem; returns the
+// entry count (warp-uniform).  DS: 27 cells m = a + delta wrapped with
+// n_k = floor(m_k/c_k); bracket B = R(delta/c).  DO: exact
+// interval overlap (R3-R5), bracket
+// B = ((col-a0) w0 + n1 e0 + n2 r12 + n3 r13, (m-a1) w1 + n2 e1 + n3 r23, dz w2 + n3 e2).
+template <typename T>
+__device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int a2, K3Smem<T>& sm, int lane) {
+  const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
+  if (g.variant == 0) {
+    if (lane < 27) {
+      int d0 = lane % 3 - 1, d1 = (lane / 3) % 3 - 1, d2 = lane / 9 - 1;
+      int m0 = a0 + d0, m1 = a1 + d1, m2 = a2 + d2;
+      int n0 = floordiv(m0, l1), n1 = floordiv(m1, l2), n2 = floordiv(m2, l3);
+      m0 -= n0 * l1; m1 -= n1 * l2; m2 -= n2 * l3;
+      uint32_t cell = (uint32_t)m0 + (uint32_t)l1 * ((uint32_t)m1 + (uint32_t)l2 * (uint32_t)m2);
+      sm.e_start[lane] = cell;  // the cell id until the counts pass replaces it
+      sm.e_n[lane][0] = n0; sm.e_n[lane][1] = n1; sm.e_n[lane][2] = n2;
+      double u0 = (double)d0 * g.cinv[0], u1 = (double)d1 * g.cinv[1], u2 = (double)d2 * g.cinv[2];
+      sm.e_B[lane][0] = g.R[0] * u0 + g.R[1] * u1 + g.R[2] * u2;
+      sm.e_B[lane][1] = g.R[4] * u1 + g.R[5] * u2;
+      sm.e_B[lane][2] = g.R[8] * u2;
+    }
+    __syncwarp();
+    return 27;
+  }
+  // DO: lanes 0..11 = (layer dz, row index ri)
+  int ncols = 0, c0 = 0, m = 0, n2 = 0, n3 = 0, kd = 0, jd = 0, dz = 0;
+  if (lane < 12) {
+    dz = lane / 4 - 1;
+    int ri = lane % 4;
+    int kk = a2 + dz;
+    n3 = floordiv(kk, l3);
+    kd = kk - n3 * l3;
+    double oy = __dmul_rn((double)n3, g.d32);
+    int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
+    int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
+    if (ri < m1 - m0) {
+      m = m0 + ri;
+      n2 = floordiv(m, l2);
+      jd = m - n2 * l2;
+      double ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
+      c0 = (int)floor(__dsub_rn((double)(a0 - 1), ox));
+      int c1 = (int)ceil(__dsub_rn((double)(a0 + 2), ox));
+      ncols = c1 - c0;
+    }
+  }
+  int x = ncols;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  int total = __shfl_sync(0xffffffffu, x, 15);
+  int off = x - ncols;
+  for (int t = 0; t < ncols; ++t) {
+    int col = c0 + t;
+    int n1 = floordiv(col, l1);
+    int id = col - n1 * l1;
+    int e = off + t;
+    sm.e_start[e] = (uint32_t)id + (uint32_t)l1 * ((uint32_t)jd + (uint32_t)l2 * (uint32_t)kd);
+    sm.e_n[e][0] = n1; sm.e_n[e][1] = n2; sm.e_n[e][2] = n3;
+    sm.e_B[e][0] = (double)(col - a0) * g.w[0] + (double)n1 * g.e[0] + (double)n2 * g.R[1] + (double)n3 * g.R[2];
+    sm.e_B[e][1] = (double)(m - a1) * g.w[1] + (double)n2 * g.e[1] + (double)n3 * g.R[5];
+    sm.e_B[e][2] = (double)dz * g.w[2] + (double)n3 * g.e[2];
+  }
+  __syncwarp();
+  return total;
+}
+
+struct Acc {
+  double fx, fy, fz, u, w0, w1, w2, w3, w4, w5;
+  uint32_t cnt, nrc;
+  uint64_t hs, hx;
+};
+
+// canonical fp64 membership test of the pair (i, j, n) (R16): only for the
+// pairs whose fp64 r^2 lies within 1e-12 r_c^2 of the cutoff.
+template <typename T>
+__device__ __noinline__ bool canonical_in(const Geom& g, const typename V4<T>::t* qs, uint32_t i, uint32_t j, int n0,
+                                          int n1, int n2) {
+  typename V4<T>::t qi = qs[i];
+  typename V4<T>::t qj = qs[j];
+  double d0 = __dsub_rn(__dadd_rn((double)qj.x, lshift_c(g, 0, n0, n1, n2)), (double)qi.x);
+  double d1 = __dsub_rn(__dadd_rn((double)qj.y, lshift_c(g, 1, n0, n1, n2)), (double)qi.y);
+  double d2 = __dsub_rn(__dadd_rn((double)qj.z, lshift_c(g, 2, n0, n1, n2)), (double)qi.z);
+  double r2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+  return r2 < g.rc2;
+}
+
+template <typename T>
+struct PairCtx {
+  double ux, uy, uz;   // i: fp32 mode = rotated cell-local fp64; fp64 mode = lab position
+  T fx, fy, fz;        // i cell-local, filter precision (fp32 mode)
+  uint32_t my;         // i sorted index
+  T hi;                // fp32 filter bound on r^2 (superset of the pair set)
+  double lo64, hi64;   // band on the fp64 r^2 where the canonical test decides
+  const typename V4<T>::t* qs;
+  const uint32_t* nh;
+  const uint32_t* gid;
+  uint32_t nh_i;
+};
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+// d_a = (q_j + L n) - q_i without intermediate rounding (error-free
+// transformations; one final rounding): the fp64-mode force displacement.
+__device__ __forceinline__ double exact_d(const Geom& g, int a, double qj, double qi, int n0, int n1, int n2) {
+  double p0 = __dmul_rn(g.L[3 * a], (double)n0), p1 = __dmul_rn(g.L[3 * a + 1], (double)n1),
+         p2 = __dmul_rn(g.L[3 * a + 2], (double)n2);
+  double e0 = __fma_rn(g.L[3 * a], (double)n0, -p0), f1 = __fma_rn(g.L[3 * a + 1], (double)n1, -p1),
+         f2 = __fma_rn(g.L[3 * a + 2], (double)n2, -p2);
+  double s1, c1, s2, c2, s3, c3, s4, c4;
+  two_sum(qj, -qi, s1, c1);
+  two_sum(s1, p0, s2, c2);
+  two_sum(s2, p1, s3, c3);
+  two_sum(s3, p2, s4, c4);
+  return s4 + (((c1 + c2) + (c3 + c4)) + ((e0 + f1) + f2));
+}
+
+// canonical membership r^2 of (i, j, n) (R16)
+__device__ __forceinline__ double canonical_r2(const Geom& g, double qj0, double qj1, double qj2, double qi0,
+                                               double qi1, double qi2, int n0, int n1, int n2) {
+  double d0 = __dsub_rn(__dadd_rn(qj0, lshift_c(g, 0, n0, n1, n2)), qi0);
+  double d1 = __dsub_rn(__dadd_rn(qj1, lshift_c(g, 1, n0, n1, n2)), qi1);
+  double d2 = __dsub_rn(__dadd_rn(qj2, lshift_c(g, 2, n0, n1, n2)), qi2);
+  return __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+}
+
+// image of staged element t relative to particle i: n_cross + nh_j - nh_i (DS: n_cross)
+template <typename T>
+__device__ __forceinline__ void image_of(const Geom& g, const K3Smem<T>& sm, uint32_t t, uint32_t nh_j, uint32_t nh_i,
+                                         int& n0, int& n1, int& n2) {
+  int e = sm.sent[t];
+  n0 = sm.e_n[e][0]; n1 = sm.e_n[e][1]; n2 = sm.e_n[e][2];
+  if (g.variant == 1) {
+    n0 += nh_x(nh_j) - nh_x(nh_i);
+    n1 += nh_y(nh_j) - nh_y(nh_i);
+  }
+}
+
+__device__ __forceinline__ void lj_accumulate(const Geom& g, Acc& acc, double dx, double dy, double dz, double r2) {
+  // 1/r^2: fp32 seed + two Newton steps in fp64
+  double ir2 = (double)__frcp_rn((float)r2);
+  ir2 = ir2 * (2.0 - r2 * ir2);
+  ir2 = ir2 * (2.0 - r2 * ir2);
+  double s2 = g.sig2 * ir2;
+  double s6 = s2 * s2 * s2;
+  double fr = 24.0 * g.eps * s6 * (2.0 * s6 - 1.0) * ir2;
+  acc.fx -= fr * dx; acc.fy -= fr * dy; acc.fz -= fr * dz;
+  acc.u += 0.5 * (4.0 * g.eps * s6 * (s6 - 1.0) - g.ushift);
+  double hf = 0.5 * fr;
+  acc.w0 += hf * dx * dx; acc.w1 += hf * dy * dy; acc.w2 += hf * dz * dz;
+  acc.w3 += hf * dx * dy; acc.w4 += hf * dx * dz; acc.w5 += hf * dy * dz;
+  acc.cnt++;
+}
+
+template <bool DIGEST>
+__device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32_t j, int n0, int n1, int n2) {
+  if (DIGEST) {
+    uint64_t key = (uint64_t)gid[j] | ((uint64_t)(n0 + 8) << 32) | ((uint64_t)(n1 + 8) << 36) |
+                   ((uint64_t)(n2 + 8) << 40);
+    uint64_t h = mix64(key);
+    acc.hs += h;
+    acc.hx ^= h;
+  }
+}
+
+// Evaluate the queued filter survivors of every lane (warp-uniform loop).
+template <typename T, bool DIGEST>
+__device__ __forceinline__ void eval_queue(const Geom& g, const PairCtx<T>& pc, K3Smem<T>& sm, Acc& acc, int qlen,
+                                           int lane) {
+  int qmax = __reduce_max_sync(0xffffffffu, qlen);
+  for (int k = 0; k < qmax; ++k) {
+    if (k < qlen) {
+      uint32_t t = sm.queue[k][lane];
+      if constexpr (sizeof(T) == 4) {
+        uint32_t j = w_to_idx(sm.stage[t].w);
+        double dx = sm.s64.x[t] - pc.ux, dy = sm.s64.y[t] - pc.uy, dz = sm.s64.z[t] - pc.uz;
+        double r2 = dx * dx + dy * dy + dz * dz;
+        bool ok = (j != pc.my) && (r2 < pc.hi64);
+        int n0 = 0, n1 = 0, n2 = 0;
+        if (ok && (DIGEST || r2 >= pc.lo64)) {
+          image_of<T>(g, sm, t, g.variant == 1 ? pc.nh[j] : 0u, pc.nh_i, n0, n1, n2);
+          if (r2 >= pc.lo64) {
+            ok = canonical_in<T>(g, pc.qs, pc.my, j, n0, n1, n2);
+            acc.nrc++;
+          }
+        }
+        if (ok) {
+          lj_accumulate(g, acc, dx, dy, dz, r2);
+          digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
+        }
+      } else {
+        // fp64 mode: the filter already applied the canonical test; exact d for the force
+        typename V4<T>::t v = sm.stage[t];
+        uint32_t j = w_to_idx(v.w);
+        int n0, n1, n2;
+        image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
+        double dx = exact_d(g, 0, v.x, pc.ux, n0, n1, n2);
+        double dy = exact_d(g, 1, v.y, pc.uy, n0, n1, n2);
+        double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
+        double r2 = dx * dx + dy * dy + dz * dz;
+        lj_accumulate(g, acc, dx, dy, dz, r2);
+        digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
+      }
+    }
+  }
+}
+
+// One filter step for staged element t (valid lanes only): true if (i, t) may interact.
+template <typename T>
+__device__ __forceinline__ bool filter_one(const Geom& g, const PairCtx<T>& pc, const K3Smem<T>& sm, uint32_t t) {
+  typename V4<T>::t v = sm.stage[t];
+  if constexpr (sizeof(T) == 4) {
+    T dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
+    T r2 = dx * dx + dy * dy + dz * dz;
+    return r2 < pc.hi;
+  } else {
+    int n0, n1, n2;
+    image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
+    double r2 = canonical_r2(g, v.x, v.y, v.z, pc.ux, pc.uy, pc.uz, n0, n1, n2);
+    return r2 < g.rc2 && w_to_idx(v.w) != pc.my;
+  }
+}
+
+__device__ __forceinline__ double shfl_comb(double x, int src, bool take) {
+  double y = __shfl_sync(0xffffffffu, x, src);
+  return take ? x + y : x;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per center cell; blocks never span a cell layer (deterministic
+// layer-ordered partials).  grid = l3 * blocks_per_layer.
+template <typename T, bool DIGEST>
+__global__ void __launch_bounds__(K3_WARPS * 32)
+k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
+        const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
+        typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
+        uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  K3Smem<T>& sm = reinterpret_cast<K3Smem<T>*>(smraw)[warp];
+  __shared__ double wpart[K3_WARPS][NPART];
+
+  const int l1 = g.dims[0], l2 = g.dims[1];
+  const int layer = blockIdx.x / bpl;
+  const int chunk = blockIdx.x - layer * bpl;
+  const int per_layer = l1 * l2;
+  const int cbeg = chunk * cpb;
+  const int cend = min(per_layer, cbeg + cpb);
+
+  PairCtx<T> pc;
+  pc.hi = (T)g.band_hi;
+  pc.lo64 = g.rc2 * (1.0 - K3_BAND64);
+  pc.hi64 = g.rc2 * (1.0 + K3_BAND64);
+  pc.qs = qs;
+  pc.nh = nh;
+  pc.gid = gid;
+
+  double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+
+  for (int cl = cbeg + warp; cl < cend; cl += K3_WARPS) {
+    const int a0 = cl % l1, a1 = cl / l1, a2 = layer;
+    const uint32_t cid = (uint32_t)cl + (uint32_t)per_layer * (uint32_t)layer;
+    const int nst = build_entries<T>(g, a0, a1, a2, sm, lane);
+    // entry sizes and staging offsets (exclusive scan over <= 36 entries)
+    uint32_t tot = 0;
+    for (int e0 = 0; e0 < nst; e0 += 32) {
+      int e = e0 + lane;
+      uint32_t cnt = 0, st = 0;
+      if (e < nst) {
+        uint32_t cell = sm.e_start[e];
+        st = cs[cell];
+        cnt = cs[cell + 1] - st;
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      __syncwarp();
+      if (e < nst) {
+        sm.e_start[e] = st;
+        sm.e_cnt[e] = cnt;
+        sm.e_off[e] = tot + x - cnt;
+      }
+      tot += __shfl_sync(0xffffffffu, x, 31);
+    }
+    __syncwarp();
+    tS += (double)nst;
+    const uint32_t ibase = cs[cid];
+    const int ni = (int)(cs[cid + 1] - ibase);
+    if (ni == 0) continue;
+    tC += (double)ni * (double)tot - (double)ni;
+
+    for (int ib = 0; ib < ni; ib += 32) {
+      const int nb = min(32, ni - ib);
+      const int S = 32 / nb;               // streams over the j list
+      const int il = lane % nb, s = lane / nb;
+      const bool act = s < S;
+      pc.my = ibase + ib + il;
+      if constexpr (sizeof(T) == 4) {
+        double4 ui = u[pc.my];
+        pc.ux = ui.x; pc.uy = ui.y; pc.uz = ui.z;
+        pc.fx = (T)ui.x; pc.fy = (T)ui.y; pc.fz = (T)ui.z;
+      } else {
+        typename V4<T>::t qi = qs[pc.my];
+        pc.ux = qi.x; pc.uy = qi.y; pc.uz = qi.z;
+      }
+      pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
+      Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+
+      int e0 = 0;
+      while (e0 < nst) {
+        const uint32_t base_off = sm.e_off[e0];
+        int e1 = e0;
+        for (int eb = e0; eb < nst; eb += 32) {
+          int e = eb + lane;
+          bool fits = e < nst && (sm.e_off[e] + sm.e_cnt[e] - base_off) <= (uint32_t)K3_CAP;
+          int nfit = __popc(__ballot_sync(0xffffffffu, fits));  // the fitting entries are a prefix
+          e1 = eb + nfit;
+          if (nfit < 32) break;
+        }
+        if (e1 == e0) e1 = e0 + 1;  // unreachable: a cell holds fewer than K3_CAP particles
+        const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
+        // stage: lane-per-entry, loop over the entry's particles; image shift B applied in fp64
+        for (int eb = e0; eb < e1; eb += 32) {
+          int e = eb + lane;
+          uint32_t cnt = 0, st = 0, dst = 0;
+          double B0 = 0, B1 = 0, B2 = 0;
+          if (e < e1) {
+            cnt = sm.e_cnt[e]; st = sm.e_start[e]; dst = sm.e_off[e] - base_off;
+            B0 = sm.e_B[e][0]; B1 = sm.e_B[e][1]; B2 = sm.e_B[e][2];
+          }
+          uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
+          for (uint32_t t = 0; t < cmax; ++t) {
+            if (t < cnt) {
+              if constexpr (sizeof(T) == 4) {
+                double4 v = u[st + t];
+                double x = v.x + B0, y = v.y + B1, z = v.z + B2;
+                sm.stage[dst + t] = mk4((T)x, (T)y, (T)z, idx_to_w(st + t, T()));
+                sm.s64.x[dst + t] = x; sm.s64.y[dst + t] = y; sm.s64.z[dst + t] = z;
+              } else {
+                typename V4<T>::t v = qs[st + t];
+                sm.stage[dst + t] = mk4(v.x, v.y, v.z, idx_to_w(st + t, T()));
+                sm.s64.nh[dst + t] = g.variant == 1 ? nh[st + t] : 0u;
+              }
+              sm.sent[dst + t] = (uint8_t)e;
+            }
+          }
+        }
+        __syncwarp();
+        // filter: stream s takes t = s, s+S, ...; all lanes run the same trip count
+        const int iters = (int)((ctot + S - 1) / S);
+        int qlen = 0;
+        int it = 0;
+        for (; it + 4 <= iters; it += 4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t t = (uint32_t)(s + (it + k) * S);
+            bool valid = act && t < ctot;
+            bool hit = filter_one<T>(g, pc, sm, valid ? t : 0u);
+            sm.queue[qlen][lane] = (uint16_t)t;
+            qlen += (valid && hit) ? 1 : 0;
+          }
+          if (__any_sync(0xffffffffu, qlen > K3_QCAP - 4)) {
+            eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
+            qlen = 0;
+          }
+        }
+        for (; it < iters; ++it) {
+          uint32_t t = (uint32_t)(s + it * S);
+          bool valid = act && t < ctot;
+          bool hit = filter_one<T>(g, pc, sm, valid ? t : 0u);
+          sm.queue[qlen][lane] = (uint16_t)t;
+          qlen += (valid && hit) ? 1 : 0;
+        }
+        eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
+        __syncwarp();
+        e0 = e1;
+      }
+
+      // combine the S streams of each i (fixed order s = 1, 2, ...)
+      for (int s2 = 1; s2 < S; ++s2) {
+        int src = lane + s2 * nb;
+        bool take = (s == 0) && (src < 32);
+        src &= 31;
+        acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
+        acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
+        acc.w0 = shfl_comb(acc.w0, src, take); acc.w1 = shfl_comb(acc.w1, src, take);
+        acc.w2 = shfl_comb(acc.w2, src, take); acc.w3 = shfl_comb(acc.w3, src, take);
+        acc.w4 = shfl_comb(acc.w4, src, take); acc.w5 = shfl_comb(acc.w5, src, take);
+        uint32_t c2 = __shfl_sync(0xffffffffu, acc.cnt, src);
+        uint32_t r2c = __shfl_sync(0xffffffffu, acc.nrc, src);
+        if (take) { acc.cnt += c2; acc.nrc += r2c; }
+        if (DIGEST) {
+          uint64_t h1 = __shfl_sync(0xffffffffu, acc.hs, src);
+          uint64_t h2 = __shfl_sync(0xffffffffu, acc.hx, src);
+          if (take) { acc.hs += h1; acc.hx ^= h2; }
+        }
+      }
+      const bool owner = (s == 0);
+      if (owner) {
+        double Fx = acc.fx, Fy = acc.fy, Fz = acc.fz;
+        if constexpr (sizeof(T) == 4) {  // lab-frame force F = Q F_rot
+          Fx = g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz;
+          Fy = g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz;
+          Fz = g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz;
+        }
+        Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, (T)0);
+        if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
+      }
+      double fchk = owner ? acc.fx + acc.fy + acc.fz + acc.u : 0.0;
+      tU += warp_sum_d(owner ? acc.u : 0.0);
+      tW[0] += warp_sum_d(owner ? acc.w0 : 0.0); tW[1] += warp_sum_d(owner ? acc.w1 : 0.0);
+      tW[2] += warp_sum_d(owner ? acc.w2 : 0.0); tW[3] += warp_sum_d(owner ? acc.w3 : 0.0);
+      tW[4] += warp_sum_d(owner ? acc.w4 : 0.0); tW[5] += warp_sum_d(owner ? acc.w5 : 0.0);
+      tI += warp_sum_d(owner ? (double)acc.cnt : 0.0);
+      tR += warp_sum_d(owner ? (double)acc.nrc : 0.0);
+      tNF += warp_sum_d(isfinite(fchk) ? 0.0 : 1.0);
+    }
+  }
+  if (lane == 0) {
+    double* wp = wpart[warp];
+    wp[0] = tU;
+    for (int k = 0; k < 6; ++k) wp[1 + k] = tW[k];
+    wp[7] = tI; wp[8] = tC; wp[9] = tS; wp[10] = tR; wp[11] = tNF;
+  }
+  __syncthreads();
+  if (threadIdx.x < NPART) {
+    double v = 0;
+    for (int w = 0; w < K3_WARPS; ++w) v += wpart[w][threadIdx.x];
+    bpart[(int64_t)blockIdx.x * NPART + threadIdx.x] = v;
+  }
+}
+
+// K3r: per-layer partials in block order, then the total in layer order.
+__global__ void k_reduce_layers(const double* __restrict__ bpart, int bpl, int nlayers, double* __restrict__ lpart) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nlayers * NPART) return;
+  int layer = k / NPART, c = k % NPART;
+  double v = 0;
+  const double* p = bpart + (int64_t)layer * bpl * NPART + c;
+  for (int b = 0; b < bpl; ++b) v += p[(int64_t)b * NPART];
+  lpart[k] = v;
+}
+
+// total in layer order; also accumulates into acc[0..NPART) and counts evaluations in acc[NPART]
+__global__ void k_reduce_total(const double* __restrict__ lpart, int nlayers, double* __restrict__ tot,
+                               double* __restrict__ acc) {
+  int c = threadIdx.x;
+  if (c > NPART) return;
+  if (c == NPART) { acc[NPART] += 1.0; return; }
+  double v = 0;
+  for (int l = 0; l < nlayers; ++l) v += lpart[(int64_t)l * NPART + c];
+  tot[c] = v;
+  acc[c] += v;
+}
+
+// neighborhood-size histogram (instrumentation): one warp per block
+__global__ void __launch_bounds__(32) k_stencil_hist(const __grid_constant__ Geom g, unsigned long long* __restrict__ hist) {
+  __shared__ K3Smem<float> tab;
+  __shared__ unsigned int h[64];
+  int lane = threadIdx.x & 31;
+  h[lane] = 0;
+  h[lane + 32] = 0;
+  __syncwarp();
+  for (int64_t c = blockIdx.x; c < g.ncells; c += gridDim.x) {
+    int a0 = (int)(c % g.dims[0]);
+    int a1 = (int)((c / g.dims[0]) % g.dims[1]);
+    int a2 = (int)(c / ((int64_t)g.dims[0] * g.dims[1]));
+    int ne = build_entries<float>(g, a0, a1, a2, tab, lane);
+    if (lane == 0) h[ne]++;
+    __syncwarp();
+  }
+  __syncwarp();
+  for (int k = lane; k < 64; k += 32)
+    if (h[k]) atomicAdd(&hist[k], (unsigned long long)h[k]);
+}
+
+// ---------------------------------------------------------------------------
+// Scatter sorted-order vectors back to gid order (n x 3 caller layout),
+// optionally rotating (not needed: forces are already lab frame).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_unsort3(int64_t n, const typename V4<T>::t* __restrict__ src, const uint32_t* __restrict__ gid,
+                          T* __restrict__ dst) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  typename V4<T>::t v = src[s];
+  int64_t g = gid[s];
+  dst[3 * g] = v.x;
+  dst[3 * g + 1] = v.y;
+  dst[3 * g + 2] = v.z;
+}
+
+template <typename T>
+__global__ void k_pack4(int64_t n, const T* __restrict__ src, typename V4<T>::t* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  dst[i] = mk4(src[3 * i], src[3 * i + 1], src[3 * i + 2], (T)0);
+}
+
+// ---------------------------------------------------------------------------
+// K4: SLLOD (reading R19).  E(s) = e^{A s} as 3x3 matrices from the host.
+// ---------------------------------------------------------------------------
+struct SllodParams {
+  double Em[9];   // e^{-A dt/2}
+  double Ed[9];   // e^{A dt}
+  double Eh[9];   // e^{A dt/2}
+  double dt, inv_m;
+};
+
+__device__ __forceinline__ void mv3(const double* E, double x, double y, double z, double& ox, double& oy, double& oz) {
+  ox = E[0] * x + E[1] * y + E[2] * z;
+  oy = E[3] * x + E[4] * y + E[5] * z;
+  oz = E[6] * x + E[7] * y + E[8] * z;
+}
+
+// p <- E(-dt/2)(p + dt/2 F); q <- E(dt) q + dt E(dt/2) p / m; then K1 on the
+// new box (wrap + key + histogram), in place on q and p.
+template <typename T>
+__global__ void k_kick_drift_key(int64_t n, typename V4<T>::t* __restrict__ q, typename V4<T>::t* __restrict__ p,
+                                 const typename V4<T>::t* __restrict__ F, SllodParams sp, const __grid_constant__ Geom g,
+                                 uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  typename V4<T>::t qi = q[i], pi = p[i], fi = F[i];
+  double hd = 0.5 * sp.dt;
+  double px = (double)pi.x + hd * (double)fi.x, py = (double)pi.y + hd * (double)fi.y,
+         pz = (double)pi.z + hd * (double)fi.z;
+  double ax, ay, az;
+  mv3(sp.Em, px, py, pz, ax, ay, az);
+  double hx, hy, hz;
+  mv3(sp.Eh, ax, ay, az, hx, hy, hz);
+  double qx, qy, qz;
+  mv3(sp.Ed, (double)qi.x, (double)qi.y, (double)qi.z, qx, qy, qz);
+  qx += sp.dt * hx * sp.inv_m;
+  qy += sp.dt * hy * sp.inv_m;
+  qz += sp.dt * hz * sp.inv_m;
+  // stored precision first, then the canonical wrap/key of K1
+  double q0 = (double)(T)qx, q1 = (double)(T)qy, q2 = (double)(T)qz;
+  uint32_t c = wrap_key_one<T>(g, q0, q1, q2);
+  q[i] = mk4((T)q0, (T)q1, (T)q2, (T)0);
+  p[i] = mk4((T)ax, (T)ay, (T)az, (T)0);
+  key[i] = c;
+  slot[i] = atomicAdd(&counts[c], 1u);
+}
+
+// p <- E(-dt/2) p + dt/2 F
+template <typename T>
+__global__ void k_kick(int64_t n, typename V4<T>::t* __restrict__ p, const typename V4<T>::t* __restrict__ F,
+                       SllodParams sp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  typename V4<T>::t pi = p[i], fi = F[i];
+  double ax, ay, az;
+  mv3(sp.Em, (double)pi.x, (double)pi.y, (double)pi.z, ax, ay, az);
+  double hd = 0.5 * sp.dt;
+  p[i] = mk4((T)(ax + hd * (double)fi.x), (T)(ay + hd * (double)fi.y), (T)(az + hd * (double)fi.z), (T)0);
+}
+
+}  // namespace nc

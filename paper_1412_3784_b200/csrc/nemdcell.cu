@@ -1,0 +1,794 @@
+// nemdcell.cu -- C-ABI (include/nemdcell.h) over the sm_100a kernels in
+// kernels.cuh.  Host side: context, buffers, geometry (geom.hpp), launch
+// sequencing on the caller's stream, pointer-kind handling, deterministic
+// reductions and error reporting.  No torch types, no exceptions across the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nemdcell.h"
+#include "geom.hpp"
+#include "kernels.cuh"
+
+using namespace nc;
+
+struct nc_ctx {
+  nc_config cfg;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+
+  // geometry / flow
+  bool have_box = false, have_flow = false, have_state = false, have_cells = false, have_eval = false;
+  Geom g;
+  double A[9] = {0};
+  Policy pol;
+  double t = 0.0;
+
+  // capacity
+  int64_t cap = 0, max_cells = 0, max_blocks = 0, max_layers = 0;
+
+  // resident state (sorted by (cell, gid)), double-buffered q/p/gid
+  void *st_q[2] = {nullptr, nullptr}, *st_p[2] = {nullptr, nullptr}, *st_F = nullptr;
+  uint32_t* st_gid[2] = {nullptr, nullptr};
+  int cur = 0;
+  int64_t n_state = 0;
+
+  // user-call scratch
+  void *wq = nullptr;     // wrapped positions, input order (T4)
+  void *sq = nullptr;     // sorted positions (T4)
+  uint32_t* sgid = nullptr;
+  void *sF = nullptr;     // sorted forces (T4)
+  void *io_a = nullptr, *io_b = nullptr;  // n x 3 device staging for host pointers
+
+  // shared transient
+  double4* u = nullptr;   // sorted cell-local rotated coords, fp64 (w = sorted index)
+  uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr, *tmp = nullptr, *tmpgid = nullptr;
+  uint32_t *counts = nullptr, *cs = nullptr, *bsum = nullptr, *tot = nullptr;
+  double *bpart = nullptr, *lpart = nullptr, *part_tot = nullptr, *part_acc = nullptr;
+  // digest
+  uint32_t* dcnt = nullptr;
+  uint64_t *dhs = nullptr, *dhx = nullptr;
+  unsigned long long* hist = nullptr;
+
+  // last build bookkeeping
+  int64_t n_last = 0;
+  bool last_resident = false;     // last build used the resident state
+  const uint32_t* last_in_gid = nullptr;  // gid of input order (nullptr = identity)
+  int last_cpb = 0, last_bpl = 0;
+  double host_tot[NPART];
+  bool tot_valid = false;
+
+  // live kernel timing (nc_profile)
+  bool prof = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t prof_start = nullptr;
+};
+
+static thread_local std::string g_create_err;
+
+namespace {
+
+size_t tsize(const nc_ctx* c) { return c->cfg.prec == NC_F32 ? sizeof(float) : sizeof(double); }
+size_t v4size(const nc_ctx* c) { return 4 * tsize(c); }
+
+nc_status fail(nc_ctx* c, nc_status st, const std::string& msg) {
+  if (c) c->err = msg; else g_create_err = msg;
+  return st;
+}
+
+nc_status cuda_check(nc_ctx* c, cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return NC_OK;
+  return fail(c, NC_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                   \
+  do {                                                             \
+    nc_status _s = cuda_check(ctx, (expr), #expr);                 \
+    if (_s != NC_OK) return _s;                                    \
+  } while (0)
+
+#define LAUNCHED()                                                     \
+  do {                                                                 \
+    ctx->launches++;                                                   \
+    nc_status _s = cuda_check(ctx, cudaGetLastError(), "kernel launch"); \
+    if (_s != NC_OK) return _s;                                        \
+  } while (0)
+
+cudaEvent_t pool_event(nc_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII-free helpers: mark the start / end of one kernel launch of kind k
+inline void prof_begin(nc_ctx* ctx) {
+  if (!ctx->prof) return;
+  ctx->prof_start = pool_event(ctx);
+  cudaEventRecord(ctx->prof_start, ctx->stream);
+}
+inline void prof_end(nc_ctx* ctx, int k) {
+  if (!ctx->prof) return;
+  cudaEvent_t e = pool_event(ctx);
+  cudaEventRecord(e, ctx->stream);
+  ctx->prof_ev.push_back({k, {ctx->prof_start, e}});
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) { cudaGetLastError(); return false; }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int cells_per_block() { return 2 * K3_WARPS; }
+
+nc_status apply_box(nc_ctx* ctx, const double* L) {
+  Geom g;
+  int st = make_geom(g, L, (int)ctx->cfg.variant, ctx->cfg.rc);
+  if (st == GEOM_BAD_BOX) return fail(ctx, NC_E_BOX, "box matrix has det <= 0 or a non-finite entry");
+  if (st == GEOM_DEGENERATE)
+    return fail(ctx, NC_E_DEGENERATE,
+                "degenerate cell grid (DS needs c_k >= 3; DO needs l1,l2 >= 4 and l3 >= 3): dims " +
+                    std::to_string(g.dims[0]) + "x" + std::to_string(g.dims[1]) + "x" + std::to_string(g.dims[2]));
+  if (g.ncells > ctx->max_cells)
+    return fail(ctx, NC_E_OOM, "cell count " + std::to_string(g.ncells) + " exceeds max_cells " +
+                                   std::to_string(ctx->max_cells));
+  int cpb = cells_per_block();
+  int64_t bpl = (((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb;
+  if (bpl * g.dims[2] > ctx->max_blocks || g.dims[2] > ctx->max_layers)
+    return fail(ctx, NC_E_OOM, "block/layer partial buffers too small for this grid");
+  g.eps = ctx->cfg.eps;
+  g.sig2 = ctx->cfg.sigma * ctx->cfg.sigma;
+  g.ushift = ctx->cfg.u_shift;
+  double tau = ctx->cfg.prec == NC_F32 ? 2e-5 : 1e-10;  // re-check band, DESIGN.md section 5
+  g.band_lo = g.rc2 * (1.0 - tau);
+  g.band_hi = g.rc2 * (1.0 + tau);
+  ctx->g = g;
+  ctx->have_box = true;
+  return NC_OK;
+}
+
+template <typename T>
+nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t* qwrap, int64_t n,
+                       const uint32_t* gid_in, const typename V4<T>::t* p_in, typename V4<T>::t* q_out,
+                       typename V4<T>::t* p_out, uint32_t* gid_out) {
+  cudaStream_t s = ctx->stream;
+  const Geom& g = ctx->g;
+  int64_t C = g.ncells;
+  CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
+  if (n > 0) {
+    prof_begin(ctx);
+    k_wrap_key<T><<<nblk(n, 256), 256, 0, s>>>(n, qin, stride, qwrap, ctx->key, ctx->slot, ctx->counts, g);
+    LAUNCHED();
+    prof_end(ctx, NC_K_WRAPKEY);
+  }
+  int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
+  prof_begin(ctx);
+  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
+  LAUNCHED();
+  prof_end(ctx, NC_K_SCAN);
+  prof_begin(ctx);
+  k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
+  LAUNCHED();
+  prof_end(ctx, NC_K_SCAN);
+  prof_begin(ctx);
+  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
+  LAUNCHED();
+  prof_end(ctx, NC_K_SCAN);
+  if (n > 0) {
+    prof_begin(ctx);
+    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, gid_in, ctx->tmp, ctx->tmpgid);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCATTER);
+    prof_begin(ctx);
+    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->key, ctx->cs, qwrap, p_in, q_out,
+                                                  p_out, gid_out, ctx->u, ctx->nh, g);
+    LAUNCHED();
+    prof_end(ctx, NC_K_RANKGATHER);
+  }
+  ctx->n_last = n;
+  ctx->last_in_gid = gid_in;
+  ctx->have_cells = true;
+  return NC_OK;
+}
+
+template <typename T, bool DIGEST>
+nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t* gid, typename V4<T>::t* F) {
+  cudaStream_t s = ctx->stream;
+  const Geom& g = ctx->g;
+  int cpb = cells_per_block();
+  int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
+  int nblocks = bpl * g.dims[2];
+  size_t smem = K3_WARPS * sizeof(K3Smem<T>);
+  static bool attr_set[2][2] = {{false, false}, {false, false}};
+  bool& as = attr_set[sizeof(T) == 8][DIGEST];
+  if (!as) {
+    CK(cudaFuncSetAttribute(k_pairs<T, DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    as = true;
+  }
+  prof_begin(ctx);
+  k_pairs<T, DIGEST><<<nblocks, K3_WARPS * 32, smem, s>>>(ctx->u, ctx->cs, qs, ctx->nh, gid, F,
+                                                         ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl);
+  LAUNCHED();
+  prof_end(ctx, NC_K_PAIRS);
+  int nl = g.dims[2];
+  prof_begin(ctx);
+  k_reduce_layers<<<nblk((int64_t)nl * NPART, 128), 128, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart);
+  LAUNCHED();
+  prof_end(ctx, NC_K_REDUCE);
+  prof_begin(ctx);
+  k_reduce_total<<<1, 32, 0, s>>>(ctx->lpart, nl, ctx->part_tot, ctx->part_acc);
+  LAUNCHED();
+  prof_end(ctx, NC_K_REDUCE);
+  ctx->last_cpb = cpb;
+  ctx->last_bpl = bpl;
+  ctx->tot_valid = false;
+  ctx->have_eval = true;
+  return NC_OK;
+}
+
+nc_status fetch_totals(nc_ctx* ctx) {
+  if (ctx->tot_valid) return NC_OK;
+  CK(cudaMemcpyAsync(ctx->host_tot, ctx->part_tot, sizeof(double) * NPART, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->tot_valid = true;
+  return NC_OK;
+}
+
+// U and the lab-frame virial W = Q W_rot Q^T (W = (xx,yy,zz,xy,xz,yz))
+void totals_to_UW(const nc_ctx* ctx, double* U, double* W) {
+  const double* t = ctx->host_tot;
+  if (U) *U = t[0];
+  if (W && ctx->cfg.prec == NC_F64) {  // fp64 mode accumulates in the lab frame
+    for (int k = 0; k < 6; ++k) W[k] = t[1 + k];
+  } else if (W) {  // fp32 mode: rotated frame, W = Q W_rot Q^T
+    double Wr[9] = {t[1], t[4], t[5], t[4], t[2], t[6], t[5], t[6], t[3]};
+    const double* Q = ctx->g.Q;
+    double X[9], Y[9];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) X[3 * r + c] = Q[3 * r] * Wr[c] + Q[3 * r + 1] * Wr[3 + c] + Q[3 * r + 2] * Wr[6 + c];
+    for (int r = 0; r < 3; ++r)
+      for (int c = 0; c < 3; ++c) Y[3 * r + c] = X[3 * r] * Q[3 * c] + X[3 * r + 1] * Q[3 * c + 1] + X[3 * r + 2] * Q[3 * c + 2];
+    W[0] = Y[0]; W[1] = Y[4]; W[2] = Y[8]; W[3] = Y[1]; W[4] = Y[2]; W[5] = Y[5];
+  }
+}
+
+nc_status check_finite(nc_ctx* ctx) {
+  nc_status st = fetch_totals(ctx);
+  if (st) return st;
+  bool ok = ctx->host_tot[11] == 0.0;
+  for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
+  if (!ok) return fail(ctx, NC_E_NONFINITE, "non-finite force, energy or virial");
+  return NC_OK;
+}
+
+// copy a caller n x 3 array to device staging if it is host memory
+nc_status stage_in(nc_ctx* ctx, const void* src, void* dev_buf, int64_t n, const void** out) {
+  if (is_device_ptr(src)) { *out = src; return NC_OK; }
+  CK(cudaMemcpyAsync(dev_buf, src, 3 * tsize(ctx) * n, cudaMemcpyHostToDevice, ctx->stream));
+  *out = dev_buf;
+  return NC_OK;
+}
+
+template <typename T>
+nc_status build_user(nc_ctx* ctx, const void* q, int64_t n) {
+  const void* qd = nullptr;
+  nc_status st = stage_in(ctx, q, ctx->io_a, n, &qd);
+  if (st) return st;
+  st = launch_build<T>(ctx, (const T*)qd, 3, (typename V4<T>::t*)ctx->wq, n, nullptr, nullptr,
+                       (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid);
+  if (st) return st;
+  ctx->last_resident = false;
+  return NC_OK;
+}
+
+template <typename T>
+nc_status unsort_out(nc_ctx* ctx, const void* src4, const uint32_t* gid, int64_t n, void* dst) {
+  bool dev = is_device_ptr(dst);
+  T* d = dev ? (T*)dst : (T*)ctx->io_b;
+  if (n > 0) {
+    prof_begin(ctx);
+    k_unsort3<T><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (const typename V4<T>::t*)src4, gid, d);
+    LAUNCHED();
+    prof_end(ctx, NC_K_OTHER);
+  }
+  if (!dev) {
+    CK(cudaMemcpyAsync(dst, ctx->io_b, 3 * sizeof(T) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  return NC_OK;
+}
+
+template <typename T>
+nc_status compute_user(nc_ctx* ctx, const void* q, int64_t n, void* F, double* U, double* W) {
+  nc_status st = build_user<T>(ctx, q, n);
+  if (st) return st;
+  st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF);
+  if (st) return st;
+  if (F) {
+    st = unsort_out<T>(ctx, ctx->sF, ctx->sgid, n, F);
+    if (st) return st;
+  }
+  st = check_finite(ctx);  // synchronizes the stream
+  if (st) return st;
+  totals_to_UW(ctx, U, W);
+  return NC_OK;
+}
+
+template <typename T>
+nc_status set_state_t(nc_ctx* ctx, const void* q, const void* p, const int64_t* gid, int64_t n) {
+  cudaStream_t s = ctx->stream;
+  const void* qd = nullptr;
+  const void* pd = nullptr;
+  nc_status st = stage_in(ctx, q, ctx->io_a, n, &qd);
+  if (st) return st;
+  // pack into the current state buffers (input order), gid
+  int c = ctx->cur;
+  if (n > 0) {
+    prof_begin(ctx);
+    k_pack4<T><<<nblk(n, 256), 256, 0, s>>>(n, (const T*)qd, (typename V4<T>::t*)ctx->st_q[c]);
+    LAUNCHED();
+    prof_end(ctx, NC_K_OTHER);
+  }
+  if (p) {
+    st = stage_in(ctx, p, ctx->io_b, n, &pd);
+    if (st) return st;
+    if (n > 0) {
+      prof_begin(ctx);
+      k_pack4<T><<<nblk(n, 256), 256, 0, s>>>(n, (const T*)pd, (typename V4<T>::t*)ctx->st_p[c]);
+      LAUNCHED();
+      prof_end(ctx, NC_K_OTHER);
+    }
+  } else {
+    CK(cudaMemsetAsync(ctx->st_p[c], 0, v4size(ctx) * n, s));
+  }
+  std::vector<uint32_t> hg(n);
+  for (int64_t i = 0; i < n; ++i) hg[i] = gid ? (uint32_t)gid[i] : (uint32_t)i;
+  CK(cudaMemcpyAsync(ctx->st_gid[c], hg.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, s));
+  // build from the packed state (stride 4), in place wrap, gather into the other buffers
+  int o = 1 - c;
+  st = launch_build<T>(ctx, (const T*)ctx->st_q[c], 4, (typename V4<T>::t*)ctx->st_q[c], n, ctx->st_gid[c],
+                       (const typename V4<T>::t*)ctx->st_p[c], (typename V4<T>::t*)ctx->st_q[o],
+                       (typename V4<T>::t*)ctx->st_p[o], ctx->st_gid[o]);
+  if (st) return st;
+  CK(cudaStreamSynchronize(s));  // hg lifetime
+  ctx->cur = o;
+  ctx->n_state = n;
+  ctx->last_resident = true;
+  st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->st_q[o], ctx->st_gid[o],
+                              (typename V4<T>::t*)ctx->st_F);
+  if (st) return st;
+  st = check_finite(ctx);
+  if (st) return st;
+  ctx->have_state = true;
+  return NC_OK;
+}
+
+template <typename T>
+nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
+  cudaStream_t s = ctx->stream;
+  int64_t n = ctx->n_state;
+  SllodParams sp;
+  expm3(ctx->A, -0.5 * dt, sp.Em);
+  expm3(ctx->A, dt, sp.Ed);
+  expm3(ctx->A, 0.5 * dt, sp.Eh);
+  sp.dt = dt;
+  sp.inv_m = 1.0 / ctx->cfg.mass;
+  for (int k = 0; k < nsteps; ++k) {
+    // new box at t + dt (remapped) before the drift+wrap kernel
+    double Lnew[9];
+    box_at(ctx->pol, ctx->A, ctx->t + dt, Lnew);
+    nc_status st = apply_box(ctx, Lnew);
+    if (st) return st;
+    ctx->t += dt;
+    int c = ctx->cur, o = 1 - c;
+    const Geom& g = ctx->g;
+    CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (g.ncells + 1), s));
+    if (n > 0) {
+      prof_begin(ctx);
+      k_kick_drift_key<T><<<nblk(n, 256), 256, 0, s>>>(n, (typename V4<T>::t*)ctx->st_q[c],
+                                                      (typename V4<T>::t*)ctx->st_p[c],
+                                                      (const typename V4<T>::t*)ctx->st_F, sp, g, ctx->key,
+                                                      ctx->slot, ctx->counts);
+      LAUNCHED();
+      prof_end(ctx, NC_K_WRAPKEY);
+    }
+    int64_t C = g.ncells;
+    int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
+    prof_begin(ctx);
+    k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCAN);
+    prof_begin(ctx);
+    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCAN);
+    prof_begin(ctx);
+    k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCAN);
+    if (n > 0) {
+      prof_begin(ctx);
+      k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->st_gid[c], ctx->tmp, ctx->tmpgid);
+      LAUNCHED();
+      prof_end(ctx, NC_K_SCATTER);
+      prof_begin(ctx);
+      k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->key, ctx->cs,
+                                                    (const typename V4<T>::t*)ctx->st_q[c],
+                                                    (const typename V4<T>::t*)ctx->st_p[c],
+                                                    (typename V4<T>::t*)ctx->st_q[o], (typename V4<T>::t*)ctx->st_p[o],
+                                                    ctx->st_gid[o], ctx->u, ctx->nh, g);
+      LAUNCHED();
+      prof_end(ctx, NC_K_RANKGATHER);
+    }
+    ctx->cur = o;
+    ctx->n_last = n;
+    ctx->last_in_gid = ctx->st_gid[c];
+    ctx->last_resident = true;
+    ctx->have_cells = true;
+    st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->st_q[o], ctx->st_gid[o],
+                                (typename V4<T>::t*)ctx->st_F);
+    if (st) return st;
+    if (n > 0) {
+      prof_begin(ctx);
+      k_kick<T><<<nblk(n, 256), 256, 0, s>>>(n, (typename V4<T>::t*)ctx->st_p[o], (const typename V4<T>::t*)ctx->st_F, sp);
+      LAUNCHED();
+      prof_end(ctx, NC_K_KICK);
+    }
+  }
+  if (U || W) {
+    nc_status st = check_finite(ctx);
+    if (st) return st;
+    totals_to_UW(ctx, U, W);
+  }
+  return NC_OK;
+}
+
+template <typename T>
+nc_status digest_t(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_t* hxor) {
+  const void* qs = ctx->last_resident ? ctx->st_q[ctx->cur] : ctx->sq;
+  const uint32_t* gid = ctx->last_resident ? ctx->st_gid[ctx->cur] : ctx->sgid;
+  void* F = ctx->last_resident ? ctx->sF : ctx->sF;
+  nc_status st = launch_pairs<T, true>(ctx, (const typename V4<T>::t*)qs, gid, (typename V4<T>::t*)F);
+  if (st) return st;
+  int64_t n = ctx->n_last;
+  std::vector<uint32_t> c(n), gg(n);
+  std::vector<uint64_t> a(n), b(n);
+  CK(cudaMemcpyAsync(c.data(), ctx->dcnt, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(a.data(), ctx->dhs, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(b.data(), ctx->dhx, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(gg.data(), gid, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t s = 0; s < n; ++s) {
+    if (cnt) cnt[gg[s]] = c[s];
+    if (hsum) hsum[gg[s]] = a[s];
+    if (hxor) hxor[gg[s]] = b[s];
+  }
+  return NC_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+
+extern "C" {
+
+const char* nc_version(void) { return "nemdcell 0.1 (sm_100a)"; }
+
+const char* nc_last_error(const nc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int64_t nc_launch_count(const nc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nc_status nc_profile(nc_ctx* ctx, int enable) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  for (auto& p : ctx->prof_ev) {
+    ctx->ev_pool.push_back(p.second.first);
+    ctx->ev_pool.push_back(p.second.second);
+  }
+  if (enable) {
+    ctx->prof_ev.clear();
+    CK(cudaMemsetAsync(ctx->part_acc, 0, sizeof(double) * (NPART + 1), ctx->stream));
+  }
+  ctx->prof = enable != 0;
+  if (enable) ctx->prof_ev.reserve(4096);
+  return NC_OK;
+}
+
+nc_status nc_profile_read(nc_ctx* ctx, double ms[8], int64_t counts[8]) {
+  if (!ctx || !ms || !counts) return fail(ctx, NC_E_ARG, "null argument");
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < NC_K_COUNT; ++k) { ms[k] = 0.0; counts[k] = 0; }
+  for (auto& p : ctx->prof_ev) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, p.second.first, p.second.second));
+    ms[p.first] += t;
+    counts[p.first]++;
+  }
+  return NC_OK;
+}
+
+nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
+  if (!out) return fail(nullptr, NC_E_ARG, "out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(nullptr, NC_E_ARG, "cfg is NULL");
+  if (cfg->variant != NC_DS && cfg->variant != NC_DO) return fail(nullptr, NC_E_ARG, "bad variant");
+  if (cfg->prec != NC_F32 && cfg->prec != NC_F64) return fail(nullptr, NC_E_ARG, "bad precision");
+  if (!(cfg->rc > 0) || !(cfg->sigma > 0) || !(cfg->mass > 0) || !std::isfinite(cfg->eps))
+    return fail(nullptr, NC_E_ARG, "rc, sigma and mass must be positive");
+  if (cfg->capacity < 0 || cfg->capacity > (int64_t)0xFFFFFFF0LL)
+    return fail(nullptr, NC_E_ARG, "capacity out of range (< 2^32 particles)");
+  nc_ctx* ctx = new nc_ctx();
+  ctx->cfg = *cfg;
+  ctx->stream = (cudaStream_t)cfg->stream;
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return fail(nullptr, NC_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  int64_t N = std::max<int64_t>(cfg->capacity, 1);
+  ctx->cap = N;
+  ctx->max_cells = cfg->max_cells > 0 ? cfg->max_cells : 2 * N + 4096;
+  int cpb = cells_per_block();
+  ctx->max_layers = 1 << 16;
+  // blocks = sum over layers of ceil(l1 l2 / cpb) <= C/cpb + layers
+  ctx->max_blocks = ctx->max_cells / cpb + ctx->max_layers + 16;
+  size_t v4 = v4size(ctx), ts = tsize(ctx);
+  int64_t C1 = ctx->max_cells + 1;
+  const size_t N_ = (size_t)N;
+  struct A { void** p; size_t bytes; } allocs[] = {
+      {&ctx->st_q[0], v4 * N_}, {&ctx->st_q[1], v4 * N_}, {&ctx->st_p[0], v4 * N_}, {&ctx->st_p[1], v4 * N_},
+      {(void**)&ctx->st_gid[0], 4 * N_}, {(void**)&ctx->st_gid[1], 4 * N_}, {&ctx->st_F, v4 * N_},
+      {&ctx->wq, v4 * N_}, {&ctx->sq, v4 * N_}, {(void**)&ctx->sgid, 4 * N_}, {&ctx->sF, v4 * N_},
+      {&ctx->io_a, 3 * ts * N_}, {&ctx->io_b, 3 * ts * N_}, {(void**)&ctx->u, sizeof(double4) * N_},
+      {(void**)&ctx->nh, 4 * N_}, {(void**)&ctx->key, 4 * N_}, {(void**)&ctx->slot, 4 * N_},
+      {(void**)&ctx->tmp, 4 * N_}, {(void**)&ctx->tmpgid, 4 * N_},
+      {(void**)&ctx->counts, 4 * (size_t)C1}, {(void**)&ctx->cs, 4 * (size_t)C1},
+      {(void**)&ctx->bsum, 4 * (size_t)(C1 / SCAN_TILE + 2)}, {(void**)&ctx->tot, 16},
+      {(void**)&ctx->bpart, sizeof(double) * NPART * (size_t)ctx->max_blocks},
+      {(void**)&ctx->lpart, sizeof(double) * NPART * (size_t)ctx->max_layers},
+      {(void**)&ctx->part_tot, sizeof(double) * NPART}, {(void**)&ctx->part_acc, sizeof(double) * (NPART + 1)},
+      {(void**)&ctx->dcnt, 4 * N_}, {(void**)&ctx->dhs, 8 * N_}, {(void**)&ctx->dhx, 8 * N_},
+      {(void**)&ctx->hist, 8 * 64},
+  };
+  for (auto& a : allocs) {
+    e = cudaMalloc(a.p, a.bytes);
+    if (e != cudaSuccess) {
+      std::string m = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+      cudaGetLastError();
+      nc_destroy(ctx);
+      return fail(nullptr, e == cudaErrorMemoryAllocation ? NC_E_OOM : NC_E_CUDA, m);
+    }
+  }
+  e = cudaMemset(ctx->part_acc, 0, sizeof(double) * (NPART + 1));
+  if (e != cudaSuccess) {
+    nc_destroy(ctx);
+    return fail(nullptr, NC_E_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
+  }
+  ctx->pol.kind = 0;
+  *out = ctx;
+  return NC_OK;
+}
+
+void nc_destroy(nc_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  void* ps[] = {ctx->st_q[0], ctx->st_q[1], ctx->st_p[0], ctx->st_p[1], ctx->st_gid[0], ctx->st_gid[1], ctx->st_F,
+                ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->nh, ctx->key, ctx->slot,
+                ctx->tmp, ctx->tmpgid, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
+                ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  for (auto& p : ctx->prof_ev) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  delete ctx;
+}
+
+nc_status nc_set_box(nc_ctx* ctx, const double L[9]) {
+  if (!ctx || !L) return fail(ctx, NC_E_ARG, "null argument");
+  nc_status st = apply_box(ctx, L);
+  if (st) return st;
+  if (!ctx->have_flow) {
+    ctx->pol.kind = 0;
+    std::memcpy(ctx->pol.L0, L, sizeof(double) * 9);
+    std::memset(ctx->A, 0, sizeof ctx->A);
+    ctx->t = 0.0;
+  }
+  return NC_OK;
+}
+
+nc_status nc_set_flow(nc_ctx* ctx, const double A[9], const nc_remap* pol, double t) {
+  if (!ctx || !A) return fail(ctx, NC_E_ARG, "null argument");
+  double amax = 1.0, tr = A[0] + A[4] + A[8];
+  for (int k = 0; k < 9; ++k) {
+    if (!std::isfinite(A[k])) return fail(ctx, NC_E_FLOW, "non-finite flow matrix");
+    amax = std::max(amax, std::fabs(A[k]));
+  }
+  if (std::fabs(tr) > 1e-12 * amax) return fail(ctx, NC_E_FLOW, "flow matrix A must be traceless (incompressible)");
+  Policy p;
+  std::memset(&p, 0, sizeof p);
+  if (pol) {
+    p.kind = (int)pol->kind;
+    std::memcpy(p.L0, pol->L0, sizeof(double) * 9);
+    p.tstar = pol->tstar;
+    for (int k = 0; k < 3; ++k) { p.om1[k] = pol->omega1[k]; p.om2[k] = pol->omega2[k]; }
+    p.beta[0] = pol->beta[0];
+    p.beta[1] = pol->beta[1];
+    p.eps = pol->eps;
+    if (p.kind < 0 || p.kind > 3) return fail(ctx, NC_E_ARG, "bad remap kind");
+    if (p.kind == 2 && !(p.tstar > 0)) return fail(ctx, NC_E_ARG, "KR needs tstar > 0");
+    if (p.kind == 1 && !(A[1] != 0.0)) return fail(ctx, NC_E_ARG, "LE needs a shear flow A[0][1] != 0");
+  } else {
+    if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_flow without a policy needs nc_set_box first");
+    p.kind = 0;
+    std::memcpy(p.L0, ctx->g.L, sizeof(double) * 9);
+  }
+  double L[9];
+  std::memcpy(ctx->A, A, sizeof(double) * 9);
+  box_at(p, A, t, L);
+  nc_status st = apply_box(ctx, L);
+  if (st) return st;
+  ctx->pol = p;
+  ctx->t = t;
+  ctx->have_flow = true;
+  return NC_OK;
+}
+
+nc_status nc_build_cells(nc_ctx* ctx, const void* q, int64_t n) {
+  if (!ctx || (!q && n > 0)) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box first");
+  if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
+  nc_status st = ctx->cfg.prec == NC_F32 ? build_user<float>(ctx, q, n) : build_user<double>(ctx, q, n);
+  if (st) return st;
+  return cuda_check(ctx, cudaStreamSynchronize(ctx->stream), "build_cells");
+}
+
+nc_status nc_compute_forces(nc_ctx* ctx, const void* q, int64_t n, void* F, double* U, double W[6]) {
+  if (!ctx || (!q && n > 0)) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box first");
+  if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
+  return ctx->cfg.prec == NC_F32 ? compute_user<float>(ctx, q, n, F, U, W) : compute_user<double>(ctx, q, n, F, U, W);
+}
+
+nc_status nc_set_state(nc_ctx* ctx, const void* q, const void* p, const int64_t* gid, int64_t n) {
+  if (!ctx || (!q && n > 0)) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
+  if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
+  if (gid)
+    for (int64_t i = 0; i < n; ++i)
+      if (gid[i] < 0 || gid[i] > 0xFFFFFFFFLL) return fail(ctx, NC_E_ARG, "gid out of range");
+  return ctx->cfg.prec == NC_F32 ? set_state_t<float>(ctx, q, p, gid, n) : set_state_t<double>(ctx, q, p, gid, n);
+}
+
+nc_status nc_step_sllod(nc_ctx* ctx, double dt, int nsteps, double* U, double W[6]) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (!ctx->have_state) return fail(ctx, NC_E_STATE, "nc_set_state first");
+  if (!(dt > 0) || nsteps < 0) return fail(ctx, NC_E_ARG, "dt must be > 0 and nsteps >= 0");
+  return ctx->cfg.prec == NC_F32 ? step_t<float>(ctx, dt, nsteps, U, W) : step_t<double>(ctx, dt, nsteps, U, W);
+}
+
+nc_status nc_get_state(nc_ctx* ctx, void* q, void* p, int64_t* gid, int64_t* n, double L[9], double* t) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (!ctx->have_state) return fail(ctx, NC_E_STATE, "no resident state");
+  int64_t m = ctx->n_state;
+  int c = ctx->cur;
+  nc_status st;
+  if (q) {
+    st = ctx->cfg.prec == NC_F32 ? unsort_out<float>(ctx, ctx->st_q[c], ctx->st_gid[c], m, q)
+                                 : unsort_out<double>(ctx, ctx->st_q[c], ctx->st_gid[c], m, q);
+    if (st) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (p) {
+    st = ctx->cfg.prec == NC_F32 ? unsort_out<float>(ctx, ctx->st_p[c], ctx->st_gid[c], m, p)
+                                 : unsort_out<double>(ctx, ctx->st_p[c], ctx->st_gid[c], m, p);
+    if (st) return st;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  if (gid) {
+    std::vector<uint32_t> g(m);
+    CK(cudaMemcpyAsync(g.data(), ctx->st_gid[c], 4 * m, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::vector<uint32_t> s(g);
+    std::sort(s.begin(), s.end());
+    for (int64_t i = 0; i < m; ++i) gid[i] = s[i];
+  }
+  if (n) *n = m;
+  if (L) std::memcpy(L, ctx->g.L, sizeof(double) * 9);
+  if (t) *t = ctx->t;
+  return NC_OK;
+}
+
+nc_status nc_get_cells(nc_ctx* ctx, int64_t* cell_of, int64_t* cell_start, int32_t dims[3], void* wrapped_q) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (!ctx->have_cells) return fail(ctx, NC_E_STATE, "no cells built");
+  int64_t n = ctx->n_last, C = ctx->g.ncells;
+  cudaStream_t s = ctx->stream;
+  std::vector<uint32_t> key(n), ig(n), cs(C + 1);
+  CK(cudaMemcpyAsync(key.data(), ctx->key, 4 * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(cs.data(), ctx->cs, 4 * (C + 1), cudaMemcpyDeviceToHost, s));
+  if (ctx->last_in_gid) CK(cudaMemcpyAsync(ig.data(), ctx->last_in_gid, 4 * n, cudaMemcpyDeviceToHost, s));
+  std::vector<unsigned char> wq;
+  size_t ts = tsize(ctx);
+  const void* wsrc = ctx->last_resident ? ctx->st_q[1 - ctx->cur] : ctx->wq;
+  if (wrapped_q) {
+    wq.resize(4 * ts * n);
+    CK(cudaMemcpyAsync(wq.data(), wsrc, 4 * ts * n, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t gi = ctx->last_in_gid ? (int64_t)ig[i] : i;
+    if (cell_of) cell_of[gi] = key[i];
+    if (wrapped_q)
+      for (int k = 0; k < 3; ++k)
+        std::memcpy((unsigned char*)wrapped_q + (3 * gi + k) * ts, wq.data() + (4 * i + k) * ts, ts);
+  }
+  if (cell_start)
+    for (int64_t c = 0; c <= C; ++c) cell_start[c] = cs[c];
+  if (dims)
+    for (int k = 0; k < 3; ++k) dims[k] = ctx->g.dims[k];
+  return NC_OK;
+}
+
+nc_status nc_get_pair_digest(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_t* hxor) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (!ctx->have_cells) return fail(ctx, NC_E_STATE, "no cells built");
+  nc_status st = ctx->cfg.prec == NC_F32 ? digest_t<float>(ctx, cnt, hsum, hxor) : digest_t<double>(ctx, cnt, hsum, hxor);
+  return st;
+}
+
+nc_status nc_get_stats(nc_ctx* ctx, nc_stats* out) {
+  if (!ctx || !out) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_eval) return fail(ctx, NC_E_STATE, "no evaluation yet");
+  nc_status st = fetch_totals(ctx);
+  if (st) return st;
+  std::memset(out, 0, sizeof *out);
+  out->n = ctx->n_last;
+  for (int k = 0; k < 3; ++k) out->dims[k] = ctx->g.dims[k];
+  out->ncells = ctx->g.ncells;
+  out->interactions = ctx->host_tot[7];
+  out->candidates = ctx->host_tot[8];
+  out->stencil_cells = ctx->host_tot[9];
+  out->rechecks = ctx->host_tot[10];
+  totals_to_UW(ctx, &out->U, out->W);
+  double acc[NPART + 1];
+  CK(cudaMemcpyAsync(acc, ctx->part_acc, sizeof acc, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  out->acc_evals = acc[NPART];
+  out->acc_interactions = acc[7];
+  out->acc_candidates = acc[8];
+  return NC_OK;
+}
+
+nc_status nc_get_stencil_histogram(nc_ctx* ctx, int64_t hist[64]) {
+  if (!ctx || !hist) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box first");
+  CK(cudaMemsetAsync(ctx->hist, 0, 8 * 64, ctx->stream));
+  prof_begin(ctx);
+  k_stencil_hist<<<1184, 32, 0, ctx->stream>>>(ctx->g, ctx->hist);
+  LAUNCHED();
+  prof_end(ctx, NC_K_OTHER);
+  unsigned long long h[64];
+  CK(cudaMemcpyAsync(h, ctx->hist, 8 * 64, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < 64; ++k) hist[k] = (int64_t)h[k];
+  return NC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,345 @@
+"""Thin Python binding of the C-ABI in include/nemdcell.h (argument marshalling only).
+
+Every function of the header is exposed under the same name; `CellList` is a
+small convenience wrapper that owns one context and takes torch tensors or
+numpy arrays.  All arithmetic of the path runs in libnemdcell.so (sm_100a);
+there is no CPU fallback: if the library cannot be loaded, or no CUDA device
+is present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import build as _build
+
+NC_DS, NC_DO = 0, 1
+NC_F32, NC_F64 = 0, 1
+NC_REMAP_NONE, NC_REMAP_LE, NC_REMAP_KR, NC_REMAP_GKR = 0, 1, 2, 3
+STATUS = {0: "NC_OK", 1: "NC_E_ARG", 2: "NC_E_BOX", 3: "NC_E_DEGENERATE", 4: "NC_E_FLOW", 5: "NC_E_STATE",
+          6: "NC_E_CUDA", 7: "NC_E_NCCL", 8: "NC_E_OOM", 9: "NC_E_NONFINITE"}
+
+EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cells", "nc_compute_forces",
+           "nc_set_state", "nc_step_sllod", "nc_get_state", "nc_get_cells", "nc_get_pair_digest", "nc_get_stats",
+           "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
+           "nc_profile_read"]
+KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
+
+
+class NcError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class nc_config(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int), ("prec", ctypes.c_int), ("rc", ctypes.c_double),
+                ("eps", ctypes.c_double), ("sigma", ctypes.c_double), ("u_shift", ctypes.c_double),
+                ("mass", ctypes.c_double), ("device", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("capacity", ctypes.c_int64), ("max_cells", ctypes.c_int64)]
+
+
+class nc_remap(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("L0", ctypes.c_double * 9), ("tstar", ctypes.c_double),
+                ("omega1", ctypes.c_double * 3), ("omega2", ctypes.c_double * 3), ("beta", ctypes.c_double * 2),
+                ("eps", ctypes.c_double)]
+
+
+class nc_stats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("dims", ctypes.c_int32 * 3), ("ncells", ctypes.c_int64),
+                ("candidates", ctypes.c_double), ("interactions", ctypes.c_double),
+                ("stencil_cells", ctypes.c_double), ("rechecks", ctypes.c_double), ("U", ctypes.c_double),
+                ("W", ctypes.c_double * 6), ("acc_evals", ctypes.c_double), ("acc_interactions", ctypes.c_double),
+                ("acc_candidates", ctypes.c_double)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(build_if_missing: bool = True) -> ctypes.CDLL:
+    """Load libnemdcell.so (building it with nvcc if missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if build_if_missing and _build.stale():
+            _build.build()
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"libnemdcell.so not found at {_build.LIB}; run paper_1412_3784_b200.build.build()")
+        L = ctypes.CDLL(_build.LIB)
+        vp, i64, i32, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+        L.nc_create.argtypes = [ctypes.POINTER(nc_config), ctypes.POINTER(vp)]
+        L.nc_destroy.argtypes = [vp]
+        L.nc_destroy.restype = None
+        L.nc_set_box.argtypes = [vp, vp]
+        L.nc_set_flow.argtypes = [vp, vp, ctypes.POINTER(nc_remap), d]
+        L.nc_build_cells.argtypes = [vp, vp, i64]
+        L.nc_compute_forces.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.nc_set_state.argtypes = [vp, vp, vp, vp, i64]
+        L.nc_step_sllod.argtypes = [vp, d, i32, vp, vp]
+        L.nc_get_state.argtypes = [vp, vp, vp, vp, vp, vp, vp]
+        L.nc_get_cells.argtypes = [vp, vp, vp, vp, vp]
+        L.nc_get_pair_digest.argtypes = [vp, vp, vp, vp]
+        L.nc_get_stats.argtypes = [vp, ctypes.POINTER(nc_stats)]
+        L.nc_get_stencil_histogram.argtypes = [vp, vp]
+        L.nc_profile.argtypes = [vp, i32]
+        L.nc_profile_read.argtypes = [vp, vp, vp]
+        L.nc_launch_count.argtypes = [vp]
+        L.nc_launch_count.restype = i64
+        L.nc_last_error.argtypes = [vp]
+        L.nc_last_error.restype = ctypes.c_char_p
+        L.nc_version.restype = ctypes.c_char_p
+        for name in EXPORTS:
+            if name not in ("nc_destroy", "nc_launch_count", "nc_last_error", "nc_version"):
+                getattr(L, name).restype = i32
+        _lib = L
+        return L
+
+
+def _ptr(x):
+    """Raw pointer of a torch tensor, numpy array or None."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous(), "tensor must be contiguous"
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"]
+        return x.ctypes.data_as(ctypes.c_void_p)
+    if isinstance(x, ctypes.c_void_p):
+        return x
+    raise TypeError(type(x))
+
+
+def _check(ctx, st):
+    if st != 0:
+        raise NcError(st, load().nc_last_error(ctx).decode())
+
+
+def _d9(L):
+    a = np.ascontiguousarray(np.asarray(L, dtype=np.float64).reshape(9))
+    return a
+
+
+# ----------------------------------------------------------------- same-name wrappers
+
+def nc_version() -> str:
+    return load().nc_version().decode()
+
+
+def nc_create(cfg: nc_config):
+    h = ctypes.c_void_p()
+    _check(None, load().nc_create(ctypes.byref(cfg), ctypes.byref(h)))
+    return h
+
+
+def nc_destroy(ctx) -> None:
+    load().nc_destroy(ctx)
+
+
+def nc_set_box(ctx, L) -> None:
+    a = _d9(L)
+    _check(ctx, load().nc_set_box(ctx, _ptr(a)))
+
+
+def nc_set_flow(ctx, A, pol: nc_remap | None, t: float) -> None:
+    a = _d9(A)
+    _check(ctx, load().nc_set_flow(ctx, _ptr(a), ctypes.byref(pol) if pol is not None else None, float(t)))
+
+
+def nc_build_cells(ctx, q, n: int) -> None:
+    _check(ctx, load().nc_build_cells(ctx, _ptr(q), int(n)))
+
+
+def nc_compute_forces(ctx, q, n: int, F):
+    U = ctypes.c_double()
+    W = np.zeros(6)
+    _check(ctx, load().nc_compute_forces(ctx, _ptr(q), int(n), _ptr(F), ctypes.byref(U), _ptr(W)))
+    return U.value, W
+
+
+def nc_set_state(ctx, q, p, gid, n: int) -> None:
+    g = None if gid is None else np.ascontiguousarray(gid, dtype=np.int64)
+    _check(ctx, load().nc_set_state(ctx, _ptr(q), _ptr(p), _ptr(g), int(n)))
+
+
+def nc_step_sllod(ctx, dt: float, nsteps: int, want_uw: bool = True):
+    U = ctypes.c_double()
+    W = np.zeros(6)
+    _check(ctx, load().nc_step_sllod(ctx, float(dt), int(nsteps), ctypes.byref(U) if want_uw else None,
+                                     _ptr(W) if want_uw else None))
+    return (U.value, W) if want_uw else None
+
+
+def nc_get_state(ctx, q=None, p=None, want_gid=False):
+    n = ctypes.c_int64()
+    L = np.zeros(9)
+    t = ctypes.c_double()
+    _check(ctx, load().nc_get_state(ctx, None, None, None, ctypes.byref(n), _ptr(L), ctypes.byref(t)))
+    gid = np.zeros(n.value, dtype=np.int64) if want_gid else None
+    _check(ctx, load().nc_get_state(ctx, _ptr(q), _ptr(p), _ptr(gid), ctypes.byref(n), _ptr(L), ctypes.byref(t)))
+    return n.value, L.reshape(3, 3), t.value, gid
+
+
+def nc_get_cells(ctx, n: int, ncells: int, wrapped_dtype=None):
+    cell_of = np.zeros(n, dtype=np.int64)
+    cs = np.zeros(ncells + 1, dtype=np.int64)
+    dims = np.zeros(3, dtype=np.int32)
+    wq = np.zeros((n, 3), dtype=wrapped_dtype) if wrapped_dtype is not None else None
+    _check(ctx, load().nc_get_cells(ctx, _ptr(cell_of), _ptr(cs), _ptr(dims), _ptr(wq)))
+    return cell_of, cs, dims, wq
+
+
+def nc_get_pair_digest(ctx, n: int):
+    cnt = np.zeros(n, dtype=np.uint32)
+    hs = np.zeros(n, dtype=np.uint64)
+    hx = np.zeros(n, dtype=np.uint64)
+    _check(ctx, load().nc_get_pair_digest(ctx, _ptr(cnt), _ptr(hs), _ptr(hx)))
+    return cnt, hs, hx
+
+
+def nc_get_stats(ctx) -> dict:
+    s = nc_stats()
+    _check(ctx, load().nc_get_stats(ctx, ctypes.byref(s)))
+    return {"n": s.n, "dims": tuple(s.dims), "ncells": s.ncells, "candidates": s.candidates,
+            "interactions": s.interactions, "stencil_cells": s.stencil_cells, "rechecks": s.rechecks,
+            "U": s.U, "W": np.array(list(s.W)), "acc_evals": s.acc_evals, "acc_interactions": s.acc_interactions,
+            "acc_candidates": s.acc_candidates}
+
+
+def nc_get_stencil_histogram(ctx) -> np.ndarray:
+    h = np.zeros(64, dtype=np.int64)
+    _check(ctx, load().nc_get_stencil_histogram(ctx, _ptr(h)))
+    return h
+
+
+def nc_profile(ctx, enable: bool) -> None:
+    _check(ctx, load().nc_profile(ctx, 1 if enable else 0))
+
+
+def nc_profile_read(ctx) -> dict:
+    ms = np.zeros(8)
+    cnt = np.zeros(8, dtype=np.int64)
+    _check(ctx, load().nc_profile_read(ctx, _ptr(ms), _ptr(cnt)))
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_IDS)}
+
+
+def nc_launch_count(ctx) -> int:
+    return int(load().nc_launch_count(ctx))
+
+
+def nc_last_error(ctx) -> str:
+    return load().nc_last_error(ctx).decode()
+
+
+# ----------------------------------------------------------------- convenience
+
+def make_remap(policy: str, L0, tstar=0.0, om1=None, om2=None, beta=None, eps=0.0) -> nc_remap | None:
+    kinds = {"none": NC_REMAP_NONE, "le": NC_REMAP_LE, "kr": NC_REMAP_KR, "gkr": NC_REMAP_GKR}
+    r = nc_remap()
+    r.kind = kinds[policy]
+    for k, v in enumerate(_d9(L0)):
+        r.L0[k] = v
+    r.tstar = float(tstar or 0.0)
+    if om1 is not None:
+        for k in range(3):
+            r.omega1[k] = float(om1[k])
+            r.omega2[k] = float(om2[k])
+    if beta is not None:
+        r.beta[0], r.beta[1] = float(beta[0]), float(beta[1])
+    r.eps = float(eps)
+    return r
+
+
+class CellList:
+    """One nemdcell context: variant 'ds'|'do', precision 'f32'|'f64'."""
+
+    def __init__(self, variant="do", prec="f32", rc=2.5, eps=1.0, sigma=1.0, u_shift=None, mass=1.0,
+                 capacity=1 << 16, max_cells=0, device=0, stream=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("nemdcell needs a CUDA device (B200, sm_100a); no CPU fallback")
+        load()
+        if u_shift is None:
+            s6 = (sigma / rc) ** 6
+            u_shift = 4.0 * eps * (s6 * s6 - s6)
+        if stream is None:
+            stream = torch.cuda.current_stream(device).cuda_stream
+        cfg = nc_config()
+        cfg.variant = NC_DS if variant == "ds" else NC_DO
+        cfg.prec = NC_F32 if prec == "f32" else NC_F64
+        cfg.rc, cfg.eps, cfg.sigma, cfg.u_shift, cfg.mass = rc, eps, sigma, u_shift, mass
+        cfg.device = device
+        cfg.stream = ctypes.c_void_p(stream)
+        cfg.capacity = int(capacity)
+        cfg.max_cells = int(max_cells)
+        self.cfg = cfg
+        self.prec = prec
+        self.dtype = torch.float32 if prec == "f32" else torch.float64
+        self.np_dtype = np.float32 if prec == "f32" else np.float64
+        self.device = device
+        self.ctx = nc_create(cfg)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            nc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_box(self, L):
+        nc_set_box(self.ctx, L)
+
+    def set_flow(self, A, policy="none", t=0.0, **kw):
+        r = make_remap(policy, kw.pop("L0"), **kw) if policy != "none" or "L0" in kw else None
+        nc_set_flow(self.ctx, A, r, t)
+
+    def build_cells(self, q):
+        nc_build_cells(self.ctx, q, q.shape[0])
+
+    def compute_forces(self, q, F=None):
+        import torch
+
+        if F is None:
+            F = torch.empty_like(q) if hasattr(q, "data_ptr") and not isinstance(q, np.ndarray) else np.empty_like(q)
+        U, W = nc_compute_forces(self.ctx, q, q.shape[0], F)
+        return F, U, W
+
+    def set_state(self, q, p=None, gid=None):
+        nc_set_state(self.ctx, q, p, gid, q.shape[0])
+
+    def step(self, dt, nsteps=1, want_uw=True):
+        return nc_step_sllod(self.ctx, dt, nsteps, want_uw)
+
+    def get_state(self, q=None, p=None, want_gid=False):
+        return nc_get_state(self.ctx, q, p, want_gid)
+
+    def cells(self, n, ncells, wrapped=True):
+        return nc_get_cells(self.ctx, n, ncells, self.np_dtype if wrapped else None)
+
+    def digest(self, n):
+        return nc_get_pair_digest(self.ctx, n)
+
+    def stats(self):
+        return nc_get_stats(self.ctx)
+
+    def stencil_histogram(self):
+        return nc_get_stencil_histogram(self.ctx)
+
+    def profile(self, enable=True):
+        nc_profile(self.ctx, enable)
+
+    def profile_read(self):
+        return nc_profile_read(self.ctx)
+
+    def launches(self):
+        return nc_launch_count(self.ctx)

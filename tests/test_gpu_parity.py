@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north star):
+  * cell assignments, cell contents (cell_start) and wrapped positions: bit-exact
+  * pair sets: bit-exact (per-particle digests over (gid_j, image n))
+  * fp64: max |dF| <= 1e-12 RMS(F), |dU|/|U| <= 1e-12, max |dW| <= 1e-12 max|W|
+  * fp32: max |dF| <= 2e-5 RMS(F), |dU|/|U| <= 1e-6, max |dW| <= 1e-6 max|W|
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests.helpers import inputs, oracle_side
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": (1e-12, 1e-12, 1e-12), "f32": (2e-5, 1e-6, 1e-6)}
+VAR = {"ds": oracle.DS, "do": oracle.DO}
+
+
+def gpu_eval(w, q, variant, prec, digest=True):
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    cl = CellList(variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, capacity=max(1, len(q)))
+    cl.set_box(w.L)
+    qt = torch.from_numpy(np.ascontiguousarray(q)).cuda()
+    F, U, W = cl.compute_forces(qt)
+    torch.cuda.synchronize()
+    st = cl.stats()
+    cell_of, cs, dims, wq = cl.cells(len(q), st["ncells"])
+    dig = cl.digest(len(q)) if digest else None
+    out = dict(F=F.double().cpu().numpy(), U=U, W=W, stats=st, cell_of=cell_of, cs=cs, dims=dims, wq=wq, dig=dig,
+               hist=cl.stencil_histogram(), launches=cl.launches())
+    cl.close()
+    return out
+
+
+def check_against_oracle(w, q, variant, prec, idx=None):
+    g = gpu_eval(w, q, variant, prec)
+    qo = oracle_side(q, w.L, prec)
+    # wrapped positions: bit-exact (same stored values)
+    assert np.array_equal(g["wq"].astype(np.float64), qo)
+    # cells: bit-exact
+    cell, nh, dims = oracle.cell_keys(VAR[variant], qo, w.L, w.rc)
+    assert list(g["dims"]) == list(dims)
+    assert np.array_equal(g["cell_of"], cell)
+    cs, _ = oracle.cell_sort(cell, int(np.prod(dims.astype(np.int64))))
+    assert np.array_equal(g["cs"], cs)
+    # stencil histogram: exact
+    hist, _ = oracle.stencil_histogram(VAR[variant], w.L, w.rc)
+    assert np.array_equal(g["hist"], hist)
+    # pair sets + forces
+    r = oracle.evaluate(VAR[variant], qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx)
+    cnt, hs, hx = g["dig"]
+    sel = slice(None) if idx is None else idx
+    assert np.array_equal(cnt[sel], r.cnt)
+    assert np.array_equal(hs[sel], r.hsum)
+    assert np.array_equal(hx[sel], r.hxor)
+    tF, tU, tW = TOL[prec]
+    Fo = r.F
+    rms = np.sqrt(np.mean(Fo ** 2))
+    err = np.abs(g["F"][sel] - Fo).max()
+    assert err <= tF * rms, (err, rms, err / rms)
+    if idx is None:
+        assert abs(g["U"] - r.U) <= tU * abs(r.U), (g["U"], r.U)
+        assert np.abs(g["W"] - r.W).max() <= tW * np.abs(r.W).max()
+        assert g["stats"]["candidates"] == r.candidates
+        assert g["stats"]["interactions"] == r.interactions
+    return g, r
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c0_equilibrium_fp64_vs_brute_force(variant):
+    w, q = inputs(0, "f64")
+    g, r = check_against_oracle(w, q, variant, "f64")
+    b = oracle.evaluate(oracle.BRUTE, oracle_side(q, w.L, "f64"), w.L, w.rc)
+    assert np.array_equal(b.cnt, r.cnt) and np.array_equal(b.hsum, r.hsum)
+    # equilibrium: every neighborhood has 27 cells
+    assert g["hist"][27] == np.prod(g["dims"])
+
+
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c1_shear(variant, prec):
+    w, q = inputs(1, prec)
+    check_against_oracle(w, q, variant, prec)
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+@pytest.mark.parametrize("t0", [0.3, 2.0, 5.0, 9.0])
+def test_kr_boxes_scaled(variant, t0):
+    from paper_1412_3784_b200 import workloads as W
+
+    w, q = inputs(2, "f32", scale=2)
+    w.L = W.box_at(w.L0, w.A, "kr", t0, w.extra)
+    q = W.positions(w, dtype=np.float32, k=2)
+    try:
+        oracle.cell_keys(VAR[variant], oracle_side(q, w.L, "f32"), w.L, w.rc)
+    except ValueError:
+        pytest.skip("degenerate grid at this t0 for the scaled box")
+    check_against_oracle(w, q, variant, "f32")
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c2_full(variant):
+    w, q = inputs(2, "f32")
+    check_against_oracle(w, q, variant, "f32")
+
+
+@pytest.mark.parametrize("flow", ["uniaxial", "biaxial"])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c3_gkr_full(variant, flow):
+    w, q = inputs(3, "f32", flow=flow)
+    check_against_oracle(w, q, variant, "f32")
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c3_fp64(variant):
+    w, q = inputs(3, "f64", scale=2)
+    check_against_oracle(w, q, variant, "f64")
+
+
+def test_ds_equals_do_pair_set():
+    w, q = inputs(2, "f32")
+    a = gpu_eval(w, q, "ds", "f32")
+    b = gpu_eval(w, q, "do", "f32")
+    for x, y in zip(a["dig"], b["dig"]):
+        assert np.array_equal(x, y)
+    assert np.abs(a["F"] - b["F"]).max() < 1e-4 * np.sqrt(np.mean(a["F"] ** 2))
+
+
+def test_deterministic_bitwise():
+    w, q = inputs(2, "f32")
+    a = gpu_eval(w, q, "do", "f32", digest=False)
+    b = gpu_eval(w, q, "do", "f32", digest=False)
+    assert np.array_equal(a["F"], b["F"]) and a["U"] == b["U"] and np.array_equal(a["W"], b["W"])
+
+
+def test_wrap_of_outside_positions():
+    """Positions far outside Omega are wrapped by the same rule on both sides."""
+    w, q = inputs(1, "f64", scale=2)
+    rng = np.random.default_rng(5)
+    shift = rng.integers(-3, 4, size=(len(q), 3)) @ w.L.T
+    q2 = q + shift
+    check_against_oracle(w, q2, "do", "f64")
+
+
+def test_edge_cases():
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList, NcError
+
+    cl = CellList("do", "f32", rc=2.5, capacity=16)
+    L = np.eye(3) * 12.0
+    cl.set_box(L)
+    # empty input
+    q = torch.zeros((0, 3), dtype=torch.float32, device="cuda")
+    F, U, W = cl.compute_forces(q)
+    assert U == 0.0 and np.all(W == 0)
+    # single particle: no self interaction
+    q = torch.tensor([[1.0, 2.0, 3.0]], device="cuda")
+    F, U, W = cl.compute_forces(q)
+    assert U == 0.0 and torch.all(F == 0)
+    # two particles across the periodic boundary
+    q = torch.tensor([[0.2, 5.0, 5.0], [11.5, 5.0, 5.0]], device="cuda")
+    F, U, W = cl.compute_forces(q)
+    assert F[0, 0] > 0 and F[1, 0] < 0
+    # errors
+    with pytest.raises(NcError, match="NC_E_DEGENERATE"):
+        cl.set_box(np.eye(3) * 9.0)
+    with pytest.raises(NcError, match="NC_E_BOX"):
+        cl.set_box(np.diag([12.0, 12.0, -12.0]))
+    with pytest.raises(NcError, match="NC_E_FLOW"):
+        cl.set_flow(np.diag([0.1, 0.1, 0.1]), "none", 0.0, L0=L)
+    with pytest.raises(NcError, match="NC_E_OOM"):
+        cl.compute_forces(torch.zeros((17, 3), device="cuda"))
+    cl.close()
+
+
+def test_host_pointers_e2e():
+    """The ABI accepts host (numpy) buffers and copies through device staging."""
+    w, q = inputs(1, "f32", scale=2)
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    cl = CellList("do", "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    cl.set_box(w.L)
+    Fh, Uh, Wh = cl.compute_forces(np.ascontiguousarray(q))
+    Fd, Ud, Wd = cl.compute_forces(torch.from_numpy(q).cuda())
+    assert np.array_equal(Fh, Fd.cpu().numpy()) and Uh == Ud
+    cl.close()
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c4_full_size_sampled(variant):
+    """BASELINE configs[4] at full size (67M particles), in the bench's launch
+    configuration: cells exact on a sample, digests and forces on a sample."""
+    w, q = inputs(4, "f32")
+    rng = np.random.default_rng(44)
+    idx = np.sort(rng.choice(len(q), size=2000, replace=False))
+    g = gpu_eval(w, q, variant, "f32")
+    qo = oracle_side(q, w.L, "f32")
+    assert np.array_equal(g["wq"].astype(np.float64), qo)
+    cell, nh, dims = oracle.cell_keys(VAR[variant], qo, w.L, w.rc)
+    assert np.array_equal(g["cell_of"], cell)
+    r = oracle.evaluate(VAR[variant], qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx)
+    cnt, hs, hx = g["dig"]
+    assert np.array_equal(cnt[idx], r.cnt) and np.array_equal(hs[idx], r.hsum) and np.array_equal(hx[idx], r.hxor)
+    rms = np.sqrt(np.mean(g["F"] ** 2))
+    assert np.abs(g["F"][idx] - r.F).max() <= 2e-5 * rms
+    # Newton's third law over the whole system
+    assert np.abs(g["F"].sum(axis=0)).max() < 1e-3 * rms * np.sqrt(len(q))
