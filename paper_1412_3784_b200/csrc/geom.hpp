@@ -75,6 +75,7 @@ struct Geom {
   // potential
   double rc, rc2, eps, sig2, ushift;
   double band_lo, band_hi;  // canonical re-check band on r^2 (fp32 path)
+  double rsplit2;           // fp32-mode pairs with r^2 >= rsplit2 (and below band_lo) use fp32 force math
 };
 
 enum { GEOM_OK = 0, GEOM_BAD_BOX = 1, GEOM_DEGENERATE = 2 };

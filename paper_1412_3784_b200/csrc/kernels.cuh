@@ -283,7 +283,8 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
                               const typename V4<T>::t* __restrict__ qw, const typename V4<T>::t* __restrict__ p_in,
                               typename V4<T>::t* __restrict__ q_out, typename V4<T>::t* __restrict__ p_out,
                               uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
-                              uint32_t* __restrict__ nh_out, const __grid_constant__ Geom g) {
+                              float4* __restrict__ u32_out, uint32_t* __restrict__ nh_out,
+                              const __grid_constant__ Geom g) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t i = tmp[s];
@@ -304,6 +305,7 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
   if (p_in) p_out[dst] = p_in[i];
   gid_out[dst] = gg;
   u_out[dst] = make_double4(u[0], u[1], u[2], (double)dst);
+  u32_out[dst] = make_float4((float)u[0], (float)u[1], (float)u[2], __uint_as_float(dst));
   nh_out[dst] = pack_nh(cp.nh0, cp.nh1);
 }
 
@@ -317,28 +319,31 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
 // accumulated in fp64.  Membership is decided by the fp64 r^2, and inside a
 // 1e-12 relative band around r_c^2 by the canonical fp64 test of R16.
 // ---------------------------------------------------------------------------
-constexpr int K3_WARPS = 4;
-constexpr int K3_CAP = 256;     // staged neighbor particles per warp per chunk
-constexpr int K3_QCAP = 24;     // per-lane queue of filter survivors
+constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
+constexpr int K3_DUMMY = K3_CAP + 32;  // permanent far element (padding slot of the evaluation)
+constexpr int K3_STAGE = K3_CAP + 33;  // + up to S far sentinels so the filter needs no bounds checks
+constexpr int K3_QCAP = 32;     // per-lane queue of filter survivors (shared addresses / staged indices)
+constexpr int K3_UNROLL = 8;    // filter candidates per lane between queue-full votes
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
+constexpr int K3_CELLS = 4;     // cells per warp (= per block: one warp per block)
 constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, nonfinite
 constexpr double K3_BAND64 = 1e-12;
 
 template <typename T>
-struct K3Stage64 {  // fp32 mode: fp64 copy of the staged rotated cell-local coordinates
-  double x[K3_CAP], y[K3_CAP], z[K3_CAP];
+struct K3Stage64 {  // fp32 mode: fp32 image brackets of the entries
+  float Bf[K3_MAXE][3];
 };
 template <>
 struct K3Stage64<double> {  // fp64 mode: stage holds LAB positions; packed DO home shift of each j
-  uint32_t nh[K3_CAP];
+  uint32_t nh[K3_STAGE];
 };
 
 template <typename T>
 struct K3Smem {
-  typename V4<T>::t stage[K3_CAP];  // filter copy, .w = sorted index
+  typename V4<T>::t stage[K3_STAGE];  // filter copy, .w = sorted index
   K3Stage64<T> s64;
-  uint16_t queue[K3_QCAP][32];
-  uint8_t sent[K3_CAP];
+  uint32_t queue[K3_QCAP][32];
+  uint8_t sent[K3_STAGE];
   uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
   int32_t e_n[K3_MAXE][3];
   double e_B[K3_MAXE][3];
@@ -419,6 +424,9 @@ __device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int 
   return total;
 }
 
+// Per-lane accumulators: F (lab frame in fp64 mode, rotated in fp32 mode),
+// u = sum s6 (s6 - 1), w = sum fr d (x) d; U_i = 2 eps u - cnt u_shift / 2 and
+// W_i = w / 2 are formed once at the end (exact algebra of R11/R12).
 struct Acc {
   double fx, fy, fz, u, w0, w1, w2, w3, w4, w5;
   uint32_t cnt, nrc;
@@ -494,19 +502,26 @@ __device__ __forceinline__ void image_of(const Geom& g, const K3Smem<T>& sm, uin
   }
 }
 
-__device__ __forceinline__ void lj_accumulate(const Geom& g, Acc& acc, double dx, double dy, double dz, double r2) {
-  // 1/r^2: fp32 seed + two Newton steps in fp64
-  double ir2 = (double)__frcp_rn((float)r2);
-  ir2 = ir2 * (2.0 - r2 * ir2);
-  ir2 = ir2 * (2.0 - r2 * ir2);
-  double s2 = g.sig2 * ir2;
+__device__ __forceinline__ double rcp64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  y = y * (2.0 - x * y);  // Newton: ~2^-23 -> 2^-46
+  y = y * (2.0 - x * y);  //         -> full fp64
+  return y;
+}
+
+// LJ 12-6 pair with energy shift (R11): fr = 24 eps s6 (2 s6 - 1) / r^2.
+__device__ __forceinline__ void lj_accumulate(double sig2, double eps24, Acc& acc, double dx, double dy, double dz,
+                                              double r2) {
+  double ir2 = rcp64(r2);
+  double s2 = sig2 * ir2;
   double s6 = s2 * s2 * s2;
-  double fr = 24.0 * g.eps * s6 * (2.0 * s6 - 1.0) * ir2;
-  acc.fx -= fr * dx; acc.fy -= fr * dy; acc.fz -= fr * dz;
-  acc.u += 0.5 * (4.0 * g.eps * s6 * (s6 - 1.0) - g.ushift);
-  double hf = 0.5 * fr;
-  acc.w0 += hf * dx * dx; acc.w1 += hf * dy * dy; acc.w2 += hf * dz * dz;
-  acc.w3 += hf * dx * dy; acc.w4 += hf * dx * dz; acc.w5 += hf * dy * dz;
+  double fr = (eps24 * s6) * (2.0 * s6 - 1.0) * ir2;
+  double tx = fr * dx, ty = fr * dy, tz = fr * dz;
+  acc.fx -= tx; acc.fy -= ty; acc.fz -= tz;
+  acc.u += s6 * s6 - s6;
+  acc.w0 += tx * dx; acc.w1 += ty * dy; acc.w2 += tz * dz;
+  acc.w3 += tx * dy; acc.w4 += tx * dz; acc.w5 += ty * dz;
   acc.cnt++;
 }
 
@@ -521,45 +536,53 @@ __device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32
   }
 }
 
-// Evaluate the queued filter survivors of every lane (warp-uniform loop).
+// Evaluate ONE queued survivor t of this lane (fp32 mode: fp64 rotated
+// cell-local coordinates; fp64 mode: exact lab-frame displacement).
+template <typename T, bool DIGEST>
+__device__ __forceinline__ void eval_one(const Geom& g, const PairCtx<T>& pc, const K3Smem<T>& sm, Acc& acc,
+                                         uint32_t t, double sig2, double eps24) {
+  if constexpr (sizeof(T) == 4) {
+    uint32_t j = w_to_idx(sm.stage[t].w);
+    double dx = sm.s64.x[t] - pc.ux, dy = sm.s64.y[t] - pc.uy, dz = sm.s64.z[t] - pc.uz;
+    double r2 = dx * dx + dy * dy + dz * dz;
+    bool ok = (j != pc.my) && (r2 < pc.hi64);
+    int n0 = 0, n1 = 0, n2 = 0;
+    if (ok && (DIGEST || r2 >= pc.lo64)) {
+      image_of<T>(g, sm, t, g.variant == 1 ? pc.nh[j] : 0u, pc.nh_i, n0, n1, n2);
+      if (r2 >= pc.lo64) {
+        ok = canonical_in<T>(g, pc.qs, pc.my, j, n0, n1, n2);
+        acc.nrc++;
+      }
+    }
+    if (ok) {
+      lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
+      digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
+    }
+  } else {
+    // fp64 mode: the filter already applied the canonical test; exact d for the force
+    typename V4<T>::t v = sm.stage[t];
+    uint32_t j = w_to_idx(v.w);
+    int n0, n1, n2;
+    image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
+    double dx = exact_d(g, 0, v.x, pc.ux, n0, n1, n2);
+    double dy = exact_d(g, 1, v.y, pc.uy, n0, n1, n2);
+    double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
+    double r2 = dx * dx + dy * dy + dz * dz;
+    lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
+    digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
+  }
+}
+
+// Evaluate the queued filter survivors of every lane (warp-uniform loop, two
+// independent entries per iteration for instruction-level parallelism).
 template <typename T, bool DIGEST>
 __device__ __forceinline__ void eval_queue(const Geom& g, const PairCtx<T>& pc, K3Smem<T>& sm, Acc& acc, int qlen,
                                            int lane) {
   int qmax = __reduce_max_sync(0xffffffffu, qlen);
-  for (int k = 0; k < qmax; ++k) {
-    if (k < qlen) {
-      uint32_t t = sm.queue[k][lane];
-      if constexpr (sizeof(T) == 4) {
-        uint32_t j = w_to_idx(sm.stage[t].w);
-        double dx = sm.s64.x[t] - pc.ux, dy = sm.s64.y[t] - pc.uy, dz = sm.s64.z[t] - pc.uz;
-        double r2 = dx * dx + dy * dy + dz * dz;
-        bool ok = (j != pc.my) && (r2 < pc.hi64);
-        int n0 = 0, n1 = 0, n2 = 0;
-        if (ok && (DIGEST || r2 >= pc.lo64)) {
-          image_of<T>(g, sm, t, g.variant == 1 ? pc.nh[j] : 0u, pc.nh_i, n0, n1, n2);
-          if (r2 >= pc.lo64) {
-            ok = canonical_in<T>(g, pc.qs, pc.my, j, n0, n1, n2);
-            acc.nrc++;
-          }
-        }
-        if (ok) {
-          lj_accumulate(g, acc, dx, dy, dz, r2);
-          digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
-        }
-      } else {
-        // fp64 mode: the filter already applied the canonical test; exact d for the force
-        typename V4<T>::t v = sm.stage[t];
-        uint32_t j = w_to_idx(v.w);
-        int n0, n1, n2;
-        image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
-        double dx = exact_d(g, 0, v.x, pc.ux, n0, n1, n2);
-        double dy = exact_d(g, 1, v.y, pc.uy, n0, n1, n2);
-        double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
-        double r2 = dx * dx + dy * dy + dz * dz;
-        lj_accumulate(g, acc, dx, dy, dz, r2);
-        digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
-      }
-    }
+  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
+  for (int k = 0; k < qmax; k += 2) {
+    if (k < qlen) eval_one<T, DIGEST>(g, pc, sm, acc, sm.queue[k][lane], sig2, eps24);
+    if (k + 1 < qlen) eval_one<T, DIGEST>(g, pc, sm, acc, sm.queue[k + 1][lane], sig2, eps24);
   }
 }
 
@@ -590,18 +613,233 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// One warp per center cell; blocks never span a cell layer (deterministic
-// layer-ordered partials).  grid = l3 * blocks_per_layer.
+// Far-away sentinel for padding the staged list (never passes the filter).
+template <typename T> __device__ __forceinline__ typename V4<T>::t far4();
+template <> __device__ __forceinline__ float4 far4<float>() { return make_float4(1e30f, 1e30f, 1e30f, 0.f); }
+template <> __device__ __forceinline__ double4 far4<double>() { return make_double4(1e300, 1e300, 1e300, 0.0); }
+
+// Filter stream s of the staged chunk: t = s, s+S, ... for `iters` steps
+// (warp-uniform count; the S sentinels after the chunk make every access
+// valid).  Survivors go to this lane's queue; the queue is evaluated when
+// any lane could overflow.
 template <typename T, bool DIGEST>
-__global__ void __launch_bounds__(K3_WARPS * 32)
-k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
+__device__ __forceinline__ void filter_chunk(const Geom& g, const PairCtx<T>& pc, K3Smem<T>& sm, Acc& acc, int s,
+                                             int S, int iters, int lane) {
+  uint32_t t = (uint32_t)s;
+  int qlen = 0;
+  int it = 0;
+  const int main_iters = iters - iters % K3_UNROLL;
+  for (; it < main_iters; it += K3_UNROLL) {
+#pragma unroll
+    for (int k = 0; k < K3_UNROLL; ++k) {
+      bool hit = filter_one<T>(g, pc, sm, t);
+      sm.queue[qlen][lane] = t;
+      qlen += hit ? 1 : 0;
+      t += (uint32_t)S;
+    }
+    if (__any_sync(0xffffffffu, qlen > K3_QCAP - K3_UNROLL)) {
+      eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
+      qlen = 0;
+    }
+  }
+  for (; it < iters; ++it) {
+    bool hit = filter_one<T>(g, pc, sm, t);
+    sm.queue[qlen][lane] = t;
+    qlen += hit ? 1 : 0;
+    t += (uint32_t)S;
+  }
+  eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Hot path of NC_F32 (hand-scheduled): fp32 filter with shared-address queues
+// (11 instructions per candidate: LDS.128, 6 FP, FSETP + predicated IADD,
+// STS, pointer step) and a branch-light fp64 evaluation of two survivors per
+// iteration.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// a += 128 if r2 < hi (one FSETP + one predicated IADD)
+__device__ __forceinline__ uint32_t bump_if_less(uint32_t a, float r2, float hi) {
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, 128;\n\t}" : "+r"(a) : "f"(r2), "f"(hi));
+  return a;
+}
+
+// fp32 accumulators of the far-pair tier (folded into the fp64 Acc after each evaluation)
+struct Acc32 {
+  float fx, fy, fz, u, w0, w1, w2, w3, w4, w5;
+  uint32_t cnt;
+};
+
+__device__ __forceinline__ void fold32(Acc& acc, Acc32& a) {
+  acc.fx += a.fx; acc.fy += a.fy; acc.fz += a.fz; acc.u += a.u;
+  acc.w0 += a.w0; acc.w1 += a.w1; acc.w2 += a.w2; acc.w3 += a.w3; acc.w4 += a.w4; acc.w5 += a.w5;
+  acc.cnt += a.cnt;
+  a = Acc32{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u};
+}
+
+// Close tier: survivors with r < r_split (large forces), in the r_c band, or
+// all survivors in digest mode -- fp64 from the fp64 staged coordinates,
+// canonical membership inside the 1e-12 band.  Two per iteration.
+template <bool DIGEST>
+__device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                               int qlen, int lane, uint32_t stage0, const double4* __restrict__ u64) {
+  const int qmax = __reduce_max_sync(0xffffffffu, qlen);
+  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
+  const uint32_t dummy = stage0 + 16u * K3_DUMMY;
+  for (int k = 0; k < qmax; k += 2) {
+    const uint32_t aa = k < qlen ? sm.queue[k][lane] : dummy;
+    const uint32_t ab = k + 1 < qlen ? sm.queue[k + 1][lane] : dummy;
+    const uint32_t ta = (aa - stage0) >> 4, tb = (ab - stage0) >> 4;
+    const uint32_t ja = __float_as_uint(sm.stage[ta].w), jb = __float_as_uint(sm.stage[tb].w);
+    const int ea = sm.sent[ta], eb = sm.sent[tb];
+    const double4 pa = u64[ja], pb = u64[jb];
+    const double dxa = (pa.x + sm.e_B[ea][0]) - pc.ux, dya = (pa.y + sm.e_B[ea][1]) - pc.uy,
+                 dza = (pa.z + sm.e_B[ea][2]) - pc.uz;
+    const double dxb = (pb.x + sm.e_B[eb][0]) - pc.ux, dyb = (pb.y + sm.e_B[eb][1]) - pc.uy,
+                 dzb = (pb.z + sm.e_B[eb][2]) - pc.uz;
+    const double r2a = dxa * dxa + dya * dya + dza * dza;
+    const double r2b = dxb * dxb + dyb * dyb + dzb * dzb;
+    bool oka = (ja != pc.my) && (r2a < pc.hi64);
+    bool okb = (jb != pc.my) && (r2b < pc.hi64);
+    int na0 = 0, na1 = 0, na2 = 0, nb0 = 0, nb1 = 0, nb2 = 0;
+    if (DIGEST || (oka && r2a >= pc.lo64) || (okb && r2b >= pc.lo64)) {  // rare: canonical band / digest
+      if (oka) {
+        image_of<float>(g, sm, ta, g.variant == 1 ? pc.nh[ja] : 0u, pc.nh_i, na0, na1, na2);
+        if (r2a >= pc.lo64) { oka = canonical_in<float>(g, pc.qs, pc.my, ja, na0, na1, na2); acc.nrc++; }
+      }
+      if (okb) {
+        image_of<float>(g, sm, tb, g.variant == 1 ? pc.nh[jb] : 0u, pc.nh_i, nb0, nb1, nb2);
+        if (r2b >= pc.lo64) { okb = canonical_in<float>(g, pc.qs, pc.my, jb, nb0, nb1, nb2); acc.nrc++; }
+      }
+    }
+    const double ira = rcp64(r2a), irb = rcp64(r2b);
+    const double s2a = sig2 * ira, s2b = sig2 * irb;
+    const double s6a = s2a * s2a * s2a, s6b = s2b * s2b * s2b;
+    double fra = (eps24 * s6a) * (2.0 * s6a - 1.0) * ira;
+    double frb = (eps24 * s6b) * (2.0 * s6b - 1.0) * irb;
+    fra = oka ? fra : 0.0;
+    frb = okb ? frb : 0.0;
+    const double txa = fra * dxa, tya = fra * dya, tza = fra * dza;
+    const double txb = frb * dxb, tyb = frb * dyb, tzb = frb * dzb;
+    acc.fx -= txa + txb; acc.fy -= tya + tyb; acc.fz -= tza + tzb;
+    acc.u += (oka ? s6a * s6a - s6a : 0.0) + (okb ? s6b * s6b - s6b : 0.0);
+    acc.w0 += txa * dxa + txb * dxb; acc.w1 += tya * dya + tyb * dyb; acc.w2 += tza * dza + tzb * dzb;
+    acc.w3 += txa * dya + txb * dyb; acc.w4 += txa * dza + txb * dzb; acc.w5 += tya * dza + tyb * dzb;
+    acc.cnt += (oka ? 1u : 0u) + (okb ? 1u : 0u);
+    if (DIGEST) {
+      if (oka) digest_add<DIGEST>(acc, pc.gid, ja, na0, na1, na2);
+      if (okb) digest_add<DIGEST>(acc, pc.gid, jb, nb0, nb1, nb2);
+    }
+  }
+}
+
+// Evaluate this lane's queued survivors.  Far tier (r_split^2 <= r^2 below
+// the lower edge of the fp32 cutoff band: definitely inside, |f| small) in
+// fp32; everything else is compacted in place and goes to the fp64 tier.
+template <bool DIGEST>
+__device__ __forceinline__ void eval_pairs_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                               Acc32& a32, int qlen, int lane, uint32_t stage0,
+                                               const double4* __restrict__ u64) {
+  int nclose = qlen;
+  if (!DIGEST) {
+    const int qmax = __reduce_max_sync(0xffffffffu, qlen);
+    const float split2 = (float)g.rsplit2, lo32 = (float)g.band_lo, sig2 = (float)g.sig2, eps24 = (float)(24.0 * g.eps);
+    const uint32_t dummy = stage0 + 16u * K3_DUMMY;
+    nclose = 0;
+    for (int k = 0; k < qmax; ++k) {
+      const bool valid = k < qlen;
+      const uint32_t a = valid ? sm.queue[k][lane] : dummy;
+      const float4 v = lds128(a);
+      const float dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      const bool far = valid && r2 >= split2 && r2 < lo32;
+      sm.queue[nclose][lane] = a;   // in-place compaction (nclose <= k)
+      nclose += (valid && !far) ? 1 : 0;
+      float ir2;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
+      const float s2 = sig2 * ir2;
+      const float s6 = s2 * s2 * s2;
+      float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
+      fr = far ? fr : 0.0f;
+      const float tx = fr * dx, ty = fr * dy, tz = fr * dz;
+      a32.fx -= tx; a32.fy -= ty; a32.fz -= tz;
+      a32.u += far ? s6 * s6 - s6 : 0.0f;
+      a32.w0 = fmaf(tx, dx, a32.w0); a32.w1 = fmaf(ty, dy, a32.w1); a32.w2 = fmaf(tz, dz, a32.w2);
+      a32.w3 = fmaf(tx, dy, a32.w3); a32.w4 = fmaf(tx, dz, a32.w4); a32.w5 = fmaf(ty, dz, a32.w5);
+      a32.cnt += far ? 1u : 0u;
+    }
+    __syncwarp();
+  }
+  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64);
+}
+
+template <bool DIGEST>
+__device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                                 Acc32& a32, int s, int S, int iters, int lane,
+                                                 const double4* __restrict__ u64) {
+  const uint32_t stage0 = smem_u32(&sm.stage[0]);
+  const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
+  const uint32_t qlim = q0 + 128u * (K3_QCAP - K3_UNROLL);
+  const uint32_t step = 16u * (uint32_t)S;
+  const float ux = pc.fx, uy = pc.fy, uz = pc.fz, hi = pc.hi;
+  uint32_t sa = stage0 + 16u * (uint32_t)s;
+  uint32_t qa = q0;
+  int it = 0;
+  const int main_iters = iters - iters % K3_UNROLL;
+  for (;;) {
+    // filter groups of K3_UNROLL until some lane's queue is nearly full
+    bool full = false;
+    while (it < main_iters) {
+#pragma unroll
+      for (int k = 0; k < K3_UNROLL; ++k) {
+        float4 v = lds128(sa);
+        float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
+        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        sts32(qa, sa);
+        qa = bump_if_less(qa, r2, hi);
+        sa += step;
+      }
+      it += K3_UNROLL;
+      if (__any_sync(0xffffffffu, qa > qlim)) { full = true; break; }
+    }
+    if (!full) {  // remainder (< K3_UNROLL iterations; every queue has room for them)
+      for (; it < iters; ++it) {
+        float4 v = lds128(sa);
+        float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
+        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        sts32(qa, sa);
+        qa = bump_if_less(qa, r2, hi);
+        sa += step;
+      }
+    }
+    __syncwarp();
+    eval_pairs_f32<DIGEST>(g, pc, sm, acc, a32, (int)((qa - q0) >> 7), lane, stage0, u64);  // the single call site
+    qa = q0;
+    if (it >= iters) break;
+  }
+}
+
+// One warp per block; each warp handles K3_CELLS consecutive cells of one
+// cell layer, so block partials are layer-aligned and their fixed-order sums
+// are independent of timing (determinism).  grid = l3 * blocks_per_layer.
+template <typename T, bool DIGEST>
+__global__ void __launch_bounds__(32, 14)
+k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
         const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
         uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  K3Smem<T>& sm = reinterpret_cast<K3Smem<T>*>(smraw)[warp];
-  __shared__ double wpart[K3_WARPS][NPART];
+  const int lane = threadIdx.x & 31;
+  K3Smem<T>& sm = *reinterpret_cast<K3Smem<T>*>(smraw);
 
   const int l1 = g.dims[0], l2 = g.dims[1];
   const int layer = blockIdx.x / bpl;
@@ -619,8 +857,16 @@ k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
   pc.gid = gid;
 
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+  if constexpr (sizeof(T) == 4) {
+    if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
+      sm.stage[K3_DUMMY] = far4<T>();
+      sm.sent[K3_DUMMY] = K3_MAXE - 1;
+      sm.e_B[K3_MAXE - 1][0] = 1e150; sm.e_B[K3_MAXE - 1][1] = 1e150; sm.e_B[K3_MAXE - 1][2] = 1e150;
+    }
+    __syncwarp();
+  }
 
-  for (int cl = cbeg + warp; cl < cend; cl += K3_WARPS) {
+  for (int cl = cbeg; cl < cend; ++cl) {
     const int a0 = cl % l1, a1 = cl / l1, a2 = layer;
     const uint32_t cid = (uint32_t)cl + (uint32_t)per_layer * (uint32_t)layer;
     const int nst = build_entries<T>(g, a0, a1, a2, sm, lane);
@@ -658,19 +904,23 @@ k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
     for (int ib = 0; ib < ni; ib += 32) {
       const int nb = min(32, ni - ib);
       const int S = 32 / nb;               // streams over the j list
-      const int il = lane % nb, s = lane / nb;
-      const bool act = s < S;
+      const int il = lane % nb;
+      const bool act = lane < S * nb;
+      const int s = act ? lane / nb : 0;   // ghost lanes shadow stream 0 (no extra smem addresses)
       pc.my = ibase + ib + il;
       if constexpr (sizeof(T) == 4) {
         double4 ui = u[pc.my];
+        float4 uf = u32[pc.my];
         pc.ux = ui.x; pc.uy = ui.y; pc.uz = ui.z;
-        pc.fx = (T)ui.x; pc.fy = (T)ui.y; pc.fz = (T)ui.z;
+        pc.fx = act ? uf.x : -1e30f;  // ghost lanes never pass the filter
+        pc.fy = uf.y; pc.fz = uf.z;
       } else {
         typename V4<T>::t qi = qs[pc.my];
-        pc.ux = qi.x; pc.uy = qi.y; pc.uz = qi.z;
+        pc.ux = act ? qi.x : -1e300; pc.uy = qi.y; pc.uz = qi.z;
       }
       pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
       Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+      Acc32 a32 = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u};
 
       int e0 = 0;
       while (e0 < nst) {
@@ -685,67 +935,71 @@ k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
         }
         if (e1 == e0) e1 = e0 + 1;  // unreachable: a cell holds fewer than K3_CAP particles
         const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
-        // stage: lane-per-entry, loop over the entry's particles; image shift B applied in fp64
-        for (int eb = e0; eb < e1; eb += 32) {
-          int e = eb + lane;
-          uint32_t cnt = 0, st = 0, dst = 0;
-          double B0 = 0, B1 = 0, B2 = 0;
-          if (e < e1) {
-            cnt = sm.e_cnt[e]; st = sm.e_start[e]; dst = sm.e_off[e] - base_off;
-            B0 = sm.e_B[e][0]; B1 = sm.e_B[e][1]; B2 = sm.e_B[e][2];
+        // stage the chunk: staged element t <- particle e_start[e] + (t - e_off[e]) of entry e, shifted
+        // by the entry's image bracket B_e in fp64.  Flattened over t (lanes read consecutive particles of
+        // each neighbor cell: coalesced), two elements per lane in flight.
+        if constexpr (sizeof(T) == 4) {
+          // (1) entry id of every staged element, fp32 brackets; (2) flattened coalesced copy
+          for (int eb = e0; eb < e1; eb += 32) {
+            const int e = eb + lane;
+            if (e < e1) {
+              const uint32_t dst = sm.e_off[e] - base_off, cnt = sm.e_cnt[e];
+              for (uint32_t k = 0; k < cnt; ++k) sm.sent[dst + k] = (uint8_t)e;
+              sm.s64.Bf[e][0] = (float)sm.e_B[e][0];
+              sm.s64.Bf[e][1] = (float)sm.e_B[e][1];
+              sm.s64.Bf[e][2] = (float)sm.e_B[e][2];
+            }
           }
-          uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
-          for (uint32_t t = 0; t < cmax; ++t) {
-            if (t < cnt) {
-              if constexpr (sizeof(T) == 4) {
-                double4 v = u[st + t];
-                double x = v.x + B0, y = v.y + B1, z = v.z + B2;
-                sm.stage[dst + t] = mk4((T)x, (T)y, (T)z, idx_to_w(st + t, T()));
-                sm.s64.x[dst + t] = x; sm.s64.y[dst + t] = y; sm.s64.z[dst + t] = z;
-              } else {
-                typename V4<T>::t v = qs[st + t];
-                sm.stage[dst + t] = mk4(v.x, v.y, v.z, idx_to_w(st + t, T()));
-                sm.s64.nh[dst + t] = g.variant == 1 ? nh[st + t] : 0u;
+          __syncwarp();
+          for (uint32_t t0 = 0; t0 < ctot; t0 += 64) {
+            const uint32_t ta = t0 + lane, tb = t0 + 32 + lane;
+            const bool va = ta < ctot, vb = tb < ctot;
+            const int ea = va ? sm.sent[ta] : e0, eb = vb ? sm.sent[tb] : e0;
+            const uint32_t ja = sm.e_start[ea] + ta - (sm.e_off[ea] - base_off);
+            const uint32_t jb = sm.e_start[eb] + tb - (sm.e_off[eb] - base_off);
+            const float4 pa = va ? u32[ja] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 pb = vb ? u32[jb] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (va) sm.stage[ta] = make_float4(pa.x + sm.s64.Bf[ea][0], pa.y + sm.s64.Bf[ea][1], pa.z + sm.s64.Bf[ea][2], pa.w);
+            if (vb) sm.stage[tb] = make_float4(pb.x + sm.s64.Bf[eb][0], pb.y + sm.s64.Bf[eb][1], pb.z + sm.s64.Bf[eb][2], pb.w);
+          }
+        } else {
+          for (int eb = e0; eb < e1; eb += 32) {
+            int e = eb + lane;
+            uint32_t cnt = 0, st = 0, dst = 0;
+            if (e < e1) { cnt = sm.e_cnt[e]; st = sm.e_start[e]; dst = sm.e_off[e] - base_off; }
+            uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
+            for (uint32_t k = 0; k < cmax; ++k) {
+              if (k < cnt) {
+                typename V4<T>::t v = qs[st + k];
+                sm.stage[dst + k] = mk4(v.x, v.y, v.z, idx_to_w(st + k, T()));
+                sm.s64.nh[dst + k] = g.variant == 1 ? nh[st + k] : 0u;
+                sm.sent[dst + k] = (uint8_t)e;
               }
-              sm.sent[dst + t] = (uint8_t)e;
             }
           }
         }
+        // S far sentinels after the chunk (indices ctot .. ctot+S-1)
+        if (lane < S) {
+          sm.stage[ctot + lane] = far4<T>();
+          sm.sent[ctot + lane] = 0;
+          if constexpr (sizeof(T) == 8) sm.s64.nh[ctot + lane] = 0u;
+        }
         __syncwarp();
-        // filter: stream s takes t = s, s+S, ...; all lanes run the same trip count
         const int iters = (int)((ctot + S - 1) / S);
-        int qlen = 0;
-        int it = 0;
-        for (; it + 4 <= iters; it += 4) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t t = (uint32_t)(s + (it + k) * S);
-            bool valid = act && t < ctot;
-            bool hit = filter_one<T>(g, pc, sm, valid ? t : 0u);
-            sm.queue[qlen][lane] = (uint16_t)t;
-            qlen += (valid && hit) ? 1 : 0;
-          }
-          if (__any_sync(0xffffffffu, qlen > K3_QCAP - 4)) {
-            eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
-            qlen = 0;
-          }
+        if constexpr (sizeof(T) == 4) {
+          filter_chunk_f32<DIGEST>(g, pc, sm, acc, a32, s, S, iters, lane, u);
+        } else {
+          filter_chunk<T, DIGEST>(g, pc, sm, acc, s, S, iters, lane);
         }
-        for (; it < iters; ++it) {
-          uint32_t t = (uint32_t)(s + it * S);
-          bool valid = act && t < ctot;
-          bool hit = filter_one<T>(g, pc, sm, valid ? t : 0u);
-          sm.queue[qlen][lane] = (uint16_t)t;
-          qlen += (valid && hit) ? 1 : 0;
-        }
-        eval_queue<T, DIGEST>(g, pc, sm, acc, qlen, lane);
         __syncwarp();
         e0 = e1;
       }
 
+      if constexpr (sizeof(T) == 4) fold32(acc, a32);
       // combine the S streams of each i (fixed order s = 1, 2, ...)
       for (int s2 = 1; s2 < S; ++s2) {
         int src = lane + s2 * nb;
-        bool take = (s == 0) && (src < 32);
+        bool take = (lane < nb) && (src < 32);
         src &= 31;
         acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
         acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
@@ -761,7 +1015,9 @@ k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
           if (take) { acc.hs += h1; acc.hx ^= h2; }
         }
       }
-      const bool owner = (s == 0);
+      const bool owner = (lane < nb);
+      // fold the factors of R11/R12: U_i = 2 eps sum s6(s6-1) - cnt u_shift / 2; W_i = sum fr d d / 2
+      const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
       if (owner) {
         double Fx = acc.fx, Fy = acc.fy, Fz = acc.fz;
         if constexpr (sizeof(T) == 4) {  // lab-frame force F = Q F_rot
@@ -772,27 +1028,31 @@ k_pairs(const double4* __restrict__ u, const uint32_t* __restrict__ cs,
         Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, (T)0);
         if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
       }
-      double fchk = owner ? acc.fx + acc.fy + acc.fz + acc.u : 0.0;
-      tU += warp_sum_d(owner ? acc.u : 0.0);
-      tW[0] += warp_sum_d(owner ? acc.w0 : 0.0); tW[1] += warp_sum_d(owner ? acc.w1 : 0.0);
-      tW[2] += warp_sum_d(owner ? acc.w2 : 0.0); tW[3] += warp_sum_d(owner ? acc.w3 : 0.0);
-      tW[4] += warp_sum_d(owner ? acc.w4 : 0.0); tW[5] += warp_sum_d(owner ? acc.w5 : 0.0);
+      double fchk = owner ? acc.fx + acc.fy + acc.fz + Ui : 0.0;
+      tU += warp_sum_d(owner ? Ui : 0.0);
+      tW[0] += warp_sum_d(owner ? 0.5 * acc.w0 : 0.0); tW[1] += warp_sum_d(owner ? 0.5 * acc.w1 : 0.0);
+      tW[2] += warp_sum_d(owner ? 0.5 * acc.w2 : 0.0); tW[3] += warp_sum_d(owner ? 0.5 * acc.w3 : 0.0);
+      tW[4] += warp_sum_d(owner ? 0.5 * acc.w4 : 0.0); tW[5] += warp_sum_d(owner ? 0.5 * acc.w5 : 0.0);
       tI += warp_sum_d(owner ? (double)acc.cnt : 0.0);
       tR += warp_sum_d(owner ? (double)acc.nrc : 0.0);
       tNF += warp_sum_d(isfinite(fchk) ? 0.0 : 1.0);
     }
   }
-  if (lane == 0) {
-    double* wp = wpart[warp];
-    wp[0] = tU;
-    for (int k = 0; k < 6; ++k) wp[1 + k] = tW[k];
-    wp[7] = tI; wp[8] = tC; wp[9] = tS; wp[10] = tR; wp[11] = tNF;
-  }
-  __syncthreads();
-  if (threadIdx.x < NPART) {
+  if (lane < NPART) {
     double v = 0;
-    for (int w = 0; w < K3_WARPS; ++w) v += wpart[w][threadIdx.x];
-    bpart[(int64_t)blockIdx.x * NPART + threadIdx.x] = v;
+    if (lane == 0) v = tU;
+    else if (lane == 1) v = tW[0];
+    else if (lane == 2) v = tW[1];
+    else if (lane == 3) v = tW[2];
+    else if (lane == 4) v = tW[3];
+    else if (lane == 5) v = tW[4];
+    else if (lane == 6) v = tW[5];
+    else if (lane == 7) v = tI;
+    else if (lane == 8) v = tC;
+    else if (lane == 9) v = tS;
+    else if (lane == 10) v = tR;
+    else v = tNF;
+    bpart[(int64_t)blockIdx.x * NPART + lane] = v;
   }
 }
 

@@ -48,6 +48,7 @@ struct nc_ctx {
 
   // shared transient
   double4* u = nullptr;   // sorted cell-local rotated coords, fp64 (w = sorted index)
+  float4* u32 = nullptr;  // the same in fp32 (w = sorted index bits): the filter's staging source
   uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr, *tmp = nullptr, *tmpgid = nullptr;
   uint32_t *counts = nullptr, *cs = nullptr, *bsum = nullptr, *tot = nullptr;
   double *bpart = nullptr, *lpart = nullptr, *part_tot = nullptr, *part_acc = nullptr;
@@ -135,7 +136,7 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-int cells_per_block() { return 2 * K3_WARPS; }
+int cells_per_block() { return K3_CELLS; }
 
 nc_status apply_box(nc_ctx* ctx, const double* L) {
   Geom g;
@@ -158,6 +159,9 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   double tau = ctx->cfg.prec == NC_F32 ? 2e-5 : 1e-10;  // re-check band, DESIGN.md section 5
   g.band_lo = g.rc2 * (1.0 - tau);
   g.band_hi = g.rc2 * (1.0 + tau);
+  // two-tier evaluation: fp32 force math only where the LJ force is small
+  // (r >= 1.2 sigma: |f| <= 2.4 eps/sigma), fp64 for closer pairs
+  g.rsplit2 = 1.44 * g.sig2;
   ctx->g = g;
   ctx->have_box = true;
   return NC_OK;
@@ -197,7 +201,7 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
     prof_end(ctx, NC_K_SCATTER);
     prof_begin(ctx);
     k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->key, ctx->cs, qwrap, p_in, q_out,
-                                                  p_out, gid_out, ctx->u, ctx->nh, g);
+                                                  p_out, gid_out, ctx->u, ctx->u32, ctx->nh, g);
     LAUNCHED();
     prof_end(ctx, NC_K_RANKGATHER);
   }
@@ -214,7 +218,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   int cpb = cells_per_block();
   int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
   int nblocks = bpl * g.dims[2];
-  size_t smem = K3_WARPS * sizeof(K3Smem<T>);
+  size_t smem = sizeof(K3Smem<T>);
   static bool attr_set[2][2] = {{false, false}, {false, false}};
   bool& as = attr_set[sizeof(T) == 8][DIGEST];
   if (!as) {
@@ -222,7 +226,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
     as = true;
   }
   prof_begin(ctx);
-  k_pairs<T, DIGEST><<<nblocks, K3_WARPS * 32, smem, s>>>(ctx->u, ctx->cs, qs, ctx->nh, gid, F,
+  k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F,
                                                          ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl);
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
@@ -431,7 +435,7 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
                                                     (const typename V4<T>::t*)ctx->st_q[c],
                                                     (const typename V4<T>::t*)ctx->st_p[c],
                                                     (typename V4<T>::t*)ctx->st_q[o], (typename V4<T>::t*)ctx->st_p[o],
-                                                    ctx->st_gid[o], ctx->u, ctx->nh, g);
+                                                    ctx->st_gid[o], ctx->u, ctx->u32, ctx->nh, g);
       LAUNCHED();
       prof_end(ctx, NC_K_RANKGATHER);
     }
@@ -553,7 +557,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {&ctx->st_q[0], v4 * N_}, {&ctx->st_q[1], v4 * N_}, {&ctx->st_p[0], v4 * N_}, {&ctx->st_p[1], v4 * N_},
       {(void**)&ctx->st_gid[0], 4 * N_}, {(void**)&ctx->st_gid[1], 4 * N_}, {&ctx->st_F, v4 * N_},
       {&ctx->wq, v4 * N_}, {&ctx->sq, v4 * N_}, {(void**)&ctx->sgid, 4 * N_}, {&ctx->sF, v4 * N_},
-      {&ctx->io_a, 3 * ts * N_}, {&ctx->io_b, 3 * ts * N_}, {(void**)&ctx->u, sizeof(double4) * N_},
+      {&ctx->io_a, 3 * ts * N_}, {&ctx->io_b, 3 * ts * N_}, {(void**)&ctx->u, sizeof(double4) * N_}, {(void**)&ctx->u32, sizeof(float4) * N_},
       {(void**)&ctx->nh, 4 * N_}, {(void**)&ctx->key, 4 * N_}, {(void**)&ctx->slot, 4 * N_},
       {(void**)&ctx->tmp, 4 * N_}, {(void**)&ctx->tmpgid, 4 * N_},
       {(void**)&ctx->counts, 4 * (size_t)C1}, {(void**)&ctx->cs, 4 * (size_t)C1},
@@ -587,7 +591,7 @@ void nc_destroy(nc_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ps[] = {ctx->st_q[0], ctx->st_q[1], ctx->st_p[0], ctx->st_p[1], ctx->st_gid[0], ctx->st_gid[1], ctx->st_F,
-                ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->nh, ctx->key, ctx->slot,
+                ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->tmp, ctx->tmpgid, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
                 ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist};
   for (void* p : ps)
