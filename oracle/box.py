@@ -121,7 +121,7 @@ class Box:
                     L~_t = exp(diag(f1 om1 + f2 om2)) L0 (R23)
     """
 
-    def __init__(self, L0, A, policy="none", t=0.0, om1=None, om2=None, beta=None, tstar=None):
+    def __init__(self, L0, A, policy="none", t=0.0, om1=None, om2=None, beta=None, tstar=None, eps=None):
         self.L0 = np.array(L0, dtype=np.float64).reshape(3, 3)
         self.A = np.array(A, dtype=np.float64).reshape(3, 3)
         check_flow(self.A)
@@ -135,10 +135,10 @@ class Box:
             self.tstar = math.log((3.0 + math.sqrt(5.0)) / 2.0) / eps
         if policy == "gkr":
             assert is_diagonal(self.A)
-            eps = np.max(np.abs(np.diag(self.A)))
-            self.eps = eps
+            # rate scale of A = eps diag(a): given with beta, else the largest |A_kk|
+            self.eps = float(eps) if eps is not None else float(np.max(np.abs(np.diag(self.A))))
             if self.beta is None:
-                self.beta = gkr_beta(self.om1, self.om2, np.diag(self.A) / eps)
+                self.beta = gkr_beta(self.om1, self.om2, np.diag(self.A) / self.eps)
         self.L = self.at(self.t)
 
     def at(self, t: float) -> np.ndarray:

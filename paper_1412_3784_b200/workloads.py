@@ -189,7 +189,7 @@ def make(k: int, r: int = 0, *, flow: str = "uniaxial", scale: int = 1) -> Workl
         L0[0, 1] = gamma * a
         A = np.zeros((3, 3)); A[0, 1] = eps
         return Workload("C1", n, L0, A, "le", 0.0, L0.copy(), WCA_RC, potential="wca", prec=("f32", "f64"),
-                        lattice="fcc", K=K, jitter=0.12, seed=(k, r), steps=0)
+                        lattice="fcc", K=K, jitter=0.05, seed=(k, r), steps=0)
     if k in (2, 4):
         K = (64 if k == 2 else 256) // scale
         lattice = "sc" if k == 2 else "fcc"
@@ -203,7 +203,7 @@ def make(k: int, r: int = 0, *, flow: str = "uniaxial", scale: int = 1) -> Workl
         extra = {"tstar": tstar, "M": np.array([[2, 1, 0], [1, 1, 0], [0, 0, 1]])}
         L = box_at(L0, A, "kr", t0, extra)
         return Workload(f"C{k}", n, L0, A, "kr", t0, L, 2.5, prec=("f32",), lattice=lattice, K=K,
-                        jitter=0.1, seed=(k, r), steps=100 if k == 2 else 50, extra=extra)
+                        jitter=0.05, seed=(k, r), steps=100 if k == 2 else 50, extra=extra)
     if k == 3:
         K = 128 // scale
         n = K ** 3
@@ -228,7 +228,7 @@ def make(k: int, r: int = 0, *, flow: str = "uniaxial", scale: int = 1) -> Workl
         extra = {"beta": beta, "eps": eps, "om1": om1, "om2": om2, "M1": M1, "M2": M2, "flow": flow}
         L = box_at(L0, A, "gkr", t0, extra)
         return Workload("C3" + ("u" if flow == "uniaxial" else "b"), n, L0, A, "gkr", t0, L, WCA_RC,
-                        potential="wca", prec=("f32",), lattice="sc", K=K, jitter=0.1, seed=(k, r), steps=steps,
+                        potential="wca", prec=("f32",), lattice="sc", K=K, jitter=0.05, seed=(k, r), steps=steps,
                         extra=extra)
     raise ValueError(k)
 

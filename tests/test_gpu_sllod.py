@@ -1,0 +1,160 @@
+"""GPU parity of the SLLOD step (K4 + box update + remap + rebuild) against the
+oracle's SLLOD map (reading R19), for the three remap policies of the paper:
+Lees-Edwards shear, Kraynik-Reinelt planar elongation
+and generalized KR uniaxial / biaxial (reading R23).  Each run
+starts just before a remap so that at least one reset happens inside it.
+
+fp64: positions within 1e-9 sigma (modulo the lattice), momenta within 1e-9,
+box bit-for-bit (same closed forms, same fp64 sequence); fp32: 1e-4 / 1e-3.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import box as obox
+from paper_1412_3784_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(w, q, p, prec, variant, dt, nsteps):
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    cl = CellList(variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
+                  capacity=len(q), max_cells=4 * len(q) + 4096)
+    kw = dict(L0=w.L0)
+    if w.policy == "kr":
+        kw["tstar"] = w.extra["tstar"]
+    if w.policy == "gkr":
+        kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
+    cl.set_flow(w.A, w.policy, w.t0, **kw)
+    cl.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
+    Ugpu, Wgpu = cl.step(dt, nsteps)
+    qo = torch.empty_like(torch.from_numpy(q)).cuda()
+    po = torch.empty_like(qo)
+    n, L, t, gid = cl.get_state(qo, po, want_gid=True)
+    cl.close()
+    assert np.array_equal(gid, np.arange(len(q)))
+    return qo.double().cpu().numpy(), po.double().cpu().numpy(), L, t, Ugpu
+
+
+def run_oracle(w, q, p, prec, variant, dt, nsteps):
+    m = oracle.DS if variant == "ds" else oracle.DO
+    b = obox.Box(w.L0, w.A, w.policy, w.t0, om1=w.extra.get("om1"), om2=w.extra.get("om2"),
+                 beta=w.extra.get("beta"), tstar=w.extra.get("tstar"), eps=w.extra.get("eps"))
+    assert np.array_equal(b.L, w.L) or np.abs(b.L - w.L).max() < 1e-12 * np.abs(w.L).max()
+    qd = oracle.wrap(np.asarray(q, dtype=np.float64), b.L, prec)
+    pd = np.asarray(p, dtype=np.float64)
+
+    def forces(qq, L):
+        r = oracle.evaluate(m, qq, L, w.rc, w.eps, w.sigma, w.ushift, want=("F", "U", "W"))
+        return r.F, r.U, r.W
+
+    F, U, _ = forces(qd, b.L)
+    resets = 0
+    Lprev = b.L.copy()
+    for _ in range(nsteps):
+        qd, pd, F, U, _ = obox.sllod_step(qd, pd, F, b, dt, forces, mass=w.mass, prec=prec)
+        X = np.linalg.solve(Lprev, b.L)
+        if np.abs(X - np.eye(3)).max() > 0.5:
+            resets += 1
+        Lprev = b.L.copy()
+    return qd, pd, b.L, b.t, U, resets
+
+
+def lattice_diff(dq, L):
+    """Displacement modulo the lattice: dq - L round(L^-1 dq)."""
+    lam = np.linalg.solve(L, dq.T).T
+    return dq - np.round(lam) @ L.T
+
+
+def near_reset(w, nsteps, dt):
+    """Move t0 so that a remap happens inside the run."""
+    if w.policy == "le":
+        eps = w.A[0, 1]
+        g0 = w.L0[0, 1] / w.L0[1, 1]
+        tx = (0.5 - g0) / eps
+        w.t0 = tx - 0.4 * nsteps * dt
+    elif w.policy == "kr":
+        w.t0 = w.extra["tstar"] - 0.4 * nsteps * dt
+    elif w.policy == "gkr":
+        rate = np.asarray(w.extra["beta"]) * w.extra["eps"]
+        a0 = rate * w.t0
+        # next half-integer crossing of either alpha_k after t0
+        nxt = [((np.floor(a + 0.5) + 0.5) / r if r > 0 else (np.ceil(a - 0.5) - 0.5) / r) for a, r in zip(a0, rate)]
+        w.t0 = min(nxt) - 0.4 * nsteps * dt
+    w.L = W.box_at(w.L0, w.A, w.policy, w.t0, w.extra)
+    return w
+
+
+CASES = [
+    # (config, scale, flow, prec, variant)
+    (1, 2, "uniaxial", "f64", "do"),
+    (1, 2, "uniaxial", "f64", "ds"),
+    (2, 2, "uniaxial", "f64", "do"),
+    (2, 2, "uniaxial", "f64", "ds"),
+    (3, 4, "uniaxial", "f64", "do"),
+    (3, 4, "biaxial", "f64", "ds"),
+    (2, 2, "uniaxial", "f32", "do"),
+    (3, 4, "biaxial", "f32", "do"),
+]
+
+
+@pytest.mark.parametrize("k,scale,flow,prec,variant", CASES)
+def test_sllod_trajectory(k, scale, flow, prec, variant):
+    w = W.make(k, scale=scale, flow=flow)
+    nsteps, dt = 20, 0.002
+    w = near_reset(w, nsteps, dt)
+    dty = np.float64 if prec == "f64" else np.float32
+    q = W.positions(w, dtype=dty, k=k)
+    p = W.momenta(w, dtype=dty, k=k)
+    try:
+        oracle.cell_keys(oracle.DO if variant == "do" else oracle.DS, oracle.wrap(q, w.L, prec), w.L, w.rc)
+    except ValueError:
+        pytest.skip("degenerate grid for this scaled box")
+    qg, pg, Lg, tg, Ug = run_gpu(w, q, p, prec, variant, dt, nsteps)
+    qo, po, Lo, to, Uo, resets = run_oracle(w, q, p, prec, variant, dt, nsteps)
+    assert resets >= 1
+    assert tg == pytest.approx(to, abs=1e-12)
+    assert np.abs(Lg - Lo).max() <= 1e-13 * np.abs(Lo).max()
+    tq, tp = (1e-9, 1e-9) if prec == "f64" else (1e-4, 1e-3)
+    assert np.abs(lattice_diff(qg - qo, Lo)).max() < tq
+    assert np.abs(pg - po).max() < tp * max(1.0, np.abs(po).max())
+    assert Ug == pytest.approx(Uo, rel=1e-9 if prec == "f64" else 1e-5)
+
+
+def test_gkr_reset_inside_run():
+    """C3's seeding puts an alpha_2 half-integer crossing inside the 100-step run (reading R22)."""
+    for flow in ("uniaxial", "biaxial"):
+        w = W.make(3, flow=flow)
+        a0 = w.extra["beta"] * w.extra["eps"] * w.t0
+        a1 = w.extra["beta"] * w.extra["eps"] * (w.t0 + w.steps * w.dt)
+        m0 = np.floor(a0 + 0.5)
+        m1 = np.floor(a1 + 0.5)
+        assert (m0 != m1).any()
+
+
+def test_equilibrium_energy_conservation_gpu():
+    """A = 0: SLLOD reduces to velocity Verlet; total energy is conserved (fp64, C0)."""
+    w = W.make(0)
+    q = W.positions(w, dtype=np.float64, k=0)
+    p = W.momenta(w, dtype=np.float64, k=0)
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    cl = CellList("do", "f64", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    cl.set_flow(w.A, "none", 0.0, L0=w.L)
+    cl.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
+    st = cl.stats()
+    E0 = st["U"] + 0.5 * float((p ** 2).sum())
+    Es = []
+    for _ in range(10):
+        U, _ = cl.step(0.002, 20)
+        po = torch.empty((len(q), 3), dtype=torch.float64, device="cuda")
+        cl.get_state(None, po)
+        Es.append(U + 0.5 * float((po ** 2).sum()))
+    cl.close()
+    assert max(abs(e - E0) for e in Es) < 1e-3 * abs(E0)
