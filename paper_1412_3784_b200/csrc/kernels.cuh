@@ -951,16 +951,25 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             }
           }
           __syncwarp();
-          for (uint32_t t0 = 0; t0 < ctot; t0 += 64) {
-            const uint32_t ta = t0 + lane, tb = t0 + 32 + lane;
-            const bool va = ta < ctot, vb = tb < ctot;
-            const int ea = va ? sm.sent[ta] : e0, eb = vb ? sm.sent[tb] : e0;
-            const uint32_t ja = sm.e_start[ea] + ta - (sm.e_off[ea] - base_off);
-            const uint32_t jb = sm.e_start[eb] + tb - (sm.e_off[eb] - base_off);
-            const float4 pa = va ? u32[ja] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 pb = vb ? u32[jb] : make_float4(0.f, 0.f, 0.f, 0.f);
-            if (va) sm.stage[ta] = make_float4(pa.x + sm.s64.Bf[ea][0], pa.y + sm.s64.Bf[ea][1], pa.z + sm.s64.Bf[ea][2], pa.w);
-            if (vb) sm.stage[tb] = make_float4(pb.x + sm.s64.Bf[eb][0], pb.y + sm.s64.Bf[eb][1], pb.z + sm.s64.Bf[eb][2], pb.w);
+          // four elements per lane in flight: all index lookups and loads first, then the stores
+          for (uint32_t t0 = 0; t0 < ctot; t0 += 128) {
+            uint32_t tt[4], jj[4];
+            int ee[4];
+            float4 pp[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              tt[r] = t0 + 32u * r + lane;
+              const bool v = tt[r] < ctot;
+              ee[r] = v ? sm.sent[tt[r]] : e0;
+              jj[r] = sm.e_start[ee[r]] + tt[r] - (sm.e_off[ee[r]] - base_off);
+              pp[r] = v ? u32[jj[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              if (tt[r] < ctot)
+                sm.stage[tt[r]] = make_float4(pp[r].x + sm.s64.Bf[ee[r]][0], pp[r].y + sm.s64.Bf[ee[r]][1],
+                                              pp[r].z + sm.s64.Bf[ee[r]][2], pp[r].w);
+            }
           }
         } else {
           for (int eb = e0; eb < e1; eb += 32) {
@@ -1056,15 +1065,28 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   }
 }
 
-// K3r: per-layer partials in block order, then the total in layer order.
-__global__ void k_reduce_layers(const double* __restrict__ bpart, int bpl, int nlayers, double* __restrict__ lpart) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= nlayers * NPART) return;
-  int layer = k / NPART, c = k % NPART;
-  double v = 0;
-  const double* p = bpart + (int64_t)layer * bpl * NPART + c;
-  for (int b = 0; b < bpl; ++b) v += p[(int64_t)b * NPART];
-  lpart[k] = v;
+// K3r: per-layer partials (one block per layer: each thread sums a fixed
+// strided subset of the layer's block partials in order, then a fixed-shape
+// tree), then the total in layer order.  Deterministic and layer-aligned, so
+// identical for any assignment of layers to devices.
+constexpr int K3R_T = 256;
+__global__ void __launch_bounds__(K3R_T) k_reduce_layers(const double* __restrict__ bpart, int bpl, int nlayers,
+                                                         double* __restrict__ lpart) {
+  __shared__ double red[K3R_T];
+  const int layer = blockIdx.x;
+  const double* base = bpart + (int64_t)layer * bpl * NPART;
+  for (int c = 0; c < NPART; ++c) {
+    double v = 0.0;
+    for (int b = threadIdx.x; b < bpl; b += K3R_T) v += base[(int64_t)b * NPART + c];
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = K3R_T / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) lpart[(int64_t)layer * NPART + c] = red[0];
+    __syncthreads();
+  }
 }
 
 // total in layer order; also accumulates into acc[0..NPART) and counts evaluations in acc[NPART]

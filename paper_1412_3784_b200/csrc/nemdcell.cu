@@ -232,7 +232,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   prof_end(ctx, NC_K_PAIRS);
   int nl = g.dims[2];
   prof_begin(ctx);
-  k_reduce_layers<<<nblk((int64_t)nl * NPART, 128), 128, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart);
+  k_reduce_layers<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart);
   LAUNCHED();
   prof_end(ctx, NC_K_REDUCE);
   prof_begin(ctx);
