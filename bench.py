@@ -168,6 +168,100 @@ def run_reference(args):
     return 0
 
 
+def run_slab(args):
+    """N > 1: slab decomposition of C4 over the ranks (strong scaling), NCCL P2P halo
+    exchange and migration (paper_1412_3784_b200/slab.py)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, lrank, ws = dist_setup("nccl")
+    torch.cuda.set_device(lrank)
+    from paper_1412_3784_b200 import workloads as W
+    from paper_1412_3784_b200.nemdcell import CellList
+    from paper_1412_3784_b200.slab import DistTransport, SlabRank, SlabSystem, own_particles
+
+    w = workload(args.config)
+    q = W.positions(w, dtype=np.float32, k=args.config, r=0)
+    p = W.momenta(w, dtype=np.float32, k=args.config, r=0)
+    kw = dict(L0=w.L0)
+    if w.policy == "kr":
+        kw["tstar"] = w.extra["tstar"]
+    if w.policy == "gkr":
+        kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
+    maxc = int(2.5 * w.n / 13) + 65536
+    full = CellList(args.variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=maxc, device=lrank)
+    full.set_flow(w.A, w.policy, w.t0, **kw)
+    idx = own_particles(full, torch.from_numpy(q).to(f"cuda:{lrank}"), rank, ws)
+    full.close()
+    torch.cuda.empty_cache()
+    stream = torch.cuda.Stream(lrank)
+    cap = int(1.3 * w.n / ws) + 4 * w.n // 171 + 65536
+    sr = SlabRank(rank, ws, variant=args.variant, prec="f32", rc=w.rc, u_shift=w.ushift, mass=w.mass, capacity=cap,
+                  max_cells=maxc, device=lrank, stream=stream.cuda_stream)
+    sr.set_flow(w.A, w.policy, w.t0, **kw)
+    sr.load(q[idx], p[idx], idx.astype(np.int32))
+    del q, p
+    from paper_1412_3784_b200.slab import LoopbackTransport
+
+    sysm = SlabSystem([sr], DistTransport(rank, ws, f"cuda:{lrank}") if ws > 1 else LoopbackTransport())
+    with torch.cuda.stream(stream):
+        sysm.forces(False)
+        for _ in range(args.warmup):
+            sysm.step(w.dt, False)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(lrank)
+    sr.cl.profile(True)
+    l0 = sr.cl.launches()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            sysm.step(w.dt, False)
+        ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    launches = sr.cl.launches() - l0
+    prof = sr.cl.profile_read()
+    st = sr.cl.stats()
+    t = torch.tensor([ms, st["acc_interactions"], st["acc_candidates"], float(launches)], dtype=torch.float64,
+                     device=f"cuda:{lrank}")
+    tmax = t.clone()
+    if ws > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t)
+    ms_max = float(tmax[0])
+    inter = float(t[1])
+    value = inter / 2.0 / (ms_max * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
+            "config": {"workload": f"C{args.config}", "n_total": w.n, "variant": args.variant,
+                       "box": "KR planar elongation, eps=0.1, dt=0.002", "potential": "LJ rc=2.5 shifted",
+                       "precision": "fp32 storage + fp32 filter, fp64 interactions",
+                       "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
+                                                                   "NCCL P2P halo + migration"},
+            "particle_steps_per_s": w.n * args.steps / (ms_max * 1e-3),
+            "kernel_ms_per_step_rank0": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
+            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": int(t[3]), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    sr.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
 
@@ -330,9 +424,12 @@ def main():
     ap.add_argument("--variant", default="do", choices=["do", "ds"])
     ap.add_argument("--ref-sample", type=int, default=200000)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.slab:
+        return run_slab(args)
     return run_ours(args)
 
 

@@ -195,6 +195,63 @@ enum { NC_K_WRAPKEY = 0, NC_K_SCAN = 1, NC_K_SCATTER = 2, NC_K_RANKGATHER = 3, N
 nc_status nc_profile(nc_ctx *ctx, int enable);
 nc_status nc_profile_read(nc_ctx *ctx, double ms[8], int64_t counts[8]);
 
+/* ---------------------------------------------------------------------------
+ * Slab decomposition for several GPUs (one process per GPU).
+ * The box is cut into slabs of whole cell layers along the third lattice
+ * direction (lambda_3; DS layer floor(lambda_3 c_3), DO layer floor(z/w_3),
+ * z = r_33 lambda_3 -- the same axis for both variants).  Each rank owns the
+ * particles of its layers, receives one r_c-thick halo layer from each
+ * neighbour rank, and computes full i-side forces for its own particles only
+ * (no reverse force communication).  The host driver
+ * (paper_1412_3784_b200/slab.py) moves the packed buffers between ranks.
+ * All pointers are DEVICE memory.  Arrays q, p, F are n x 3 (storage type),
+ * gid is uint32.  Records: migration = 2 four-vectors per particle
+ * (q.xyz + gid, p.xyz + 0), halo = 1 four-vector (q.xyz + gid); gid is the
+ * bit pattern (fp32) or the exact value (fp64) of the fourth component.
+ * ------------------------------------------------------------------------- */
+
+/* Layers [klo, khi) owned by rank of nranks for the current box (needs
+ * l3 >= 2 nranks).  Errors: NC_E_STATE, NC_E_DEGENERATE, NC_E_ARG. */
+nc_status nc_slab_layers(nc_ctx *ctx, int rank, int nranks, int32_t *klo, int32_t *khi, int32_t *l3);
+
+/* SLLOD first half (R19) on n own particles in place, then advance the box
+ * to t + dt with its remap.  Positions are wrapped by nc_slab_migrate. */
+nc_status nc_slab_kick_drift(nc_ctx *ctx, void *q, void *p, const void *F, int64_t n, double dt);
+
+/* Wrap q in place (R15), then split the n particles by layer: those still
+ * in [klo, khi) go to q_out/p_out/gid_out (index order), those in layer
+ * klo-1 / khi (mod l3) are packed as migration records into send_lo /
+ * send_hi (capacity cap each).  counts = (stay, to_lo, to_hi).
+ * NC_E_STATE if a particle moved further than one layer. */
+nc_status nc_slab_migrate(nc_ctx *ctx, void *q, const void *p, const uint32_t *gid, int64_t n, int klo, int khi,
+                          void *q_out, void *p_out, uint32_t *gid_out, void *send_lo, void *send_hi, int64_t cap,
+                          int64_t counts[3]);
+
+/* Unpack n migration records into n x 3 q, p and gid (append arrivals). */
+nc_status nc_slab_unpack(nc_ctx *ctx, const void *rec, int64_t n, void *q, void *p, uint32_t *gid);
+
+/* Pack halo records of the own particles in layer klo (-> halo_lo, for rank
+ * r-1) and in layer khi-1 (-> halo_hi, for rank r+1).  counts = (lo, hi). */
+nc_status nc_slab_halo(nc_ctx *ctx, void *q, const uint32_t *gid, int64_t n, int klo, int khi, void *halo_lo,
+                       void *halo_hi, int64_t cap, int64_t counts[2]);
+
+/* Forces on the n_own own particles (output F in their input order) with the
+ * halo records received from the lower and upper neighbour; K3 runs over the
+ * own layers [klo, khi) only.  layer_parts (host, (khi-klo) x 12 doubles, may
+ * be NULL) receives the per-layer partials (U, W0..W5, interactions,
+ * candidates, stencil cells, rechecks, non-finite) for nc_slab_reduce. */
+nc_status nc_slab_forces(nc_ctx *ctx, const void *q, const uint32_t *gid, int64_t n_own, const void *halo_from_lo,
+                         int64_t n_lo, const void *halo_from_hi, int64_t n_hi, int klo, int khi, void *F,
+                         double *layer_parts);
+
+/* SLLOD second half: p <- E(-dt/2) p + dt/2 F on n own particles. */
+nc_status nc_slab_kick(nc_ctx *ctx, void *p, const void *F, int64_t n, double dt);
+
+/* Fixed-order sum of all l3 layers' partials (global layer order, host) ->
+ * U, W (lab frame) and stats = (interactions, candidates, stencil cells,
+ * rechecks): bitwise the same as a single-device evaluation. */
+nc_status nc_slab_reduce(nc_ctx *ctx, const double *parts, int nlayers, double *U, double W[6], double stats[4]);
+
 /* Number of kernel launches this context has issued so far. */
 int64_t nc_launch_count(const nc_ctx *ctx);
 

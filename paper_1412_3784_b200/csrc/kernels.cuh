@@ -284,7 +284,7 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
                               typename V4<T>::t* __restrict__ q_out, typename V4<T>::t* __restrict__ p_out,
                               uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
                               float4* __restrict__ u32_out, uint32_t* __restrict__ nh_out,
-                              const __grid_constant__ Geom g) {
+                              const __grid_constant__ Geom g, uint32_t* __restrict__ idx_out = nullptr) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   uint32_t i = tmp[s];
@@ -307,6 +307,7 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
   u_out[dst] = make_double4(u[0], u[1], u[2], (double)dst);
   u32_out[dst] = make_float4((float)u[0], (float)u[1], (float)u[2], __uint_as_float(dst));
   nh_out[dst] = pack_nh(cp.nh0, cp.nh1);
+  if (idx_out) idx_out[dst] = i;
 }
 
 // ---------------------------------------------------------------------------
@@ -836,14 +837,15 @@ __global__ void __launch_bounds__(32, 14)
 k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
         const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
-        uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl) {
+        uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl,
+        int layer0) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lane = threadIdx.x & 31;
   K3Smem<T>& sm = *reinterpret_cast<K3Smem<T>*>(smraw);
 
   const int l1 = g.dims[0], l2 = g.dims[1];
-  const int layer = blockIdx.x / bpl;
-  const int chunk = blockIdx.x - layer * bpl;
+  const int layer = layer0 + (int)(blockIdx.x / bpl);  // global cell layer (slab mode: owned layers only)
+  const int chunk = (int)blockIdx.x - (layer - layer0) * bpl;
   const int per_layer = l1 * l2;
   const int cbeg = chunk * cpb;
   const int cend = min(per_layer, cbeg + cpb);
@@ -1202,6 +1204,176 @@ __global__ void k_kick(int64_t n, typename V4<T>::t* __restrict__ p, const typen
   mv3(sp.Em, (double)pi.x, (double)pi.y, (double)pi.z, ax, ay, az);
   double hd = 0.5 * sp.dt;
   p[i] = mk4((T)(ax + hd * (double)fi.x), (T)(ay + hd * (double)fi.y), (T)(az + hd * (double)fi.z), (T)0);
+}
+
+
+// ---------------------------------------------------------------------------
+// Slab decomposition primitives (multi-GPU).  Caller arrays are
+// n x 3 (the ABI layout); records exchanged between ranks are T4 words:
+// migration = 2 words (q.xyz + gid, p.xyz + 0), halo = 1 word (q.xyz + gid).
+// The gid travels as the bit pattern (fp32) or the exact value (fp64) of .w.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_kick_drift3(int64_t n, T* __restrict__ q, T* __restrict__ p, const T* __restrict__ F, SllodParams sp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double hd = 0.5 * sp.dt;
+  double px = (double)p[3 * i] + hd * (double)F[3 * i], py = (double)p[3 * i + 1] + hd * (double)F[3 * i + 1],
+         pz = (double)p[3 * i + 2] + hd * (double)F[3 * i + 2];
+  double ax, ay, az, hx, hy, hz, qx, qy, qz;
+  mv3(sp.Em, px, py, pz, ax, ay, az);
+  mv3(sp.Eh, ax, ay, az, hx, hy, hz);
+  mv3(sp.Ed, (double)q[3 * i], (double)q[3 * i + 1], (double)q[3 * i + 2], qx, qy, qz);
+  q[3 * i] = (T)(qx + sp.dt * hx * sp.inv_m);
+  q[3 * i + 1] = (T)(qy + sp.dt * hy * sp.inv_m);
+  q[3 * i + 2] = (T)(qz + sp.dt * hz * sp.inv_m);
+  p[3 * i] = (T)ax; p[3 * i + 1] = (T)ay; p[3 * i + 2] = (T)az;
+}
+
+template <typename T>
+__global__ void k_kick3(int64_t n, T* __restrict__ p, const T* __restrict__ F, SllodParams sp) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double ax, ay, az;
+  mv3(sp.Em, (double)p[3 * i], (double)p[3 * i + 1], (double)p[3 * i + 2], ax, ay, az);
+  double hd = 0.5 * sp.dt;
+  p[3 * i] = (T)(ax + hd * (double)F[3 * i]);
+  p[3 * i + 1] = (T)(ay + hd * (double)F[3 * i + 1]);
+  p[3 * i + 2] = (T)(az + hd * (double)F[3 * i + 2]);
+}
+
+// mode 0 (migration): wrap q in place (R15); class 0 = layer owned, 1 = layer klo-1 (to rank r-1),
+//                     2 = layer khi (to rank r+1), 3 = further away (error).
+// mode 1 (halo):      class 1 = layer klo (copy to r-1), 2 = layer khi-1 (copy to r+1), else 0.
+template <typename T>
+__global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_constant__ Geom g, int klo, int khi,
+                                int mode, uint8_t* __restrict__ cls) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q0 = (double)q[3 * i], q1 = (double)q[3 * i + 1], q2 = (double)q[3 * i + 2];
+  double lam[3];
+  frac_c(g, q0, q1, q2, lam);
+  if (lam[0] < 0.0 || lam[0] >= 1.0 || lam[1] < 0.0 || lam[1] >= 1.0 || lam[2] < 0.0 || lam[2] >= 1.0) {
+    int n0 = (int)floor(lam[0]), n1 = (int)floor(lam[1]), n2 = (int)floor(lam[2]);
+    q0 = round_to(__dsub_rn(q0, lshift_c(g, 0, n0, n1, n2)), T());
+    q1 = round_to(__dsub_rn(q1, lshift_c(g, 1, n0, n1, n2)), T());
+    q2 = round_to(__dsub_rn(q2, lshift_c(g, 2, n0, n1, n2)), T());
+    q[3 * i] = (T)q0; q[3 * i + 1] = (T)q1; q[3 * i + 2] = (T)q2;
+    frac_c(g, q0, q1, q2, lam);
+  }
+  CellPos cp;
+  cell_of(g, lam, cp);
+  const int k = cp.a[2], l3 = g.dims[2];
+  uint8_t c;
+  if (mode == 0) {
+    if (k >= klo && k < khi) c = 0;
+    else if (k == (klo - 1 + l3) % l3) c = 1;
+    else if (k == khi % l3) c = 2;
+    else c = 3;
+  } else {
+    c = (k == klo) ? 1 : (k == khi - 1 ? 2 : 0);
+  }
+  cls[i] = c;
+}
+
+constexpr int PART_T = 256;
+// per-block counts of classes 0..3
+__global__ void k_class_count(int64_t n, const uint8_t* __restrict__ cls, uint32_t* __restrict__ bcnt) {
+  __shared__ uint32_t c[4];
+  if (threadIdx.x < 4) c[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t i = (int64_t)blockIdx.x * PART_T + threadIdx.x;
+  if (i < n) atomicAdd(&c[cls[i]], 1u);  // counts only: order-free
+  __syncthreads();
+  if (threadIdx.x < 4) bcnt[(int64_t)blockIdx.x * 4 + threadIdx.x] = c[threadIdx.x];
+}
+// exclusive scan per class over blocks (single block, sequential per class: nb is small)
+__global__ void k_class_scan(uint32_t* __restrict__ bcnt, int64_t nb, uint32_t* __restrict__ tot) {
+  int c = threadIdx.x;
+  if (c >= 4) return;
+  uint32_t run = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    uint32_t v = bcnt[b * 4 + c];
+    bcnt[b * 4 + c] = run;
+    run += v;
+  }
+  tot[c] = run;
+}
+// stable partition by class (index order within each class): class 0 -> SoA outputs, classes 1, 2 ->
+// records of `words` T4 words (2: q+gid, p; 1: q+gid)
+template <typename T>
+__global__ void k_class_scatter(int64_t n, const uint8_t* __restrict__ cls, const uint32_t* __restrict__ boff,
+                                const T* __restrict__ q, const T* __restrict__ p, const uint32_t* __restrict__ gid,
+                                T* __restrict__ q0, T* __restrict__ p0, uint32_t* __restrict__ g0,
+                                typename V4<T>::t* __restrict__ r1, typename V4<T>::t* __restrict__ r2, int words) {
+  __shared__ uint32_t wsum[PART_T / 32][4];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t i = (int64_t)blockIdx.x * PART_T + threadIdx.x;
+  const int c = i < n ? cls[i] : 4;
+  uint32_t rank_in_warp = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    unsigned b = __ballot_sync(0xffffffffu, c == k);
+    if (c == k) rank_in_warp = __popc(b & ((1u << lane) - 1u));
+    if (lane == 0) wsum[wid][k] = __popc(b);
+  }
+  __syncthreads();
+  if (c >= 3) return;
+  uint32_t pos = boff[(int64_t)blockIdx.x * 4 + c] + rank_in_warp;
+  for (int w = 0; w < wid; ++w) pos += wsum[w][c];
+  const T x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
+  const uint32_t gg = gid[i];
+  if (c == 0) {
+    if (q0) {
+      q0[3 * pos] = x; q0[3 * pos + 1] = y; q0[3 * pos + 2] = z;
+      if (p0) { p0[3 * pos] = p[3 * i]; p0[3 * pos + 1] = p[3 * i + 1]; p0[3 * pos + 2] = p[3 * i + 2]; }
+      g0[pos] = gg;
+    }
+    return;
+  }
+  typename V4<T>::t* r = (c == 1 ? r1 : r2) + (int64_t)pos * words;
+  r[0] = mk4(x, y, z, idx_to_w(gg, T()));
+  if (words == 2) r[1] = mk4(p[3 * i], p[3 * i + 1], p[3 * i + 2], (T)0);
+}
+
+template <typename T>
+__global__ void k_records_unpack(int64_t n, const typename V4<T>::t* __restrict__ r, T* __restrict__ q,
+                                 T* __restrict__ p, uint32_t* __restrict__ gid) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  typename V4<T>::t a = r[2 * i], b = r[2 * i + 1];
+  q[3 * i] = a.x; q[3 * i + 1] = a.y; q[3 * i + 2] = a.z;
+  p[3 * i] = b.x; p[3 * i + 1] = b.y; p[3 * i + 2] = b.z;
+  gid[i] = w_to_idx(a.w);
+}
+
+// K1 over one source of the local system (own particles: n x 3 + gid array; halo records: T4 with gid in .w)
+template <typename T>
+__global__ void k_wrap_key_src(int64_t n, const T* __restrict__ qin, int stride, const uint32_t* __restrict__ gsrc,
+                               int64_t off, typename V4<T>::t* __restrict__ qout, uint32_t* __restrict__ gout,
+                               uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
+                               const __grid_constant__ Geom g) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double q0 = (double)qin[i * stride], q1 = (double)qin[i * stride + 1], q2 = (double)qin[i * stride + 2];
+  uint32_t gg = gsrc ? gsrc[i] : w_to_idx(qin[i * stride + 3]);
+  uint32_t c = wrap_key_one<T>(g, q0, q1, q2);
+  qout[off + i] = mk4((T)q0, (T)q1, (T)q2, (T)0);
+  gout[off + i] = gg;
+  key[off + i] = c;
+  slot[off + i] = atomicAdd(&counts[c], 1u);
+}
+
+// F of the own particles back to their input order (sorted slot -> original local index)
+template <typename T>
+__global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ src, const uint32_t* __restrict__ sidx,
+                             int64_t n_own, T* __restrict__ dst) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t i = sidx[s];
+  if ((int64_t)i >= n_own) return;
+  typename V4<T>::t v = src[s];
+  dst[3 * (int64_t)i] = v.x; dst[3 * (int64_t)i + 1] = v.y; dst[3 * (int64_t)i + 2] = v.z;
 }
 
 }  // namespace nc

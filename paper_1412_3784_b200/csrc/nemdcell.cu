@@ -51,6 +51,9 @@ struct nc_ctx {
   float4* u32 = nullptr;  // the same in fp32 (w = sorted index bits): the filter's staging source
   uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr, *tmp = nullptr, *tmpgid = nullptr;
   uint32_t *counts = nullptr, *cs = nullptr, *bsum = nullptr, *tot = nullptr;
+  // slab (multi-GPU) scratch
+  uint32_t *gin = nullptr, *sidx = nullptr, *pbcnt = nullptr, *ptot = nullptr;
+  uint8_t* cls = nullptr;
   double *bpart = nullptr, *lpart = nullptr, *part_tot = nullptr, *part_acc = nullptr;
   // digest
   uint32_t* dcnt = nullptr;
@@ -212,12 +215,14 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
 }
 
 template <typename T, bool DIGEST>
-nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t* gid, typename V4<T>::t* F) {
+nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t* gid, typename V4<T>::t* F,
+                       int layer0 = 0, int nlay = -1) {
   cudaStream_t s = ctx->stream;
   const Geom& g = ctx->g;
+  if (nlay < 0) nlay = g.dims[2];
   int cpb = cells_per_block();
   int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
-  int nblocks = bpl * g.dims[2];
+  int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
   static bool attr_set[2][2] = {{false, false}, {false, false}};
   bool& as = attr_set[sizeof(T) == 8][DIGEST];
@@ -227,10 +232,10 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   }
   prof_begin(ctx);
   k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F,
-                                                         ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl);
+                                                         ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
-  int nl = g.dims[2];
+  int nl = nlay;
   prof_begin(ctx);
   k_reduce_layers<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart);
   LAUNCHED();
@@ -485,6 +490,100 @@ nc_status digest_t(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_t* hxor) {
   return NC_OK;
 }
 
+
+// ---------------------------------------------------------------- slab helpers
+nc_status sllod_params(nc_ctx* ctx, double dt, SllodParams& sp) {
+  expm3(ctx->A, -0.5 * dt, sp.Em);
+  expm3(ctx->A, dt, sp.Ed);
+  expm3(ctx->A, 0.5 * dt, sp.Eh);
+  sp.dt = dt;
+  sp.inv_m = 1.0 / ctx->cfg.mass;
+  return NC_OK;
+}
+
+// deterministic class partition of n particles; returns class totals on the host
+template <typename T>
+nc_status partition(nc_ctx* ctx, int64_t n, const T* q, const T* p, const uint32_t* gid, T* q0, T* p0, uint32_t* g0,
+                    typename V4<T>::t* r1, typename V4<T>::t* r2, int words, uint32_t tot_out[4]) {
+  cudaStream_t s = ctx->stream;
+  int64_t nb = (n + PART_T - 1) / PART_T;
+  if (n > 0) {
+    prof_begin(ctx);
+    k_class_count<<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pbcnt);
+    LAUNCHED();
+    k_class_scan<<<1, 32, 0, s>>>(ctx->pbcnt, nb, ctx->ptot);
+    LAUNCHED();
+    k_class_scatter<T><<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pbcnt, q, p, gid, q0, p0, g0, r1, r2, words);
+    LAUNCHED();
+    prof_end(ctx, NC_K_OTHER);
+    CK(cudaMemcpyAsync(tot_out, ctx->ptot, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    tot_out[0] = tot_out[1] = tot_out[2] = tot_out[3] = 0;
+  }
+  return NC_OK;
+}
+
+template <typename T>
+nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_own, const void* h1, int64_t n1,
+                        const void* h2, int64_t n2, int klo, int khi, T* F, double* parts) {
+  cudaStream_t s = ctx->stream;
+  const Geom& g = ctx->g;
+  const int64_t n = n_own + n1 + n2;
+  if (n > ctx->cap) return fail(ctx, NC_E_OOM, "own + halo particles exceed capacity");
+  int64_t C = g.ncells;
+  CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
+  typename V4<T>::t* wq = (typename V4<T>::t*)ctx->wq;
+  prof_begin(ctx);
+  if (n_own > 0)
+    k_wrap_key_src<T><<<nblk(n_own, 256), 256, 0, s>>>(n_own, q, 3, gid, 0, wq, ctx->gin, ctx->key, ctx->slot,
+                                                      ctx->counts, g);
+  if (n1 > 0)
+    k_wrap_key_src<T><<<nblk(n1, 256), 256, 0, s>>>(n1, (const T*)h1, 4, nullptr, n_own, wq, ctx->gin, ctx->key,
+                                                    ctx->slot, ctx->counts, g);
+  if (n2 > 0)
+    k_wrap_key_src<T><<<nblk(n2, 256), 256, 0, s>>>(n2, (const T*)h2, 4, nullptr, n_own + n1, wq, ctx->gin,
+                                                    ctx->key, ctx->slot, ctx->counts, g);
+  LAUNCHED();
+  prof_end(ctx, NC_K_WRAPKEY);
+  int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
+  prof_begin(ctx);
+  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
+  k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
+  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
+  LAUNCHED();
+  prof_end(ctx, NC_K_SCAN);
+  if (n > 0) {
+    prof_begin(ctx);
+    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp, ctx->tmpgid);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCATTER);
+    prof_begin(ctx);
+    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->key, ctx->cs, wq, nullptr,
+                                                  (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u, ctx->u32,
+                                                  ctx->nh, g, ctx->sidx);
+    LAUNCHED();
+    prof_end(ctx, NC_K_RANKGATHER);
+  }
+  ctx->n_last = n;
+  ctx->last_in_gid = ctx->gin;
+  ctx->last_resident = false;
+  ctx->have_cells = true;
+  nc_status st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid,
+                                        (typename V4<T>::t*)ctx->sF, klo, khi - klo);
+  if (st) return st;
+  if (n > 0 && F) {
+    prof_begin(ctx);
+    k_unsort_idx<T><<<nblk(n, 256), 256, 0, s>>>(n, (const typename V4<T>::t*)ctx->sF, ctx->sidx, n_own, F);
+    LAUNCHED();
+    prof_end(ctx, NC_K_OTHER);
+  }
+  if (parts) {
+    CK(cudaMemcpyAsync(parts, ctx->lpart, sizeof(double) * NPART * (size_t)(khi - klo), cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return NC_OK;
+}
 }  // namespace
 
 // ============================================================================ C-ABI
@@ -567,6 +666,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {(void**)&ctx->part_tot, sizeof(double) * NPART}, {(void**)&ctx->part_acc, sizeof(double) * (NPART + 1)},
       {(void**)&ctx->dcnt, 4 * N_}, {(void**)&ctx->dhs, 8 * N_}, {(void**)&ctx->dhx, 8 * N_},
       {(void**)&ctx->hist, 8 * 64},
+      {(void**)&ctx->gin, 4 * N_}, {(void**)&ctx->sidx, 4 * N_}, {(void**)&ctx->cls, N_},
+      {(void**)&ctx->pbcnt, 16 * (N_ / PART_T + 2)}, {(void**)&ctx->ptot, 16},
   };
   for (auto& a : allocs) {
     e = cudaMalloc(a.p, a.bytes);
@@ -593,7 +694,8 @@ void nc_destroy(nc_ctx* ctx) {
   void* ps[] = {ctx->st_q[0], ctx->st_q[1], ctx->st_p[0], ctx->st_p[1], ctx->st_gid[0], ctx->st_gid[1], ctx->st_F,
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->tmp, ctx->tmpgid, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
-                ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist};
+                ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
+                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->ptot};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& p : ctx->prof_ev) {
@@ -792,6 +894,161 @@ nc_status nc_get_stencil_histogram(nc_ctx* ctx, int64_t hist[64]) {
   CK(cudaMemcpyAsync(h, ctx->hist, 8 * 64, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (int k = 0; k < 64; ++k) hist[k] = (int64_t)h[k];
+  return NC_OK;
+}
+
+
+// ============================================================================ slab (multi-GPU) C-ABI
+
+nc_status nc_slab_layers(nc_ctx* ctx, int rank, int nranks, int32_t* klo, int32_t* khi, int32_t* l3) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, NC_E_ARG, "bad rank / nranks");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
+  const int L3 = ctx->g.dims[2];
+  if (L3 < 2 * nranks) return fail(ctx, NC_E_DEGENERATE, "slab decomposition needs >= 2 cell layers per rank");
+  if (klo) *klo = (int32_t)((int64_t)rank * L3 / nranks);
+  if (khi) *khi = (int32_t)((int64_t)(rank + 1) * L3 / nranks);
+  if (l3) *l3 = L3;
+  return NC_OK;
+}
+
+nc_status nc_slab_kick_drift(nc_ctx* ctx, void* q, void* p, const void* F, int64_t n, double dt) {
+  if (!ctx || (n > 0 && (!q || !p || !F))) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_flow && !ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_flow first");
+  if (!(dt > 0)) return fail(ctx, NC_E_ARG, "dt must be > 0");
+  SllodParams sp;
+  sllod_params(ctx, dt, sp);
+  double Lnew[9];
+  box_at(ctx->pol, ctx->A, ctx->t + dt, Lnew);
+  nc_status st = apply_box(ctx, Lnew);
+  if (st) return st;
+  ctx->t += dt;
+  if (n > 0) {
+    prof_begin(ctx);
+    if (ctx->cfg.prec == NC_F32)
+      k_kick_drift3<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, (float*)p, (const float*)F, sp);
+    else
+      k_kick_drift3<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, (double*)p, (const double*)F, sp);
+    LAUNCHED();
+    prof_end(ctx, NC_K_KICK);
+  }
+  return NC_OK;
+}
+
+nc_status nc_slab_migrate(nc_ctx* ctx, void* q, const void* p, const uint32_t* gid, int64_t n, int klo, int khi,
+                          void* q_out, void* p_out, uint32_t* gid_out, void* send_lo, void* send_hi, int64_t cap,
+                          int64_t counts[3]) {
+  if (!ctx || !counts || (n > 0 && (!q || !p || !gid || !q_out || !p_out || !gid_out || !send_lo || !send_hi)))
+    return fail(ctx, NC_E_ARG, "null argument");
+  if (n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
+  uint32_t tot[4] = {0, 0, 0, 0};
+  nc_status st;
+  if (n > 0) {
+    prof_begin(ctx);
+    if (ctx->cfg.prec == NC_F32)
+      k_slab_classify<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, ctx->g, klo, khi, 0, ctx->cls);
+    else
+      k_slab_classify<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, ctx->g, klo, khi, 0, ctx->cls);
+    LAUNCHED();
+    prof_end(ctx, NC_K_WRAPKEY);
+  }
+  if (ctx->cfg.prec == NC_F32)
+    st = partition<float>(ctx, n, (const float*)q, (const float*)p, gid, (float*)q_out, (float*)p_out, gid_out,
+                          (float4*)send_lo, (float4*)send_hi, 2, tot);
+  else
+    st = partition<double>(ctx, n, (const double*)q, (const double*)p, gid, (double*)q_out, (double*)p_out, gid_out,
+                           (double4*)send_lo, (double4*)send_hi, 2, tot);
+  if (st) return st;
+  if (tot[3]) return fail(ctx, NC_E_STATE, "a particle moved more than one cell layer past its slab in one step");
+  if ((int64_t)tot[1] > cap || (int64_t)tot[2] > cap) return fail(ctx, NC_E_OOM, "migration buffer too small");
+  counts[0] = tot[0]; counts[1] = tot[1]; counts[2] = tot[2];
+  return NC_OK;
+}
+
+nc_status nc_slab_unpack(nc_ctx* ctx, const void* rec, int64_t n, void* q, void* p, uint32_t* gid) {
+  if (!ctx || (n > 0 && (!rec || !q || !p || !gid))) return fail(ctx, NC_E_ARG, "null argument");
+  if (n <= 0) return NC_OK;
+  prof_begin(ctx);
+  if (ctx->cfg.prec == NC_F32)
+    k_records_unpack<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (const float4*)rec, (float*)q, (float*)p, gid);
+  else
+    k_records_unpack<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (const double4*)rec, (double*)q, (double*)p,
+                                                                     gid);
+  LAUNCHED();
+  prof_end(ctx, NC_K_OTHER);
+  return NC_OK;
+}
+
+nc_status nc_slab_halo(nc_ctx* ctx, void* q, const uint32_t* gid, int64_t n, int klo, int khi, void* halo_lo,
+                       void* halo_hi, int64_t cap, int64_t counts[2]) {
+  if (!ctx || !counts || (n > 0 && (!q || !gid || !halo_lo || !halo_hi))) return fail(ctx, NC_E_ARG, "null argument");
+  if (khi - klo < 2) return fail(ctx, NC_E_DEGENERATE, "slab decomposition needs >= 2 cell layers per rank");
+  uint32_t tot[4] = {0, 0, 0, 0};
+  nc_status st;
+  if (n > 0) {
+    prof_begin(ctx);
+    if (ctx->cfg.prec == NC_F32)
+      k_slab_classify<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, ctx->g, klo, khi, 1, ctx->cls);
+    else
+      k_slab_classify<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, ctx->g, klo, khi, 1, ctx->cls);
+    LAUNCHED();
+    prof_end(ctx, NC_K_WRAPKEY);
+  }
+  if (ctx->cfg.prec == NC_F32)
+    st = partition<float>(ctx, n, (const float*)q, nullptr, gid, nullptr, nullptr, nullptr, (float4*)halo_lo,
+                          (float4*)halo_hi, 1, tot);
+  else
+    st = partition<double>(ctx, n, (const double*)q, nullptr, gid, nullptr, nullptr, nullptr, (double4*)halo_lo,
+                           (double4*)halo_hi, 1, tot);
+  if (st) return st;
+  if ((int64_t)tot[1] > cap || (int64_t)tot[2] > cap) return fail(ctx, NC_E_OOM, "halo buffer too small");
+  counts[0] = tot[1];
+  counts[1] = tot[2];
+  return NC_OK;
+}
+
+nc_status nc_slab_forces(nc_ctx* ctx, const void* q, const uint32_t* gid, int64_t n_own, const void* halo_from_lo,
+                         int64_t n_lo, const void* halo_from_hi, int64_t n_hi, int klo, int khi, void* F,
+                         double* layer_parts) {
+  if (!ctx || (n_own > 0 && (!q || !gid))) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
+  if (klo < 0 || khi > ctx->g.dims[2] || khi - klo < 1) return fail(ctx, NC_E_ARG, "bad layer range");
+  return ctx->cfg.prec == NC_F32
+             ? slab_forces_t<float>(ctx, (const float*)q, gid, n_own, halo_from_lo, n_lo, halo_from_hi, n_hi, klo, khi,
+                                    (float*)F, layer_parts)
+             : slab_forces_t<double>(ctx, (const double*)q, gid, n_own, halo_from_lo, n_lo, halo_from_hi, n_hi, klo,
+                                     khi, (double*)F, layer_parts);
+}
+
+nc_status nc_slab_kick(nc_ctx* ctx, void* p, const void* F, int64_t n, double dt) {
+  if (!ctx || (n > 0 && (!p || !F))) return fail(ctx, NC_E_ARG, "null argument");
+  if (n <= 0) return NC_OK;
+  SllodParams sp;
+  sllod_params(ctx, dt, sp);
+  prof_begin(ctx);
+  if (ctx->cfg.prec == NC_F32)
+    k_kick3<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)p, (const float*)F, sp);
+  else
+    k_kick3<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)p, (const double*)F, sp);
+  LAUNCHED();
+  prof_end(ctx, NC_K_KICK);
+  return NC_OK;
+}
+
+nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* U, double W[6], double stats[4]) {
+  if (!ctx || !parts || nlayers < 1) return fail(ctx, NC_E_ARG, "null argument");
+  // the same fixed-order sum as k_reduce_total, then the same frame rotation as a single-device evaluation
+  for (int c = 0; c < NPART; ++c) {
+    double v = 0;
+    for (int l = 0; l < nlayers; ++l) v += parts[(int64_t)l * NPART + c];
+    ctx->host_tot[c] = v;
+  }
+  ctx->tot_valid = true;
+  ctx->have_eval = true;
+  bool ok = ctx->host_tot[11] == 0.0;
+  for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
+  totals_to_UW(ctx, U, W);
+  if (stats) { stats[0] = ctx->host_tot[7]; stats[1] = ctx->host_tot[8]; stats[2] = ctx->host_tot[9]; stats[3] = ctx->host_tot[10]; }
+  if (!ok) return fail(ctx, NC_E_NONFINITE, "non-finite force, energy or virial");
   return NC_OK;
 }
 

@@ -25,7 +25,8 @@ STATUS = {0: "NC_OK", 1: "NC_E_ARG", 2: "NC_E_BOX", 3: "NC_E_DEGENERATE", 4: "NC
 EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cells", "nc_compute_forces",
            "nc_set_state", "nc_step_sllod", "nc_get_state", "nc_get_cells", "nc_get_pair_digest", "nc_get_stats",
            "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
-           "nc_profile_read"]
+           "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_migrate", "nc_slab_unpack",
+           "nc_slab_halo", "nc_slab_forces", "nc_slab_kick", "nc_slab_reduce"]
 KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
 
 
@@ -88,6 +89,14 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_get_stencil_histogram.argtypes = [vp, vp]
         L.nc_profile.argtypes = [vp, i32]
         L.nc_profile_read.argtypes = [vp, vp, vp]
+        L.nc_slab_layers.argtypes = [vp, i32, i32, vp, vp, vp]
+        L.nc_slab_kick_drift.argtypes = [vp, vp, vp, vp, i64, d]
+        L.nc_slab_migrate.argtypes = [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp]
+        L.nc_slab_unpack.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.nc_slab_halo.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, i64, vp]
+        L.nc_slab_forces.argtypes = [vp, vp, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]
+        L.nc_slab_kick.argtypes = [vp, vp, vp, i64, d]
+        L.nc_slab_reduce.argtypes = [vp, vp, i32, vp, vp, vp]
         L.nc_launch_count.argtypes = [vp]
         L.nc_launch_count.restype = i64
         L.nc_last_error.argtypes = [vp]
@@ -226,6 +235,57 @@ def nc_profile_read(ctx) -> dict:
     cnt = np.zeros(8, dtype=np.int64)
     _check(ctx, load().nc_profile_read(ctx, _ptr(ms), _ptr(cnt)))
     return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_IDS)}
+
+
+# ----------------------------------------------------------------- slab (multi-GPU) primitives
+
+def nc_slab_layers(ctx, rank: int, nranks: int):
+    lo, hi, l3 = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _check(ctx, load().nc_slab_layers(ctx, int(rank), int(nranks), ctypes.byref(lo), ctypes.byref(hi),
+                                      ctypes.byref(l3)))
+    return lo.value, hi.value, l3.value
+
+
+def nc_slab_kick_drift(ctx, q, p, F, n: int, dt: float) -> None:
+    _check(ctx, load().nc_slab_kick_drift(ctx, _ptr(q), _ptr(p), _ptr(F), int(n), float(dt)))
+
+
+def nc_slab_migrate(ctx, q, p, gid, n, klo, khi, q_out, p_out, gid_out, send_lo, send_hi, cap):
+    c = np.zeros(3, dtype=np.int64)
+    _check(ctx, load().nc_slab_migrate(ctx, _ptr(q), _ptr(p), _ptr(gid), int(n), int(klo), int(khi), _ptr(q_out),
+                                       _ptr(p_out), _ptr(gid_out), _ptr(send_lo), _ptr(send_hi), int(cap), _ptr(c)))
+    return int(c[0]), int(c[1]), int(c[2])
+
+
+def nc_slab_unpack(ctx, rec, n, q, p, gid) -> None:
+    _check(ctx, load().nc_slab_unpack(ctx, _ptr(rec), int(n), _ptr(q), _ptr(p), _ptr(gid)))
+
+
+def nc_slab_halo(ctx, q, gid, n, klo, khi, halo_lo, halo_hi, cap):
+    c = np.zeros(2, dtype=np.int64)
+    _check(ctx, load().nc_slab_halo(ctx, _ptr(q), _ptr(gid), int(n), int(klo), int(khi), _ptr(halo_lo),
+                                    _ptr(halo_hi), int(cap), _ptr(c)))
+    return int(c[0]), int(c[1])
+
+
+def nc_slab_forces(ctx, q, gid, n_own, h_lo, n_lo, h_hi, n_hi, klo, khi, F, want_parts=True):
+    parts = np.zeros((khi - klo, 12)) if want_parts else None
+    _check(ctx, load().nc_slab_forces(ctx, _ptr(q), _ptr(gid), int(n_own), _ptr(h_lo), int(n_lo), _ptr(h_hi),
+                                      int(n_hi), int(klo), int(khi), _ptr(F), _ptr(parts)))
+    return parts
+
+
+def nc_slab_kick(ctx, p, F, n, dt) -> None:
+    _check(ctx, load().nc_slab_kick(ctx, _ptr(p), _ptr(F), int(n), float(dt)))
+
+
+def nc_slab_reduce(ctx, parts: np.ndarray):
+    parts = np.ascontiguousarray(parts, dtype=np.float64)
+    U = ctypes.c_double()
+    W = np.zeros(6)
+    st = np.zeros(4)
+    _check(ctx, load().nc_slab_reduce(ctx, _ptr(parts), int(parts.shape[0]), ctypes.byref(U), _ptr(W), _ptr(st)))
+    return U.value, W, {"interactions": st[0], "candidates": st[1], "stencil_cells": st[2], "rechecks": st[3]}
 
 
 def nc_launch_count(ctx) -> int:

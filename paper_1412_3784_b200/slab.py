@@ -1,0 +1,234 @@
+"""Slab decomposition of the cell-list path over several GPUs.
+
+One rank per GPU.  The box is cut into slabs of whole cell layers along the
+third lattice direction (lambda_3: DS layer floor(lambda_3 c_3), DO layer
+floor(z/w_3) with z = r_33 lambda_3 -- the same axis for both variants, so the
+DO rearrangement never crosses a slab).  Rank r owns layers
+[floor(r l3/P), floor((r+1) l3/P)).  One SLLOD step:
+
+  kick + drift (own particles)                      nc_slab_kick_drift
+  wrap, split leavers by layer, pack                nc_slab_migrate
+  exchange migration records with r-1, r+1          transport
+  append arrivals                                   nc_slab_unpack
+  pack the two boundary layers as halo records      nc_slab_halo
+  exchange halo records with r-1, r+1               transport
+  cells over own + halo, K3 over own layers only    nc_slab_forces
+  second kick                                       nc_slab_kick
+  layer partials all-gathered, fixed-order sum      nc_slab_reduce
+
+Every arithmetic step runs in libnemdcell.so; this module only moves buffers
+(torch.distributed P2P: NCCL over NVLink between GPUs, gloo on CPU) and keeps
+the bookkeeping.  Halo = one cell layer (thickness >= r_c), positions + gid
+only; full i-side accumulation means no reverse force communication.
+Results are bitwise identical to a single-device evaluation (same cell
+contents in (cell, gid) order, same per-layer reductions, same final sum).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import nemdcell as nc
+
+NPART = 12
+
+
+class SlabRank:
+    """State of one rank: own particles (device tensors), its context, buffers."""
+
+    def __init__(self, rank: int, nranks: int, *, variant="do", prec="f32", rc=2.5, eps=1.0, sigma=1.0,
+                 u_shift=None, mass=1.0, capacity=1 << 16, max_cells=0, device=0, stream=None):
+        import torch
+
+        self.torch = torch
+        self.rank, self.nranks = rank, nranks
+        self.cl = nc.CellList(variant, prec, rc=rc, eps=eps, sigma=sigma, u_shift=u_shift, mass=mass,
+                              capacity=capacity, max_cells=max_cells, device=device, stream=stream)
+        self.ctx = self.cl.ctx
+        self.dev = f"cuda:{device}"
+        self.dtype = self.cl.dtype
+        self.cap = capacity
+        t = lambda *s: torch.zeros(*s, dtype=self.dtype, device=self.dev)  # noqa: E731
+        self.q, self.p, self.F = t(capacity, 3), t(capacity, 3), t(capacity, 3)
+        self.q2, self.p2 = t(capacity, 3), t(capacity, 3)
+        self.gid = torch.zeros(capacity, dtype=torch.int32, device=self.dev)
+        self.gid2 = torch.zeros_like(self.gid)
+        self.bcap = max(4096, capacity // 4)
+        self.send = [t(self.bcap, 8), t(self.bcap, 8)]           # migration records to r-1, r+1
+        self.recv = [t(self.bcap, 8), t(self.bcap, 8)]           # from r-1, r+1
+        self.hsend = [t(self.bcap, 4), t(self.bcap, 4)]          # halo records to r-1, r+1
+        self.hrecv = [t(self.bcap, 4), t(self.bcap, 4)]
+        self.n = 0
+
+    def set_flow(self, A, policy, t0, **kw):
+        self.cl.set_flow(A, policy, t0, **kw)
+
+    def layers(self):
+        return nc.nc_slab_layers(self.ctx, self.rank, self.nranks)
+
+    def load(self, q_own, p_own, gid_own):
+        n = len(q_own)
+        assert n <= self.cap
+        self.q[:n].copy_(self.torch.as_tensor(q_own))
+        self.p[:n].copy_(self.torch.as_tensor(p_own))
+        self.gid[:n].copy_(self.torch.as_tensor(np.asarray(gid_own, dtype=np.int32)))
+        self.n = n
+
+    # ---------------------------------------------------------------- phases
+    def kick_drift(self, dt):
+        nc.nc_slab_kick_drift(self.ctx, self.q, self.p, self.F, self.n, dt)
+
+    def migrate(self):
+        klo, khi, _ = self.layers()
+        ns, nlo, nhi = nc.nc_slab_migrate(self.ctx, self.q, self.p, self.gid, self.n, klo, khi, self.q2, self.p2,
+                                          self.gid2, self.send[0], self.send[1], self.bcap)
+        self.q, self.q2 = self.q2, self.q
+        self.p, self.p2 = self.p2, self.p
+        self.gid, self.gid2 = self.gid2, self.gid
+        self.n = ns
+        return (self.send[0], nlo, self.send[1], nhi)
+
+    def absorb(self, from_lo, n_lo, from_hi, n_hi):
+        for rec, k in ((from_lo, n_lo), (from_hi, n_hi)):
+            if k:
+                assert self.n + k <= self.cap, "slab capacity exceeded"
+                nc.nc_slab_unpack(self.ctx, rec, k, self.q[self.n:], self.p[self.n:], self.gid[self.n:])
+                self.n += k
+
+    def halo(self):
+        if self.nranks == 1:  # a single slab wraps onto itself: no halo
+            return (self.hsend[0], 0, self.hsend[1], 0)
+        klo, khi, _ = self.layers()
+        nlo, nhi = nc.nc_slab_halo(self.ctx, self.q, self.gid, self.n, klo, khi, self.hsend[0], self.hsend[1],
+                                   self.bcap)
+        return (self.hsend[0], nlo, self.hsend[1], nhi)
+
+    def forces(self, h_lo, n_lo, h_hi, n_hi, want_parts=True):
+        klo, khi, _ = self.layers()
+        return nc.nc_slab_forces(self.ctx, self.q, self.gid, self.n, h_lo, n_lo, h_hi, n_hi, klo, khi, self.F,
+                                 want_parts)
+
+    def kick(self, dt):
+        nc.nc_slab_kick(self.ctx, self.p, self.F, self.n, dt)
+
+    def reduce(self, all_parts):
+        return nc.nc_slab_reduce(self.ctx, all_parts)
+
+    def close(self):
+        self.cl.close()
+
+
+# -------------------------------------------------------------------- transports
+
+class LoopbackTransport:
+    """All ranks in one process (tests on one GPU): rank r's send_lo is rank r-1's
+    from_hi, its send_hi is rank r+1's from_lo (periodic in the rank index)."""
+
+    def exchange(self, sends, recv_bufs):
+        P = len(sends)
+        out = []
+        for r in range(P):
+            lo_src = sends[(r - 1) % P]   # rank r-1 sends its upper boundary up
+            hi_src = sends[(r + 1) % P]   # rank r+1 sends its lower boundary down
+            b_lo, b_hi = recv_bufs[r]
+            n_lo, n_hi = lo_src[3], hi_src[1]
+            b_lo[:n_lo].copy_(lo_src[2][:n_lo])
+            b_hi[:n_hi].copy_(hi_src[0][:n_hi])
+            out.append((b_lo, n_lo, b_hi, n_hi))
+        return out
+
+    def gather(self, parts):
+        return np.concatenate(parts, axis=0)
+
+
+class DistTransport:
+    """One rank of a torch.distributed group (NCCL between GPUs, gloo on CPU).
+    Messages to one peer are matched in issue order: each rank sends to r-1
+    first, then to r+1, and receives from r+1 first, then from r-1."""
+
+    def __init__(self, rank, nranks, device):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist = torch, dist
+        self.rank, self.P = rank, nranks
+        self.device = device
+
+    def _p2p(self, tensors_out, tensors_in):
+        dist = self.dist
+        lo, hi = (self.rank - 1) % self.P, (self.rank + 1) % self.P
+        ops = [dist.P2POp(dist.isend, tensors_out[0], lo), dist.P2POp(dist.isend, tensors_out[1], hi),
+               dist.P2POp(dist.irecv, tensors_in[1], hi), dist.P2POp(dist.irecv, tensors_in[0], lo)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+
+    def exchange(self, sends, recv_bufs):
+        torch = self.torch
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        b_lo, b_hi = recv_bufs[0]
+        cnt_out = [torch.tensor([n_lo], dtype=torch.int64, device=self.device),
+                   torch.tensor([n_hi], dtype=torch.int64, device=self.device)]
+        cnt_in = [torch.zeros(1, dtype=torch.int64, device=self.device) for _ in range(2)]
+        self._p2p(cnt_out, cnt_in)
+        m_lo, m_hi = int(cnt_in[0].item()), int(cnt_in[1].item())
+        assert m_lo <= len(b_lo) and m_hi <= len(b_hi), "receive buffer too small"
+        self._p2p([s_lo[:max(n_lo, 1)], s_hi[:max(n_hi, 1)]], [b_lo[:max(m_lo, 1)], b_hi[:max(m_hi, 1)]])
+        return [(b_lo, m_lo, b_hi, m_hi)]
+
+    def gather(self, parts):
+        torch, dist = self.torch, self.dist
+        part, = parts
+        n = torch.tensor([part.shape[0]], dtype=torch.int64, device=self.device)
+        ns = [torch.zeros(1, dtype=torch.int64, device=self.device) for _ in range(self.P)]
+        dist.all_gather(ns, n)
+        mx = max(int(x.item()) for x in ns)
+        buf = torch.zeros((mx, NPART), dtype=torch.float64, device=self.device)
+        buf[:part.shape[0]] = torch.as_tensor(part, device=self.device)
+        bufs = [torch.zeros_like(buf) for _ in range(self.P)]
+        dist.all_gather(bufs, buf)
+        return np.concatenate([b[:int(k.item())].cpu().numpy() for b, k in zip(bufs, ns)], axis=0)
+
+
+# -------------------------------------------------------------------- driver
+
+def own_particles(cl_full, q_all, rank, nranks):
+    """Initial split (not on the timed path): the layer of every particle from
+    the library's own cell keys of the full system; returns the own indices."""
+    n = len(q_all)
+    nc.nc_build_cells(cl_full.ctx, q_all, n)
+    cell = np.zeros(n, dtype=np.int64)
+    dims = np.zeros(3, dtype=np.int32)
+    nc._check(cl_full.ctx, nc.load().nc_get_cells(cl_full.ctx, nc._ptr(cell), None, nc._ptr(dims), None))
+    layer = cell // (int(dims[0]) * int(dims[1]))
+    l3 = int(dims[2])
+    klo, khi = rank * l3 // nranks, (rank + 1) * l3 // nranks
+    return np.nonzero((layer >= klo) & (layer < khi))[0]
+
+
+class SlabSystem:
+    """Runs the slab step for the local ranks through a transport (loopback: all
+    ranks here; distributed: the one rank of this process)."""
+
+    def __init__(self, ranks, transport):
+        self.ranks = ranks
+        self.tr = transport
+
+    def forces(self, want_uw=True):
+        hs = [r.halo() for r in self.ranks]
+        hr = self.tr.exchange(hs, [r.hrecv for r in self.ranks])
+        parts = [r.forces(*h, want_parts=want_uw) for r, h in zip(self.ranks, hr)]
+        if not want_uw:
+            return None
+        allp = self.tr.gather(parts)
+        return self.ranks[0].reduce(allp)
+
+    def step(self, dt, want_uw=True):
+        for r in self.ranks:
+            r.kick_drift(dt)
+        sends = [r.migrate() for r in self.ranks]
+        recvs = self.tr.exchange(sends, [r.recv for r in self.ranks])
+        for r, rv in zip(self.ranks, recvs):
+            r.absorb(*rv)
+        out = self.forces(want_uw)
+        for r in self.ranks:
+            r.kick(dt)
+        return out
