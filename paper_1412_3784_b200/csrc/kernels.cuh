@@ -1277,27 +1277,21 @@ __global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_const
 }
 
 constexpr int PART_T = 256;
-// per-block counts of classes 0..3
-__global__ void k_class_count(int64_t n, const uint8_t* __restrict__ cls, uint32_t* __restrict__ bcnt) {
+// per-block counts of classes 0..3, CLASS-MAJOR (bcnt[c * nb + b]) so that one
+// exclusive scan of the 4 nb entries gives every class's block offsets
+__global__ void k_class_count(int64_t n, int64_t nb, const uint8_t* __restrict__ cls, uint32_t* __restrict__ bcnt) {
   __shared__ uint32_t c[4];
   if (threadIdx.x < 4) c[threadIdx.x] = 0;
   __syncthreads();
   int64_t i = (int64_t)blockIdx.x * PART_T + threadIdx.x;
   if (i < n) atomicAdd(&c[cls[i]], 1u);  // counts only: order-free
   __syncthreads();
-  if (threadIdx.x < 4) bcnt[(int64_t)blockIdx.x * 4 + threadIdx.x] = c[threadIdx.x];
+  if (threadIdx.x < 4) bcnt[(int64_t)threadIdx.x * nb + blockIdx.x] = c[threadIdx.x];
 }
-// exclusive scan per class over blocks (single block, sequential per class: nb is small)
-__global__ void k_class_scan(uint32_t* __restrict__ bcnt, int64_t nb, uint32_t* __restrict__ tot) {
+// class totals from the scanned class-major counts (boff has 4 nb + 1 entries)
+__global__ void k_class_totals(const uint32_t* __restrict__ boff, int64_t nb, uint32_t* __restrict__ tot) {
   int c = threadIdx.x;
-  if (c >= 4) return;
-  uint32_t run = 0;
-  for (int64_t b = 0; b < nb; ++b) {
-    uint32_t v = bcnt[b * 4 + c];
-    bcnt[b * 4 + c] = run;
-    run += v;
-  }
-  tot[c] = run;
+  if (c < 4) tot[c] = boff[(c + 1) * nb] - boff[c * nb];
 }
 // stable partition by class (index order within each class): class 0 -> SoA outputs, classes 1, 2 ->
 // records of `words` T4 words (2: q+gid, p; 1: q+gid)
@@ -1319,7 +1313,8 @@ __global__ void k_class_scatter(int64_t n, const uint8_t* __restrict__ cls, cons
   }
   __syncthreads();
   if (c >= 3) return;
-  uint32_t pos = boff[(int64_t)blockIdx.x * 4 + c] + rank_in_warp;
+  const int64_t nb = gridDim.x;
+  uint32_t pos = boff[(int64_t)c * nb + blockIdx.x] - boff[(int64_t)c * nb] + rank_in_warp;
   for (int w = 0; w < wid; ++w) pos += wsum[w][c];
   const T x = q[3 * i], y = q[3 * i + 1], z = q[3 * i + 2];
   const uint32_t gg = gid[i];

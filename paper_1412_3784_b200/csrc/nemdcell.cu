@@ -52,7 +52,7 @@ struct nc_ctx {
   uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr, *tmp = nullptr, *tmpgid = nullptr;
   uint32_t *counts = nullptr, *cs = nullptr, *bsum = nullptr, *tot = nullptr;
   // slab (multi-GPU) scratch
-  uint32_t *gin = nullptr, *sidx = nullptr, *pbcnt = nullptr, *ptot = nullptr;
+  uint32_t *gin = nullptr, *sidx = nullptr, *pbcnt = nullptr, *pboff = nullptr, *ptot = nullptr;
   uint8_t* cls = nullptr;
   double *bpart = nullptr, *lpart = nullptr, *part_tot = nullptr, *part_acc = nullptr;
   // digest
@@ -509,11 +509,16 @@ nc_status partition(nc_ctx* ctx, int64_t n, const T* q, const T* p, const uint32
   int64_t nb = (n + PART_T - 1) / PART_T;
   if (n > 0) {
     prof_begin(ctx);
-    k_class_count<<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pbcnt);
+    k_class_count<<<(unsigned)nb, PART_T, 0, s>>>(n, nb, ctx->cls, ctx->pbcnt);
     LAUNCHED();
-    k_class_scan<<<1, 32, 0, s>>>(ctx->pbcnt, nb, ctx->ptot);
+    const int64_t m = 4 * nb;
+    const int64_t sb = (m + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_reduce<<<(unsigned)sb, SCAN_T, 0, s>>>(ctx->pbcnt, m, ctx->bsum);
+    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, sb, ctx->tot);
+    k_scan_apply<<<(unsigned)sb, SCAN_T, 0, s>>>(ctx->pbcnt, m, ctx->bsum, ctx->pboff, ctx->tot);
+    k_class_totals<<<1, 32, 0, s>>>(ctx->pboff, nb, ctx->ptot);
     LAUNCHED();
-    k_class_scatter<T><<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pbcnt, q, p, gid, q0, p0, g0, r1, r2, words);
+    k_class_scatter<T><<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pboff, q, p, gid, q0, p0, g0, r1, r2, words);
     LAUNCHED();
     prof_end(ctx, NC_K_OTHER);
     CK(cudaMemcpyAsync(tot_out, ctx->ptot, 16, cudaMemcpyDeviceToHost, s));
@@ -667,7 +672,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {(void**)&ctx->dcnt, 4 * N_}, {(void**)&ctx->dhs, 8 * N_}, {(void**)&ctx->dhx, 8 * N_},
       {(void**)&ctx->hist, 8 * 64},
       {(void**)&ctx->gin, 4 * N_}, {(void**)&ctx->sidx, 4 * N_}, {(void**)&ctx->cls, N_},
-      {(void**)&ctx->pbcnt, 16 * (N_ / PART_T + 2)}, {(void**)&ctx->ptot, 16},
+      {(void**)&ctx->pbcnt, 16 * (N_ / PART_T + 2)}, {(void**)&ctx->pboff, 16 * (N_ / PART_T + 2) + 4},
+      {(void**)&ctx->ptot, 16},
   };
   for (auto& a : allocs) {
     e = cudaMalloc(a.p, a.bytes);
@@ -695,7 +701,7 @@ void nc_destroy(nc_ctx* ctx) {
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->tmp, ctx->tmpgid, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
                 ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
-                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->ptot};
+                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot};
   for (void* p : ps)
     if (p) cudaFree(p);
   for (auto& p : ctx->prof_ev) {
