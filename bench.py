@@ -113,6 +113,15 @@ def dist_setup(backend):
     return rank, lrank, ws
 
 
+def box_text(w):
+    return {"none": "equilibrium cube", "le": "Lees-Edwards shear", "kr": "KR planar elongation",
+            "gkr": "generalized KR " + str(w.extra.get("flow", ""))}[w.policy] + f", dt={w.dt}"
+
+
+def pot_text(w):
+    return ("WCA" if w.potential == "wca" else "LJ") + f" rc={w.rc:.4f} shifted"
+
+
 def workload(k: int):
     from paper_1412_3784_b200 import workloads as W
 
@@ -188,7 +197,7 @@ def run_slab(args):
         kw["tstar"] = w.extra["tstar"]
     if w.policy == "gkr":
         kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
-    maxc = int(2.5 * w.n / 13) + 65536
+    maxc = 0
     full = CellList(args.variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=maxc, device=lrank)
     full.set_flow(w.A, w.policy, w.t0, **kw)
     idx = own_particles(full, torch.from_numpy(q).to(f"cuda:{lrank}"), rank, ws)
@@ -247,7 +256,7 @@ def run_slab(args):
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
             "config": {"workload": f"C{args.config}", "n_total": w.n, "variant": args.variant,
-                       "box": "KR planar elongation, eps=0.1, dt=0.002", "potential": "LJ rc=2.5 shifted",
+                       "box": box_text(w), "potential": pot_text(w),
                        "precision": "fp32 storage + fp32 filter, fp64 interactions",
                        "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
                                                                    "NCCL P2P halo + migration"},
@@ -277,7 +286,7 @@ def run_ours(args):
     p = W.momenta(w, dtype=np.float32, k=args.config, r=0)
     stream = torch.cuda.Stream(lrank)
     cl = CellList(args.variant, "f32", rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
-                  capacity=w.n, max_cells=int(2.5 * w.n / 13) + 65536, device=lrank, stream=stream.cuda_stream)
+                  capacity=w.n, max_cells=0, device=lrank, stream=stream.cuda_stream)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
@@ -388,7 +397,7 @@ def run_ours(args):
             "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
             "config": {"workload": f"C{args.config}", "n_per_gpu": w.n, "variant": args.variant,
-                       "box": "KR planar elongation, eps=0.1, dt=0.002", "potential": "LJ rc=2.5 shifted",
+                       "box": box_text(w), "potential": pot_text(w),
                        "precision": "fp32 storage + fp32 filter, fp64 interactions",
                        "l2": "inputs (~7 GB) >> L2 (126 MB); no flush", "parallelism": f"replicas x{ws}"},
             "particle_steps_per_s": psteps,

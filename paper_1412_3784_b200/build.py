@@ -17,6 +17,9 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off",
     "-shared",
+    # one CUDA runtime per process: share libcudart.so.12 with torch instead of a
+    # private static copy (two runtimes tearing down the same context at exit crashed)
+    "-cudart", "shared", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
 ]
 
 

@@ -603,12 +603,13 @@ int64_t nc_launch_count(const nc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 nc_status nc_profile(nc_ctx* ctx, int enable) {
   if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  CK(cudaStreamSynchronize(ctx->stream));  // recorded events may still be pending
   for (auto& p : ctx->prof_ev) {
     ctx->ev_pool.push_back(p.second.first);
     ctx->ev_pool.push_back(p.second.second);
   }
+  ctx->prof_ev.clear();  // every event now lives in exactly one list (destroyed once)
   if (enable) {
-    ctx->prof_ev.clear();
     CK(cudaMemsetAsync(ctx->part_acc, 0, sizeof(double) * (NPART + 1), ctx->stream));
   }
   ctx->prof = enable != 0;
