@@ -323,7 +323,7 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 32;  // permanent far element (padding slot of the evaluation)
 constexpr int K3_STAGE = K3_CAP + 33;  // + up to S far sentinels so the filter needs no bounds checks
-constexpr int K3_QCAP = 32;     // per-lane queue of filter survivors (shared addresses / staged indices)
+constexpr int K3_QCAP = 64;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
 constexpr int K3_UNROLL = 8;    // filter candidates per lane between queue-full votes
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
 constexpr int K3_CELLS = 4;     // cells per warp (= per block: one warp per block)
@@ -343,7 +343,7 @@ template <typename T>
 struct K3Smem {
   typename V4<T>::t stage[K3_STAGE];  // filter copy, .w = sorted index
   K3Stage64<T> s64;
-  uint32_t queue[K3_QCAP][32];
+  uint16_t queue[K3_QCAP][32];
   uint8_t sent[K3_STAGE];
   uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
   int32_t e_n[K3_MAXE][3];
@@ -634,7 +634,7 @@ __device__ __forceinline__ void filter_chunk(const Geom& g, const PairCtx<T>& pc
 #pragma unroll
     for (int k = 0; k < K3_UNROLL; ++k) {
       bool hit = filter_one<T>(g, pc, sm, t);
-      sm.queue[qlen][lane] = t;
+      sm.queue[qlen][lane] = (uint16_t)t;
       qlen += hit ? 1 : 0;
       t += (uint32_t)S;
     }
@@ -645,7 +645,7 @@ __device__ __forceinline__ void filter_chunk(const Geom& g, const PairCtx<T>& pc
   }
   for (; it < iters; ++it) {
     bool hit = filter_one<T>(g, pc, sm, t);
-    sm.queue[qlen][lane] = t;
+    sm.queue[qlen][lane] = (uint16_t)t;
     qlen += hit ? 1 : 0;
     t += (uint32_t)S;
   }
@@ -668,9 +668,18 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
-// a += 128 if r2 < hi (one FSETP + one predicated IADD)
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+// full shared address of a staged element from the low 16 bits kept in a queue
+// (the staged array spans < 64 KB, so one possible carry into bit 16)
+__device__ __forceinline__ uint32_t addr_from16(uint32_t lo16, uint32_t stage0) {
+  uint32_t a = (stage0 & 0xffff0000u) | lo16;
+  return a < stage0 ? a + 0x10000u : a;
+}
+// a += 64 (one queue row of 32 u16) if r2 < hi (one FSETP + one predicated IADD)
 __device__ __forceinline__ uint32_t bump_if_less(uint32_t a, float r2, float hi) {
-  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, 128;\n\t}" : "+r"(a) : "f"(r2), "f"(hi));
+  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, 64;\n\t}" : "+r"(a) : "f"(r2), "f"(hi));
   return a;
 }
 
@@ -697,8 +706,8 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   const uint32_t dummy = stage0 + 16u * K3_DUMMY;
   for (int k = 0; k < qmax; k += 2) {
-    const uint32_t aa = k < qlen ? sm.queue[k][lane] : dummy;
-    const uint32_t ab = k + 1 < qlen ? sm.queue[k + 1][lane] : dummy;
+    const uint32_t aa = k < qlen ? addr_from16(sm.queue[k][lane], stage0) : dummy;
+    const uint32_t ab = k + 1 < qlen ? addr_from16(sm.queue[k + 1][lane], stage0) : dummy;
     const uint32_t ta = (aa - stage0) >> 4, tb = (ab - stage0) >> 4;
     const uint32_t ja = __float_as_uint(sm.stage[ta].w), jb = __float_as_uint(sm.stage[tb].w);
     const int ea = sm.sent[ta], eb = sm.sent[tb];
@@ -758,12 +767,12 @@ __device__ __forceinline__ void eval_pairs_f32(const Geom& g, const PairCtx<floa
     nclose = 0;
     for (int k = 0; k < qmax; ++k) {
       const bool valid = k < qlen;
-      const uint32_t a = valid ? sm.queue[k][lane] : dummy;
+      const uint32_t a = valid ? addr_from16(sm.queue[k][lane], stage0) : dummy;
       const float4 v = lds128(a);
       const float dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       const bool far = valid && r2 >= split2 && r2 < lo32;
-      sm.queue[nclose][lane] = a;   // in-place compaction (nclose <= k)
+      sm.queue[nclose][lane] = (uint16_t)a;   // in-place compaction (nclose <= k)
       nclose += (valid && !far) ? 1 : 0;
       float ir2;
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
@@ -789,7 +798,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
                                                  const double4* __restrict__ u64) {
   const uint32_t stage0 = smem_u32(&sm.stage[0]);
   const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
-  const uint32_t qlim = q0 + 128u * (K3_QCAP - K3_UNROLL);
+  const uint32_t qlim = q0 + 64u * (K3_QCAP - K3_UNROLL);
   const uint32_t step = 16u * (uint32_t)S;
   const float ux = pc.fx, uy = pc.fy, uz = pc.fz, hi = pc.hi;
   uint32_t sa = stage0 + 16u * (uint32_t)s;
@@ -805,7 +814,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
         float4 v = lds128(sa);
         float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
         float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        sts32(qa, sa);
+        sts16(qa, sa);
         qa = bump_if_less(qa, r2, hi);
         sa += step;
       }
@@ -817,13 +826,13 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
         float4 v = lds128(sa);
         float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
         float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        sts32(qa, sa);
+        sts16(qa, sa);
         qa = bump_if_less(qa, r2, hi);
         sa += step;
       }
     }
     __syncwarp();
-    eval_pairs_f32<DIGEST>(g, pc, sm, acc, a32, (int)((qa - q0) >> 7), lane, stage0, u64);  // the single call site
+    eval_pairs_f32<DIGEST>(g, pc, sm, acc, a32, (int)((qa - q0) >> 6), lane, stage0, u64);  // the single call site
     qa = q0;
     if (it >= iters) break;
   }
