@@ -452,6 +452,8 @@ template <typename T>
 struct PairCtx {
   double ux, uy, uz;   // i: fp32 mode = rotated cell-local fp64; fp64 mode = lab position
   T fx, fy, fz;        // i cell-local, filter precision (fp32 mode)
+  float m2x, m2y, m2z, uu;  // fp32 filter: -2 u_i and |u_i|^2 (r^2 = (|v|^2 + |u|^2) + v.(-2u))
+  uint32_t base_off;   // staging offset of the current chunk (sorted index of a staged element: see sidx_of)
   uint32_t my;         // i sorted index
   T hi;                // fp32 filter bound on r^2 (superset of the pair set)
   double lo64, hi64;   // band on the fp64 r^2 where the canonical test decides
@@ -616,7 +618,9 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // Far-away sentinel for padding the staged list (never passes the filter).
 template <typename T> __device__ __forceinline__ typename V4<T>::t far4();
-template <> __device__ __forceinline__ float4 far4<float>() { return make_float4(1e30f, 1e30f, 1e30f, 0.f); }
+template <> __device__ __forceinline__ float4 far4<float>() {
+  return make_float4(1e30f, 1e30f, 1e30f, __int_as_float(0x7f800000));  // |v|^2 = +inf
+}
 template <> __device__ __forceinline__ double4 far4<double>() { return make_double4(1e300, 1e300, 1e300, 0.0); }
 
 // Filter stream s of the staged chunk: t = s, s+S, ... for `iters` steps
@@ -699,6 +703,12 @@ __device__ __forceinline__ void fold32(Acc& acc, Acc32& a) {
 // Close tier: survivors with r < r_split (large forces), in the r_c band, or
 // all survivors in digest mode -- fp64 from the fp64 staged coordinates,
 // canonical membership inside the 1e-12 band.  Two per iteration.
+// sorted particle index of staged element t (entry e = sent[t] of the current chunk)
+__device__ __forceinline__ uint32_t sidx_of(const K3Smem<float>& sm, uint32_t t, uint32_t base_off) {
+  const int e = sm.sent[t];
+  return sm.e_start[e] + t - (sm.e_off[e] - base_off);
+}
+
 template <bool DIGEST>
 __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                int qlen, int lane, uint32_t stage0, const double4* __restrict__ u64) {
@@ -709,7 +719,8 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
     const uint32_t aa = k < qlen ? addr_from16(sm.queue[k][lane], stage0) : dummy;
     const uint32_t ab = k + 1 < qlen ? addr_from16(sm.queue[k + 1][lane], stage0) : dummy;
     const uint32_t ta = (aa - stage0) >> 4, tb = (ab - stage0) >> 4;
-    const uint32_t ja = __float_as_uint(sm.stage[ta].w), jb = __float_as_uint(sm.stage[tb].w);
+    const uint32_t ja = k < qlen ? sidx_of(sm, ta, pc.base_off) : pc.my;
+    const uint32_t jb = k + 1 < qlen ? sidx_of(sm, tb, pc.base_off) : pc.my;
     const int ea = sm.sent[ta], eb = sm.sent[tb];
     const double4 pa = u64[ja], pb = u64[jb];
     const double dxa = (pa.x + sm.e_B[ea][0]) - pc.ux, dya = (pa.y + sm.e_B[ea][1]) - pc.uy,
@@ -800,7 +811,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
   const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
   const uint32_t qlim = q0 + 64u * (K3_QCAP - K3_UNROLL);
   const uint32_t step = 16u * (uint32_t)S;
-  const float ux = pc.fx, uy = pc.fy, uz = pc.fz, hi = pc.hi;
+  const float mx = pc.m2x, my = pc.m2y, mz = pc.m2z, uu = pc.uu, hi = pc.hi;
   uint32_t sa = stage0 + 16u * (uint32_t)s;
   uint32_t qa = q0;
   int it = 0;
@@ -812,8 +823,9 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 #pragma unroll
       for (int k = 0; k < K3_UNROLL; ++k) {
         float4 v = lds128(sa);
-        float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
-        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        // r^2 = (|v|^2 + |u|^2) - 2 v.u: 1 FADD + 3 FFMA; cancellation error <~ 1e-5 sigma^2, far inside
+        // the superset band (R16 membership is decided later in fp64)
+        float r2 = fmaf(v.z, mz, fmaf(v.y, my, fmaf(v.x, mx, v.w + uu)));
         sts16(qa, sa);
         qa = bump_if_less(qa, r2, hi);
         sa += step;
@@ -824,8 +836,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     if (!full) {  // remainder (< K3_UNROLL iterations; every queue has room for them)
       for (; it < iters; ++it) {
         float4 v = lds128(sa);
-        float dx = v.x - ux, dy = v.y - uy, dz = v.z - uz;
-        float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        float r2 = fmaf(v.z, mz, fmaf(v.y, my, fmaf(v.x, mx, v.w + uu)));
         sts16(qa, sa);
         qa = bump_if_less(qa, r2, hi);
         sa += step;
@@ -925,6 +936,8 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         pc.ux = ui.x; pc.uy = ui.y; pc.uz = ui.z;
         pc.fx = act ? uf.x : -1e30f;  // ghost lanes never pass the filter
         pc.fy = uf.y; pc.fz = uf.z;
+        pc.m2x = -2.0f * pc.fx; pc.m2y = -2.0f * pc.fy; pc.m2z = -2.0f * pc.fz;
+        pc.uu = act ? fmaf(pc.fz, pc.fz, fmaf(pc.fy, pc.fy, pc.fx * pc.fx)) : __int_as_float(0x7f800000);
       } else {
         typename V4<T>::t qi = qs[pc.my];
         pc.ux = act ? qi.x : -1e300; pc.uy = qi.y; pc.uz = qi.z;
@@ -977,9 +990,11 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             }
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-              if (tt[r] < ctot)
-                sm.stage[tt[r]] = make_float4(pp[r].x + sm.s64.Bf[ee[r]][0], pp[r].y + sm.s64.Bf[ee[r]][1],
-                                              pp[r].z + sm.s64.Bf[ee[r]][2], pp[r].w);
+              if (tt[r] < ctot) {
+                const float x = pp[r].x + sm.s64.Bf[ee[r]][0], y = pp[r].y + sm.s64.Bf[ee[r]][1],
+                            z = pp[r].z + sm.s64.Bf[ee[r]][2];
+                sm.stage[tt[r]] = make_float4(x, y, z, fmaf(z, z, fmaf(y, y, x * x)));  // .w = |v|^2
+              }
             }
           }
         } else {
@@ -1006,6 +1021,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         }
         __syncwarp();
         const int iters = (int)((ctot + S - 1) / S);
+        pc.base_off = base_off;
         if constexpr (sizeof(T) == 4) {
           filter_chunk_f32<DIGEST>(g, pc, sm, acc, a32, s, S, iters, lane, u);
         } else {
@@ -1048,16 +1064,24 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, (T)0);
         if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
       }
+      // per-lane partials across the warp's cells; one fixed-order warp reduction at the end
       double fchk = owner ? acc.fx + acc.fy + acc.fz + Ui : 0.0;
-      tU += warp_sum_d(owner ? Ui : 0.0);
-      tW[0] += warp_sum_d(owner ? 0.5 * acc.w0 : 0.0); tW[1] += warp_sum_d(owner ? 0.5 * acc.w1 : 0.0);
-      tW[2] += warp_sum_d(owner ? 0.5 * acc.w2 : 0.0); tW[3] += warp_sum_d(owner ? 0.5 * acc.w3 : 0.0);
-      tW[4] += warp_sum_d(owner ? 0.5 * acc.w4 : 0.0); tW[5] += warp_sum_d(owner ? 0.5 * acc.w5 : 0.0);
-      tI += warp_sum_d(owner ? (double)acc.cnt : 0.0);
-      tR += warp_sum_d(owner ? (double)acc.nrc : 0.0);
-      tNF += warp_sum_d(isfinite(fchk) ? 0.0 : 1.0);
+      if (owner) {
+        tU += Ui;
+        tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
+        tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
+        tI += (double)acc.cnt;
+        tR += (double)acc.nrc;
+      }
+      tNF += isfinite(fchk) ? 0.0 : 1.0;
     }
   }
+  tU = warp_sum_d(tU);
+  tW[0] = warp_sum_d(tW[0]); tW[1] = warp_sum_d(tW[1]); tW[2] = warp_sum_d(tW[2]);
+  tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
+  tI = warp_sum_d(tI);
+  tR = warp_sum_d(tR);
+  tNF = warp_sum_d(tNF);
   if (lane < NPART) {
     double v = 0;
     if (lane == 0) v = tU;

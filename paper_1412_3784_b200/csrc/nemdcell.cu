@@ -159,7 +159,8 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   g.eps = ctx->cfg.eps;
   g.sig2 = ctx->cfg.sigma * ctx->cfg.sigma;
   g.ushift = ctx->cfg.u_shift;
-  double tau = ctx->cfg.prec == NC_F32 ? 2e-5 : 1e-10;  // re-check band, DESIGN.md section 5
+  // fp32 superset band: the dot-form filter's cancellation error (<~ 1e-5 sigma^2) stays far inside it
+  double tau = ctx->cfg.prec == NC_F32 ? 1e-4 : 1e-10;
   g.band_lo = g.rc2 * (1.0 - tau);
   g.band_hi = g.rc2 * (1.0 + tau);
   // two-tier evaluation: fp32 force math only where the LJ force is small
