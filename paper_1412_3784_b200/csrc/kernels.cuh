@@ -1032,11 +1032,11 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
       }
 
       if constexpr (sizeof(T) == 4) fold32(acc, a32);
-      // combine the S streams of each i (fixed order s = 1, 2, ...)
-      for (int s2 = 1; s2 < S; ++s2) {
-        int src = lane + s2 * nb;
-        bool take = (lane < nb) && (src < 32);
-        src &= 31;
+      // combine the S streams of each i: fixed binary tree over s (log2 S shuffle steps)
+      for (int o = 1; o < S; o <<= 1) {
+        const int src_s = s + o;
+        bool take = act && ((s & (2 * o - 1)) == 0) && (src_s < S);
+        const int src = (lane + o * nb) & 31;
         acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
         acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
         acc.w0 = shfl_comb(acc.w0, src, take); acc.w1 = shfl_comb(acc.w1, src, take);
