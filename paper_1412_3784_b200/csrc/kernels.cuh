@@ -361,8 +361,8 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 // n_k = floor(m_k/c_k); bracket B = R(delta/c).  DO: exact
 // interval overlap (R3-R5), bracket
 // B = ((col-a0) w0 + n1 e0 + n2 r12 + n3 r13, (m-a1) w1 + n2 e1 + n3 r23, dz w2 + n3 e2).
-template <typename T>
-__device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int a2, K3Smem<T>& sm, int lane) {
+template <typename SM>
+__device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int a2, SM& sm, int lane) {
   const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
   if (g.variant == 0) {
     if (lane < 27) {
@@ -891,7 +891,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   for (int cl = cbeg; cl < cend; ++cl) {
     const int a0 = cl % l1, a1 = cl / l1, a2 = layer;
     const uint32_t cid = (uint32_t)cl + (uint32_t)per_layer * (uint32_t)layer;
-    const int nst = build_entries<T>(g, a0, a1, a2, sm, lane);
+    const int nst = build_entries(g, a0, a1, a2, sm, lane);
     // entry sizes and staging offsets (exclusive scan over <= 36 entries)
     uint32_t tot = 0;
     for (int e0 = 0; e0 < nst; e0 += 32) {
@@ -1148,7 +1148,7 @@ __global__ void __launch_bounds__(32) k_stencil_hist(const __grid_constant__ Geo
     int a0 = (int)(c % g.dims[0]);
     int a1 = (int)((c / g.dims[0]) % g.dims[1]);
     int a2 = (int)(c / ((int64_t)g.dims[0] * g.dims[1]));
-    int ne = build_entries<float>(g, a0, a1, a2, tab, lane);
+    int ne = build_entries(g, a0, a1, a2, tab, lane);
     if (lane == 0) h[ne]++;
     __syncwarp();
   }
@@ -1405,3 +1405,5 @@ __global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ sr
 }
 
 }  // namespace nc
+
+#include "k3_pairs.cuh"

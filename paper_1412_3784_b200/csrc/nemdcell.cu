@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -141,6 +142,16 @@ bool is_device_ptr(const void* p) {
 
 int cells_per_block() { return K3_CELLS; }
 
+// fp32 pair kernel generation: 1 = k_pairs (v11, default); 2 = k_pairs_v3 (two particles per lane,
+// packed FFMA2 filter; parity-green but slower on C4: 51-57 ms vs 41.6 ms) -- NC_K3=2 for A/B runs.
+int k3_version() {
+  static int v = [] {
+    const char* e = getenv("NC_K3");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
+  return v;
+}
+
 nc_status apply_box(nc_ctx* ctx, const double* L) {
   Geom g;
   int st = make_geom(g, L, (int)ctx->cfg.variant, ctx->cfg.rc);
@@ -166,6 +177,12 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   // two-tier evaluation: fp32 force math only where the LJ force is small
   // (r >= 1.2 sigma: |f| <= 2.4 eps/sigma), fp64 for closer pairs
   g.rsplit2 = 1.44 * g.sig2;
+  g.f_split2 = (float)g.rsplit2;
+  g.f_lo = (float)g.band_lo;
+  g.f_hi = (float)g.band_hi;
+  g.f_sig2 = (float)g.sig2;
+  g.f_c48 = (float)(48.0 * g.eps);
+  g.f_m24 = (float)(-24.0 * g.eps);
   ctx->g = g;
   ctx->have_box = true;
   return NC_OK;
@@ -232,8 +249,25 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
     as = true;
   }
   prof_begin(ctx);
-  k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F,
-                                                         ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+  if constexpr (sizeof(T) == 4) {
+    if (k3_version() == 2) {
+      size_t smem2 = sizeof(V3Smem);
+      static bool attr2[2] = {false, false};
+      if (!attr2[DIGEST]) {
+        CK(cudaFuncSetAttribute(k_pairs_v3<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        attr2[DIGEST] = true;
+      }
+      k_pairs_v3<DIGEST><<<nblocks, 32, smem2, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
+                                                    (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl,
+                                                    layer0);
+    } else {
+      k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
+                                                   ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+    }
+  } else {
+    k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart, ctx->dcnt,
+                                                 ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+  }
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
   int nl = nlay;

@@ -69,9 +69,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
             return _lib
         if build_if_missing and _build.stale():
             _build.build()
-        if not os.path.exists(_build.LIB):
-            raise ImportError(f"libnemdcell.so not found at {_build.LIB}; run paper_1412_3784_b200.build.build()")
-        L = ctypes.CDLL(_build.LIB)
+        path = os.environ.get("NC_LIB") or _build.LIB  # NC_LIB: an alternative build (A/B experiments)
+        if not os.path.exists(path):
+            raise ImportError(f"libnemdcell.so not found at {path}; run paper_1412_3784_b200.build.build()")
+        L = ctypes.CDLL(path)
         vp, i64, i32, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
         L.nc_create.argtypes = [ctypes.POINTER(nc_config), ctypes.POINTER(vp)]
         L.nc_destroy.argtypes = [vp]
