@@ -1,0 +1,459 @@
+// k3_seg.cuh -- K3 for sparse cells (WCA: ~1.3 particles per cell), NC_F32.
+// Included at the end of kernels.cuh.
+//
+// The warp-per-cell kernel (k_pairs) spends almost all of its time on the
+// per-cell neighborhood setup when a cell holds ~1 particle.  Here one warp
+// owns a SEGMENT of G consecutive cells of one row (same a1, a2) and builds
+// the UNION of their neighborhoods once: the stencil rows of the segment
+// (9 DS rows; up to 12 DO rows by the exact interval rule R4,
+// P:673-687), each row's union column range, the neighbor particles staged
+// in shared memory in the segment's frame (cell-local coordinates plus the
+// column's image bracket).  Every lane owns one particle i of the segment and
+// scans exactly its own cell's neighborhood -- the same 27 (DS) or 27/30/34/36
+// (DO) cells as k_pairs, row by row, as contiguous sub-ranges of the staged
+// union -- so the candidate set, the pair set and every count are those of
+// the method.  Filter in fp32 (difference form), superset band as k_pairs;
+// every survivor is evaluated in fp64 from the fp64 cell-local coordinates
+// (WCA pairs all lie below r_split), membership inside the 1e-12 band by the
+// canonical R16 test.  Full i-side accumulation, no atomics, layer-aligned
+// deterministic block partials (one block = one segment).
+#pragma once
+
+namespace nc {
+
+constexpr int SG_CAP = 640;                 // staged union elements
+constexpr int SG_ROWS = 12;                 // stencil rows (DS 9, DO <= 12)
+constexpr int SG_GMAX = 32;                 // cells per segment
+constexpr int SG_MAXE = SG_ROWS * (SG_GMAX + 4);  // union entries (row x column)
+constexpr int SG_QCAP = 32;                 // per-lane hit queue
+
+struct SgSmem {
+  float4 stage[SG_CAP];                     // segment-frame x, y, z; w = sorted index bits
+  uint32_t e_start[SG_MAXE];                // first sorted particle of the entry's cell
+  uint16_t e_off[SG_MAXE + 1];              // staging offset of the entry
+  uint16_t sent[SG_CAP];                    // entry of each staged element
+  uint8_t e_row[SG_MAXE];
+  uint8_t e_ci[SG_MAXE];                    // column index inside the row's union range
+  uint16_t rg[SG_GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
+  uint16_t queue[SG_QCAP][32];
+  uint32_t cst[SG_GMAX];                    // first sorted particle of each segment cell
+  uint16_t ct0[SG_GMAX];                    // staged offset of each segment cell
+  // rows
+  int r_lo[SG_ROWS], r_n[SG_ROWS], r_eb[SG_ROWS + 1], r_base[SG_ROWS];
+  int r_ny[SG_ROWS], r_nz[SG_ROWS];         // image shifts of the row (DO n2, n3; DS n1, n2)
+  double r_ox[SG_ROWS];                     // DO: row x offset in cell units (n3 d31 + n2 d21)
+  double r_b[SG_ROWS][3];                   // row part of the bracket (fp64)
+  float r_bf[SG_ROWS][3];
+  int nrows, r0;                            // row count; the center row (dy = dz = 0)
+};
+
+__device__ __forceinline__ int fdiv_fast(int m, int l) {  // floor(m / l), l > 0; |m| small in practice
+  if (m >= 0 && m < l) return 0;
+  if (m < 0 && m >= -l) return -1;
+  if (m >= l && m < 2 * l) return 1;
+  return floordiv(m, l);
+}
+
+// Stencil rows of the segment [A, A+G) in row (a1, a2): union column ranges, brackets.
+// Returns false if the union holds more than SG_CAP elements (caller shrinks G).
+__device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const float4* __restrict__ u32, int A, int G,
+                         int a1, int a2, SgSmem& sm, int lane) {
+  const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
+  // ---- rows
+  bool valid = false;
+  int lo = 0, n = 0, ny = 0, nz = 0, base = 0;
+  double ox = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+  bool center = false;
+  if (g.variant == 0) {
+    if (lane < 9) {
+      const int d1 = lane % 3 - 1, d2 = lane / 3 - 1;
+      int m1 = a1 + d1, m2 = a2 + d2;
+      ny = floordiv(m1, l2);
+      nz = floordiv(m2, l3);
+      m1 -= ny * l2;
+      m2 -= nz * l3;
+      base = l1 * (m1 + l2 * m2);
+      lo = A - 1;
+      n = G + 2;
+      const double v1 = (double)d1 * g.cinv[1], v2 = (double)d2 * g.cinv[2];
+      b0 = g.R[1] * v1 + g.R[2] * v2;
+      b1 = g.R[4] * v1 + g.R[5] * v2;
+      b2 = g.R[8] * v2;
+      valid = true;
+      center = (d1 == 0 && d2 == 0);
+    }
+  } else {
+    if (lane < 12) {
+      const int dz = lane / 4 - 1, ri = lane % 4;
+      const int kk = a2 + dz;
+      const int n3 = floordiv(kk, l3);
+      const int kd = kk - n3 * l3;
+      const double oy = __dmul_rn((double)n3, g.d32);
+      const int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
+      const int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
+      if (ri < m1 - m0) {
+        const int m = m0 + ri;
+        const int n2 = floordiv(m, l2);
+        const int jd = m - n2 * l2;
+        ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
+        // union of [floor(a0 - 1 - ox), ceil(a0 + 2 - ox)) over a0 in [A, A+G) (exact expressions of build_entries)
+        lo = (int)floor(__dsub_rn((double)(A - 1), ox));
+        const int hi = (int)ceil(__dsub_rn((double)(A + G - 1 + 2), ox));
+        n = hi - lo;
+        ny = n2;
+        nz = n3;
+        base = l1 * (jd + l2 * kd);
+        b0 = (double)n2 * g.R[1] + (double)n3 * g.R[2];
+        b1 = (double)(m - a1) * g.w[1] + (double)n2 * g.e[1] + (double)n3 * g.R[5];
+        b2 = (double)dz * g.w[2] + (double)n3 * g.e[2];
+        valid = true;
+        center = (dz == 0 && m == a1);
+      }
+    }
+  }
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  const int ridx = __popc(vm & ((1u << lane) - 1u));
+  int ncols = valid ? n : 0;
+  int x = ncols;
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (valid) {
+    sm.r_lo[ridx] = lo; sm.r_n[ridx] = n; sm.r_eb[ridx] = x - ncols; sm.r_base[ridx] = base;
+    sm.r_ny[ridx] = ny; sm.r_nz[ridx] = nz; sm.r_ox[ridx] = ox;
+    sm.r_b[ridx][0] = b0; sm.r_b[ridx][1] = b1; sm.r_b[ridx][2] = b2;
+    sm.r_bf[ridx][0] = (float)b0; sm.r_bf[ridx][1] = (float)b1; sm.r_bf[ridx][2] = (float)b2;
+    if (center) sm.r0 = ridx;
+  }
+  const int nrows = __popc(vm);
+  const int E = __shfl_sync(0xffffffffu, x, 15);
+  if (lane == 0) { sm.nrows = nrows; sm.r_eb[nrows] = E; }
+  __syncwarp();
+  if (E > SG_MAXE) return false;
+  // ---- entries (row, column): counts and offsets.  All cell-start loads of the union are issued
+  // before the first use (one memory latency instead of one per 32 entries).
+  constexpr int SG_EPL = (SG_MAXE + 31) / 32;
+  uint32_t est[SG_EPL], ecn[SG_EPL];
+#pragma unroll
+  for (int k = 0; k < SG_EPL; ++k) {
+    const int e = k * 32 + lane;
+    est[k] = 0u;
+    ecn[k] = 0u;
+    if (e < E) {
+      int r = 0;
+      while (r + 1 < nrows && sm.r_eb[r + 1] <= e) ++r;
+      const int ci = e - sm.r_eb[r];
+      const int col = sm.r_lo[r] + ci;
+      const int nx = fdiv_fast(col, l1);
+      const uint32_t cell = (uint32_t)sm.r_base[r] + (uint32_t)(col - nx * l1);
+      est[k] = cs[cell];
+      ecn[k] = cs[cell + 1];
+      sm.e_row[e] = (uint8_t)r;
+      sm.e_ci[e] = (uint8_t)ci;
+    }
+  }
+  uint32_t tot = 0;
+#pragma unroll
+  for (int k = 0; k < SG_EPL; ++k) {
+    if (k * 32 >= E) break;
+    const int e = k * 32 + lane;
+    const uint32_t cnt = ecn[k] - est[k];
+    uint32_t y = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += z;
+    }
+    if (e < E) {
+      sm.e_start[e] = est[k];
+      sm.e_off[e] = (uint16_t)min(tot + y - cnt, 65535u);
+    }
+    tot += __shfl_sync(0xffffffffu, y, 31);
+  }
+  if (lane == 0) sm.e_off[E] = (uint16_t)min(tot, 65535u);
+  __syncwarp();
+  if (tot > (uint32_t)SG_CAP) return false;
+  // ---- staged element -> entry, then the coalesced copy with the bracket in the segment frame
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + lane;
+    if (e < E)
+      for (uint32_t k = sm.e_off[e]; k < sm.e_off[e + 1]; ++k) sm.sent[k] = (uint16_t)e;
+  }
+  __syncwarp();
+  const float wx = g.variant == 0 ? (float)(g.R[0] * g.cinv[0]) : (float)g.w[0];
+  const float ex = g.variant == 0 ? 0.0f : (float)g.e[0];
+  for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
+    uint32_t tt[4], jj[4];
+    int ee[4];
+    float4 pp[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      tt[r] = t0 + 32u * r + lane;
+      const bool v = tt[r] < tot;
+      ee[r] = v ? sm.sent[tt[r]] : 0;
+      jj[r] = sm.e_start[ee[r]] + tt[r] - sm.e_off[ee[r]];
+      pp[r] = v ? u32[jj[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      if (tt[r] < tot) {
+        const int row = sm.e_row[ee[r]];
+        const int col = sm.r_lo[row] + sm.e_ci[ee[r]];
+        const int nx = fdiv_fast(col, l1);
+        const float bx = (float)(col - A) * wx + (float)nx * ex + sm.r_bf[row][0];
+        sm.stage[tt[r]] = make_float4(pp[r].x + bx, pp[r].y + sm.r_bf[row][1], pp[r].z + sm.r_bf[row][2],
+                                      __uint_as_float(jj[r]));
+      }
+    }
+  }
+  // ---- per cell and row: the cell's own sub-range of the union row (exact stencil of k_pairs)
+  if (lane < G) {
+    const int a0 = A + lane;
+    for (int r = 0; r < nrows; ++r) {
+      int c0, c1;
+      if (g.variant == 0) {
+        c0 = a0 - 1;
+        c1 = a0 + 2;
+      } else {
+        c0 = (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
+        c1 = (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r]));
+      }
+      const int eb = sm.r_eb[r] - sm.r_lo[r];
+      sm.rg[lane][r][0] = sm.e_off[eb + c0];
+      sm.rg[lane][r][1] = sm.e_off[eb + c1];
+    }
+    const int ec = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + a0;
+    sm.cst[lane] = sm.e_start[ec];
+    sm.ct0[lane] = sm.e_off[ec];
+  }
+  __syncwarp();
+  return true;
+}
+
+// fp64 evaluation of one lane's queued staged indices (four per iteration, global loads first).
+template <bool DIGEST>
+__device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const double4* __restrict__ u,
+                                        const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
+                                        const uint32_t* __restrict__ gid, uint32_t qb, int nq, uint32_t me,
+                                        uint32_t nh_i, int A, double uix, double uiy, double uiz, double wx64,
+                                        double lo64, double hi64, Acc& acc) {
+  const int qmax = __reduce_max_sync(0xffffffffu, nq);
+  const int l1 = g.dims[0];
+  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
+  for (int q0 = 0; q0 < qmax; q0 += 4) {
+    uint32_t jj[4];
+    int ee[4];
+    bool ok0[4];
+    double4 uj[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      ok0[h] = q0 + h < nq;
+      const uint32_t tq = ok0[h] ? lds16(qb + 64u * (uint32_t)(q0 + h)) : 0u;
+      jj[h] = ok0[h] ? __float_as_uint(sm.stage[tq].w) : me;
+      ee[h] = sm.sent[tq];
+      uj[h] = u[jj[h]];
+    }
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t j = jj[h];
+      const int row = sm.e_row[ee[h]];
+      const int col = sm.r_lo[row] + sm.e_ci[ee[h]];
+      const int nx = fdiv_fast(col, l1);
+      const double bx = (double)(col - A) * wx64 + (g.variant == 1 ? (double)nx * g.e[0] : 0.0) + sm.r_b[row][0];
+      const double dx = (uj[h].x + bx) - uix, dy = (uj[h].y + sm.r_b[row][1]) - uiy,
+                   dz = (uj[h].z + sm.r_b[row][2]) - uiz;
+      const double r2 = dx * dx + dy * dy + dz * dz;
+      bool ok = ok0[h] && (j != me) && (r2 < hi64);
+      int n0 = 0, n1 = 0, n2 = 0;
+      if (ok && (DIGEST || r2 >= lo64)) {
+        n0 = nx;
+        n1 = sm.r_ny[row];
+        n2 = sm.r_nz[row];
+        if (g.variant == 1) {
+          const uint32_t nh_j = nh[j];
+          n0 += nh_x(nh_j) - nh_x(nh_i);
+          n1 += nh_y(nh_j) - nh_y(nh_i);
+        }
+        if (r2 >= lo64) {
+          const float4 qi = qs[me], qj = qs[j];
+          ok = canonical_r2(g, (double)qj.x, (double)qj.y, (double)qj.z, (double)qi.x, (double)qi.y, (double)qi.z, n0,
+                            n1, n2) < g.rc2;
+          acc.nrc++;
+        }
+      }
+      const double ir = rcp64(r2);
+      const double s2 = sig2 * ir;
+      const double s6 = s2 * s2 * s2;
+      double fr = (eps24 * s6) * (2.0 * s6 - 1.0) * ir;
+      fr = ok ? fr : 0.0;
+      const double tx = fr * dx, ty = fr * dy, tz = fr * dz;
+      acc.fx -= tx; acc.fy -= ty; acc.fz -= tz;
+      acc.u += ok ? s6 * s6 - s6 : 0.0;
+      acc.w0 += tx * dx; acc.w1 += ty * dy; acc.w2 += tz * dz;
+      acc.w3 += tx * dy; acc.w4 += tx * dz; acc.w5 += ty * dz;
+      acc.cnt += ok ? 1u : 0u;
+      if (DIGEST && ok) {
+        const uint64_t key = (uint64_t)gid[j] | ((uint64_t)(n0 + 8) << 32) | ((uint64_t)(n1 + 8) << 36) |
+                             ((uint64_t)(n2 + 8) << 40);
+        const uint64_t hh = mix64(key);
+        acc.hs += hh;
+        acc.hx ^= hh;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <bool DIGEST>
+__global__ void __launch_bounds__(32, 16)
+k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
+            const float4* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
+            float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
+            uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int G, int nseg,
+            int bpl, int layer0) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SgSmem& sm = *reinterpret_cast<SgSmem*>(smraw);
+  const int lane = threadIdx.x & 31;
+  const int l1 = g.dims[0];
+  const int layer = layer0 + (int)(blockIdx.x / bpl);
+  const int rem = (int)blockIdx.x - (layer - layer0) * bpl;
+  const int a1 = rem / nseg, a2 = layer;
+  const int Abeg = (rem - a1 * nseg) * G;
+  const int Aend = min(l1, Abeg + G);
+  const double lo64 = g.rc2 * (1.0 - K3_BAND64), hi64 = g.rc2 * (1.0 + K3_BAND64);
+  const float hi32 = (float)g.band_hi;
+  const double wx64 = g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0];
+  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
+  const uint32_t qb = smem_u32(&sm.queue[0][lane]);
+  const uint32_t stage0 = smem_u32(&sm.stage[0]);
+
+  double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+
+  int A = Abeg;
+  while (A < Aend) {
+    int Gs = Aend - A;
+    while (!sg_setup(g, cs, u32, A, Gs, a1, a2, sm, lane)) {
+      if (Gs == 1) { Gs = 0; break; }  // a single cell's neighborhood above SG_CAP: flagged below
+      Gs = (Gs + 1) / 2;
+    }
+    if (Gs == 0) {  // cannot stage (cells of > ~20 particles): report as non-finite so the host fails loudly
+      tNF += 1.0;
+      A += 1;
+      continue;
+    }
+    const int nrows = sm.nrows;
+    // neighborhood size of every cell (instrumentation: k_pairs' tS)
+    if (lane < Gs) {
+      int ns = 0;
+      for (int r = 0; r < nrows; ++r) {
+        // cells of the sub-range = columns; recover from the entry offsets is not possible for empty cells,
+        // so count columns directly
+        if (g.variant == 0) ns += 3;
+        else {
+          const int a0 = A + lane;
+          ns += (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r])) - (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
+        }
+      }
+      tS += (double)ns;
+    }
+    // particles of the segment: contiguous in the center row
+    const int ecA = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + A;
+    const uint32_t P0 = sm.e_start[ecA];
+    const uint32_t P1 = sm.e_start[ecA + Gs - 1] + (uint32_t)(sm.e_off[ecA + Gs] - sm.e_off[ecA + Gs - 1]);
+    for (uint32_t pb = P0; pb < P1; pb += 32) {
+      const uint32_t p = pb + (uint32_t)lane;
+      const bool act = p < P1;
+      // cell of p inside the segment
+      int gc = 0;
+      if (act) {
+        int lo_ = 0, hi_ = Gs - 1;
+        while (lo_ < hi_) {
+          const int mid = (lo_ + hi_ + 1) >> 1;
+          if (sm.cst[mid] <= p) lo_ = mid; else hi_ = mid - 1;
+        }
+        // skip empty cells that share the start
+        gc = lo_;
+      }
+      const uint32_t ti = sm.ct0[gc] + (p - sm.cst[gc]);
+      const float4 vi = sm.stage[act ? ti : 0];
+      // i in the segment frame, fp64
+      const uint32_t me = act ? p : 0u;
+      const double4 ui = u[me];
+      const double uix = ui.x + (double)(A + gc - A) * wx64, uiy = ui.y, uiz = ui.z;
+      const uint32_t nh_i = (g.variant == 1 && act) ? nh[me] : 0u;
+      // candidates of i: its cell's stencil minus itself
+      int T = 0;
+      if (act)
+        for (int r = 0; r < nrows; ++r) T += sm.rg[gc][r][1] - sm.rg[gc][r][0];
+      if (act) tC += (double)(T - 1);
+      Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+      // filter: rows in order; every lane scans its own cell's contiguous sub-range of the row
+      // (uniform trip count = the warp's longest sub-range, predicated per lane)
+      int nq = 0;
+      for (int r = 0; r < nrows; ++r) {
+        const uint32_t st = act ? sm.rg[gc][r][0] : 0u, en = act ? sm.rg[gc][r][1] : 0u;
+        const int len = (int)(en - st);
+        const int lmax = __reduce_max_sync(0xffffffffu, len);
+        for (int k0 = 0; k0 < lmax; k0 += 8) {
+          if (__any_sync(0xffffffffu, nq > SG_QCAP - 8)) {  // room for 8 more hits in every queue
+            sg_eval<DIGEST>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+            nq = 0;
+          }
+          const int kend = min(lmax, k0 + 8);
+          for (int k = k0; k < kend; ++k) {
+            const uint32_t t = st + (uint32_t)k;
+            const float4 v = lds128(stage0 + 16u * min(t, (uint32_t)(SG_CAP - 1)));
+            const float dx = v.x - vi.x, dy = v.y - vi.y, dz = v.z - vi.z;
+            const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+            const bool hit = (k < len) && (r2 < hi32) && (t != ti);
+            sts16(qb + 64u * (uint32_t)nq, t);  // nq <= SG_QCAP - 1 here
+            nq += hit ? 1 : 0;
+          }
+        }
+      }
+      sg_eval<DIGEST>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+      const double fx = acc.fx, fy = acc.fy, fz = acc.fz, uu = acc.u;
+      const double w0 = acc.w0, w1 = acc.w1, w2 = acc.w2, w3 = acc.w3, w4 = acc.w4, w5 = acc.w5;
+      const uint32_t cnt = acc.cnt, nrc = acc.nrc;
+      const uint64_t hs = acc.hs, hx = acc.hx;
+      if (act) {
+        const double Ui = 2.0 * g.eps * uu - 0.5 * g.ushift * (double)cnt;
+        Fout[me] = make_float4((float)(g.Q[0] * fx + g.Q[1] * fy + g.Q[2] * fz),
+                               (float)(g.Q[3] * fx + g.Q[4] * fy + g.Q[5] * fz),
+                               (float)(g.Q[6] * fx + g.Q[7] * fy + g.Q[8] * fz), 0.0f);
+        if (DIGEST) { dcnt[me] = cnt; dhs[me] = hs; dhx[me] = hx; }
+        tU += Ui;
+        tW[0] += 0.5 * w0; tW[1] += 0.5 * w1; tW[2] += 0.5 * w2;
+        tW[3] += 0.5 * w3; tW[4] += 0.5 * w4; tW[5] += 0.5 * w5;
+        tI += (double)cnt;
+        tR += (double)nrc;
+        tNF += isfinite(fx + fy + fz + Ui) ? 0.0 : 1.0;
+      }
+    }
+    A += Gs;
+    __syncwarp();
+  }
+  tU = warp_sum_d(tU);
+  tW[0] = warp_sum_d(tW[0]); tW[1] = warp_sum_d(tW[1]); tW[2] = warp_sum_d(tW[2]);
+  tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
+  tI = warp_sum_d(tI);
+  tC = warp_sum_d(tC);
+  tS = warp_sum_d(tS);
+  tR = warp_sum_d(tR);
+  tNF = warp_sum_d(tNF);
+  if (lane < NPART) {
+    double v = 0;
+    if (lane == 0) v = tU;
+    else if (lane <= 6) v = tW[lane - 1];
+    else if (lane == 7) v = tI;
+    else if (lane == 8) v = tC;
+    else if (lane == 9) v = tS;
+    else if (lane == 10) v = tR;
+    else v = tNF;
+    bpart[(int64_t)blockIdx.x * NPART + lane] = v;
+  }
+}
+
+}  // namespace nc

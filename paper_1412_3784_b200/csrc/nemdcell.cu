@@ -144,6 +144,24 @@ int cells_per_block() { return K3_CELLS; }
 
 // fp32 pair kernel generation: 1 = k_pairs (v11, default); 2 = k_pairs_v3 (two particles per lane,
 // packed FFMA2 filter; parity-green but slower on C4: 51-57 ms vs 41.6 ms) -- NC_K3=2 for A/B runs.
+// Cells per warp of the sparse-cell kernel, 0 = use the warp-per-cell kernel.  Mean occupancy
+// below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~24 particles;
+// NC_SEG=0 / NC_SEG=1 force the choice (A/B runs).
+int seg_cells(const nc_ctx* ctx, const Geom& g) {
+  static int mode = [] {
+    const char* e = getenv("NC_SEG");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+  }();
+  if (mode == 0) return 0;
+  const double occ = (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
+  if (mode < 0 && occ >= 4.0) return 0;
+  int G = (int)std::floor(24.0 / std::max(occ, 0.5));
+  G = std::max(4, std::min(G, std::min(SG_GMAX, g.dims[0])));
+  int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
+  if (blocks > ctx->max_blocks) return 0;
+  return G;
+}
+
 int k3_version() {
   static int v = [] {
     const char* e = getenv("NC_K3");
@@ -242,6 +260,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
   int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
+  (void)nblocks;
   static bool attr_set[2][2] = {{false, false}, {false, false}};
   bool& as = attr_set[sizeof(T) == 8][DIGEST];
   if (!as) {
@@ -250,7 +269,22 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   }
   prof_begin(ctx);
   if constexpr (sizeof(T) == 4) {
-    if (k3_version() == 2) {
+    const int Gseg = seg_cells(ctx, g);
+    if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
+      const int nseg = (g.dims[0] + Gseg - 1) / Gseg;
+      const int bpl_s = nseg * g.dims[1];
+      const size_t smem_s = sizeof(SgSmem);
+      static bool attr_s[2] = {false, false};
+      if (!attr_s[DIGEST]) {
+        CK(cudaFuncSetAttribute(k_pairs_seg<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+        attr_s[DIGEST] = true;
+      }
+      bpl = bpl_s;
+      nblocks = bpl * nlay;
+      k_pairs_seg<DIGEST><<<nblocks, 32, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
+                                                      (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
+                                                      nseg, bpl, layer0);
+    } else if (k3_version() == 2) {
       size_t smem2 = sizeof(V3Smem);
       static bool attr2[2] = {false, false};
       if (!attr2[DIGEST]) {

@@ -26,7 +26,7 @@ def main():
     dt = np.float32 if a.prec == "f32" else np.float64
     q = W.positions(w, dtype=dt, k=a.config)
     p = W.momenta(w, dtype=dt, k=a.config)
-    cl = CellList(a.variant, a.prec, rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=int(2.5 * w.n / 13) + 65536)
+    cl = CellList(a.variant, a.prec, rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=0)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
