@@ -21,9 +21,11 @@
 
 namespace nc {
 
-constexpr int SG_CAP = 640;                 // staged union elements
+constexpr int SG_NW = 2;                    // warps per block (share one staged union)
+constexpr int SG_NT = 32 * SG_NW;
+constexpr int SG_CAP = 768;                 // staged union elements
 constexpr int SG_ROWS = 12;                 // stencil rows (DS 9, DO <= 12)
-constexpr int SG_GMAX = 32;                 // cells per segment
+constexpr int SG_GMAX = 48;                 // cells per segment
 constexpr int SG_MAXE = SG_ROWS * (SG_GMAX + 4);  // union entries (row x column)
 constexpr int SG_QCAP = 32;                 // per-lane hit queue
 
@@ -35,7 +37,9 @@ struct SgSmem {
   uint8_t e_row[SG_MAXE];
   uint8_t e_ci[SG_MAXE];                    // column index inside the row's union range
   uint16_t rg[SG_GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
-  uint16_t queue[SG_QCAP][32];
+  uint16_t queue[SG_NW][SG_QCAP][32];
+  uint32_t ssum[SG_NW];                     // block scan scratch
+  double part[SG_NW][NPART];                // per-warp partials (fixed-order combine)
   uint32_t cst[SG_GMAX];                    // first sorted particle of each segment cell
   uint16_t ct0[SG_GMAX];                    // staged offset of each segment cell
   // rows
@@ -54,91 +58,96 @@ __device__ __forceinline__ int fdiv_fast(int m, int l) {  // floor(m / l), l > 0
   return floordiv(m, l);
 }
 
-// Stencil rows of the segment [A, A+G) in row (a1, a2): union column ranges, brackets.
-// Returns false if the union holds more than SG_CAP elements (caller shrinks G).
+// Stencil rows of the segment [A, A+G) in row (a1, a2): union column ranges, brackets,
+// staged union, per-cell sub-ranges.  All SG_NT threads of the block call it.  Returns
+// false (uniformly) if the union holds more than SG_CAP elements (caller shrinks G).
 __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const float4* __restrict__ u32, int A, int G,
-                         int a1, int a2, SgSmem& sm, int lane) {
+                         int a1, int a2, SgSmem& sm, int tid) {
   const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
-  // ---- rows
-  bool valid = false;
-  int lo = 0, n = 0, ny = 0, nz = 0, base = 0;
-  double ox = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
-  bool center = false;
-  if (g.variant == 0) {
-    if (lane < 9) {
-      const int d1 = lane % 3 - 1, d2 = lane / 3 - 1;
-      int m1 = a1 + d1, m2 = a2 + d2;
-      ny = floordiv(m1, l2);
-      nz = floordiv(m2, l3);
-      m1 -= ny * l2;
-      m2 -= nz * l3;
-      base = l1 * (m1 + l2 * m2);
-      lo = A - 1;
-      n = G + 2;
-      const double v1 = (double)d1 * g.cinv[1], v2 = (double)d2 * g.cinv[2];
-      b0 = g.R[1] * v1 + g.R[2] * v2;
-      b1 = g.R[4] * v1 + g.R[5] * v2;
-      b2 = g.R[8] * v2;
-      valid = true;
-      center = (d1 == 0 && d2 == 0);
-    }
-  } else {
-    if (lane < 12) {
-      const int dz = lane / 4 - 1, ri = lane % 4;
-      const int kk = a2 + dz;
-      const int n3 = floordiv(kk, l3);
-      const int kd = kk - n3 * l3;
-      const double oy = __dmul_rn((double)n3, g.d32);
-      const int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
-      const int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
-      if (ri < m1 - m0) {
-        const int m = m0 + ri;
-        const int n2 = floordiv(m, l2);
-        const int jd = m - n2 * l2;
-        ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
-        // union of [floor(a0 - 1 - ox), ceil(a0 + 2 - ox)) over a0 in [A, A+G) (exact expressions of build_entries)
-        lo = (int)floor(__dsub_rn((double)(A - 1), ox));
-        const int hi = (int)ceil(__dsub_rn((double)(A + G - 1 + 2), ox));
-        n = hi - lo;
-        ny = n2;
-        nz = n3;
-        base = l1 * (jd + l2 * kd);
-        b0 = (double)n2 * g.R[1] + (double)n3 * g.R[2];
-        b1 = (double)(m - a1) * g.w[1] + (double)n2 * g.e[1] + (double)n3 * g.R[5];
-        b2 = (double)dz * g.w[2] + (double)n3 * g.e[2];
+  const int lane = tid & 31, wid = tid >> 5;
+  // ---- rows (warp 0)
+  if (wid == 0) {
+    bool valid = false;
+    int lo = 0, n = 0, ny = 0, nz = 0, base = 0;
+    double ox = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    bool center = false;
+    if (g.variant == 0) {
+      if (lane < 9) {
+        const int d1 = lane % 3 - 1, d2 = lane / 3 - 1;
+        int m1 = a1 + d1, m2 = a2 + d2;
+        ny = floordiv(m1, l2);
+        nz = floordiv(m2, l3);
+        m1 -= ny * l2;
+        m2 -= nz * l3;
+        base = l1 * (m1 + l2 * m2);
+        lo = A - 1;
+        n = G + 2;
+        const double v1 = (double)d1 * g.cinv[1], v2 = (double)d2 * g.cinv[2];
+        b0 = g.R[1] * v1 + g.R[2] * v2;
+        b1 = g.R[4] * v1 + g.R[5] * v2;
+        b2 = g.R[8] * v2;
         valid = true;
-        center = (dz == 0 && m == a1);
+        center = (d1 == 0 && d2 == 0);
+      }
+    } else {
+      if (lane < 12) {
+        const int dz = lane / 4 - 1, ri = lane % 4;
+        const int kk = a2 + dz;
+        const int n3 = floordiv(kk, l3);
+        const int kd = kk - n3 * l3;
+        const double oy = __dmul_rn((double)n3, g.d32);
+        const int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
+        const int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
+        if (ri < m1 - m0) {
+          const int m = m0 + ri;
+          const int n2 = floordiv(m, l2);
+          const int jd = m - n2 * l2;
+          ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
+          // union of [floor(a0 - 1 - ox), ceil(a0 + 2 - ox)) over a0 in [A, A+G) (build_entries' expressions)
+          lo = (int)floor(__dsub_rn((double)(A - 1), ox));
+          const int hi = (int)ceil(__dsub_rn((double)(A + G - 1 + 2), ox));
+          n = hi - lo;
+          ny = n2;
+          nz = n3;
+          base = l1 * (jd + l2 * kd);
+          b0 = (double)n2 * g.R[1] + (double)n3 * g.R[2];
+          b1 = (double)(m - a1) * g.w[1] + (double)n2 * g.e[1] + (double)n3 * g.R[5];
+          b2 = (double)dz * g.w[2] + (double)n3 * g.e[2];
+          valid = true;
+          center = (dz == 0 && m == a1);
+        }
       }
     }
-  }
-  const unsigned vm = __ballot_sync(0xffffffffu, valid);
-  const int ridx = __popc(vm & ((1u << lane) - 1u));
-  int ncols = valid ? n : 0;
-  int x = ncols;
+    const unsigned vm = __ballot_sync(0xffffffffu, valid);
+    const int ridx = __popc(vm & ((1u << lane) - 1u));
+    const int ncols = valid ? n : 0;
+    int x = ncols;
 #pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+    for (int o = 1; o < 16; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (valid) {
+      sm.r_lo[ridx] = lo; sm.r_n[ridx] = n; sm.r_eb[ridx] = x - ncols; sm.r_base[ridx] = base;
+      sm.r_ny[ridx] = ny; sm.r_nz[ridx] = nz; sm.r_ox[ridx] = ox;
+      sm.r_b[ridx][0] = b0; sm.r_b[ridx][1] = b1; sm.r_b[ridx][2] = b2;
+      sm.r_bf[ridx][0] = (float)b0; sm.r_bf[ridx][1] = (float)b1; sm.r_bf[ridx][2] = (float)b2;
+      if (center) sm.r0 = ridx;
+    }
+    const int nrows_w = __popc(vm);
+    const int E_w = __shfl_sync(0xffffffffu, x, 15);
+    if (lane == 0) { sm.nrows = nrows_w; sm.r_eb[nrows_w] = E_w; }
   }
-  if (valid) {
-    sm.r_lo[ridx] = lo; sm.r_n[ridx] = n; sm.r_eb[ridx] = x - ncols; sm.r_base[ridx] = base;
-    sm.r_ny[ridx] = ny; sm.r_nz[ridx] = nz; sm.r_ox[ridx] = ox;
-    sm.r_b[ridx][0] = b0; sm.r_b[ridx][1] = b1; sm.r_b[ridx][2] = b2;
-    sm.r_bf[ridx][0] = (float)b0; sm.r_bf[ridx][1] = (float)b1; sm.r_bf[ridx][2] = (float)b2;
-    if (center) sm.r0 = ridx;
-  }
-  const int nrows = __popc(vm);
-  const int E = __shfl_sync(0xffffffffu, x, 15);
-  if (lane == 0) { sm.nrows = nrows; sm.r_eb[nrows] = E; }
-  __syncwarp();
+  __syncthreads();
+  const int nrows = sm.nrows;
+  const int E = sm.r_eb[nrows];
   if (E > SG_MAXE) return false;
-  // ---- entries (row, column): counts and offsets.  All cell-start loads of the union are issued
-  // before the first use (one memory latency instead of one per 32 entries).
-  constexpr int SG_EPL = (SG_MAXE + 31) / 32;
-  uint32_t est[SG_EPL], ecn[SG_EPL];
+  // ---- entries (row, column): all cell-start loads issued first, then a block scan of the counts
+  constexpr int SG_EPT = (SG_MAXE + SG_NT - 1) / SG_NT;
+  uint32_t est[SG_EPT], ecn[SG_EPT];
 #pragma unroll
-  for (int k = 0; k < SG_EPL; ++k) {
-    const int e = k * 32 + lane;
+  for (int k = 0; k < SG_EPT; ++k) {
+    const int e = k * SG_NT + tid;
     est[k] = 0u;
     ecn[k] = 0u;
     if (e < E) {
@@ -156,9 +165,9 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
   }
   uint32_t tot = 0;
 #pragma unroll
-  for (int k = 0; k < SG_EPL; ++k) {
-    if (k * 32 >= E) break;
-    const int e = k * 32 + lane;
+  for (int k = 0; k < SG_EPT; ++k) {
+    if (k * SG_NT >= E) break;
+    const int e = k * SG_NT + tid;
     const uint32_t cnt = ecn[k] - est[k];
     uint32_t y = cnt;
 #pragma unroll
@@ -166,31 +175,38 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
       const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
       if (lane >= o) y += z;
     }
+    if (lane == 31) sm.ssum[wid] = y;
+    __syncthreads();
+    uint32_t before = tot, all = 0;
+#pragma unroll
+    for (int w = 0; w < SG_NW; ++w) {
+      const uint32_t v = sm.ssum[w];
+      if (w < wid) before += v;
+      all += v;
+    }
     if (e < E) {
       sm.e_start[e] = est[k];
-      sm.e_off[e] = (uint16_t)min(tot + y - cnt, 65535u);
+      sm.e_off[e] = (uint16_t)min(before + y - cnt, 65535u);
     }
-    tot += __shfl_sync(0xffffffffu, y, 31);
+    tot += all;
+    __syncthreads();
   }
-  if (lane == 0) sm.e_off[E] = (uint16_t)min(tot, 65535u);
-  __syncwarp();
+  if (tid == 0) sm.e_off[E] = (uint16_t)min(tot, 65535u);
+  __syncthreads();
   if (tot > (uint32_t)SG_CAP) return false;
   // ---- staged element -> entry, then the coalesced copy with the bracket in the segment frame
-  for (int e0 = 0; e0 < E; e0 += 32) {
-    const int e = e0 + lane;
-    if (e < E)
-      for (uint32_t k = sm.e_off[e]; k < sm.e_off[e + 1]; ++k) sm.sent[k] = (uint16_t)e;
-  }
-  __syncwarp();
+  for (int e = tid; e < E; e += SG_NT)
+    for (uint32_t k = sm.e_off[e]; k < sm.e_off[e + 1]; ++k) sm.sent[k] = (uint16_t)e;
+  __syncthreads();
   const float wx = g.variant == 0 ? (float)(g.R[0] * g.cinv[0]) : (float)g.w[0];
   const float ex = g.variant == 0 ? 0.0f : (float)g.e[0];
-  for (uint32_t t0 = 0; t0 < tot; t0 += 128) {
+  for (uint32_t t0 = 0; t0 < tot; t0 += 4 * SG_NT) {
     uint32_t tt[4], jj[4];
     int ee[4];
     float4 pp[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      tt[r] = t0 + 32u * r + lane;
+      tt[r] = t0 + (uint32_t)(SG_NT * r + tid);
       const bool v = tt[r] < tot;
       ee[r] = v ? sm.sent[tt[r]] : 0;
       jj[r] = sm.e_start[ee[r]] + tt[r] - sm.e_off[ee[r]];
@@ -209,8 +225,8 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
     }
   }
   // ---- per cell and row: the cell's own sub-range of the union row (exact stencil of k_pairs)
-  if (lane < G) {
-    const int a0 = A + lane;
+  if (tid < G) {
+    const int a0 = A + tid;
     for (int r = 0; r < nrows; ++r) {
       int c0, c1;
       if (g.variant == 0) {
@@ -221,14 +237,14 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
         c1 = (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r]));
       }
       const int eb = sm.r_eb[r] - sm.r_lo[r];
-      sm.rg[lane][r][0] = sm.e_off[eb + c0];
-      sm.rg[lane][r][1] = sm.e_off[eb + c1];
+      sm.rg[tid][r][0] = sm.e_off[eb + c0];
+      sm.rg[tid][r][1] = sm.e_off[eb + c1];
     }
     const int ec = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + a0;
-    sm.cst[lane] = sm.e_start[ec];
-    sm.ct0[lane] = sm.e_off[ec];
+    sm.cst[tid] = sm.e_start[ec];
+    sm.ct0[tid] = sm.e_off[ec];
   }
-  __syncwarp();
+  __syncthreads();
   return true;
 }
 
@@ -307,7 +323,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
 }
 
 template <bool DIGEST>
-__global__ void __launch_bounds__(32, 16)
+__global__ void __launch_bounds__(SG_NT, 8)
 k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
             const float4* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
             float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
@@ -315,7 +331,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
             int bpl, int layer0) {
   extern __shared__ __align__(16) unsigned char smraw[];
   SgSmem& sm = *reinterpret_cast<SgSmem*>(smraw);
-  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int l1 = g.dims[0];
   const int layer = layer0 + (int)(blockIdx.x / bpl);
   const int rem = (int)blockIdx.x - (layer - layer0) * bpl;
@@ -326,7 +342,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
   const float hi32 = (float)g.band_hi;
   const double wx64 = g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0];
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
-  const uint32_t qb = smem_u32(&sm.queue[0][lane]);
+  const uint32_t qb = smem_u32(&sm.queue[wid][0][lane]);
   const uint32_t stage0 = smem_u32(&sm.stage[0]);
 
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
@@ -334,7 +350,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
   int A = Abeg;
   while (A < Aend) {
     int Gs = Aend - A;
-    while (!sg_setup(g, cs, u32, A, Gs, a1, a2, sm, lane)) {
+    while (!sg_setup(g, cs, u32, A, Gs, a1, a2, sm, tid)) {
       if (Gs == 1) { Gs = 0; break; }  // a single cell's neighborhood above SG_CAP: flagged below
       Gs = (Gs + 1) / 2;
     }
@@ -345,14 +361,14 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     }
     const int nrows = sm.nrows;
     // neighborhood size of every cell (instrumentation: k_pairs' tS)
-    if (lane < Gs) {
+    if (tid < Gs) {
       int ns = 0;
       for (int r = 0; r < nrows; ++r) {
         // cells of the sub-range = columns; recover from the entry offsets is not possible for empty cells,
         // so count columns directly
         if (g.variant == 0) ns += 3;
         else {
-          const int a0 = A + lane;
+          const int a0 = A + tid;
           ns += (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r])) - (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
         }
       }
@@ -362,7 +378,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     const int ecA = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + A;
     const uint32_t P0 = sm.e_start[ecA];
     const uint32_t P1 = sm.e_start[ecA + Gs - 1] + (uint32_t)(sm.e_off[ecA + Gs] - sm.e_off[ecA + Gs - 1]);
-    for (uint32_t pb = P0; pb < P1; pb += 32) {
+    for (uint32_t pb = P0 + 32u * (uint32_t)wid; pb < P1; pb += (uint32_t)SG_NT) {
       const uint32_t p = pb + (uint32_t)lane;
       const bool act = p < P1;
       // cell of p inside the segment
@@ -433,7 +449,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
       }
     }
     A += Gs;
-    __syncwarp();
+    __syncthreads();  // the next sub-segment overwrites the staged union
   }
   tU = warp_sum_d(tU);
   tW[0] = warp_sum_d(tW[0]); tW[1] = warp_sum_d(tW[1]); tW[2] = warp_sum_d(tW[2]);
@@ -452,7 +468,13 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     else if (lane == 9) v = tS;
     else if (lane == 10) v = tR;
     else v = tNF;
-    bpart[(int64_t)blockIdx.x * NPART + lane] = v;
+    sm.part[wid][lane] = v;
+  }
+  __syncthreads();
+  if (tid < NPART) {  // fixed-order combine of the warps
+    double v = 0.0;
+    for (int w = 0; w < SG_NW; ++w) v += sm.part[w][tid];
+    bpart[(int64_t)blockIdx.x * NPART + tid] = v;
   }
 }
 

@@ -155,7 +155,7 @@ int seg_cells(const nc_ctx* ctx, const Geom& g) {
   if (mode == 0) return 0;
   const double occ = (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (mode < 0 && occ >= 4.0) return 0;
-  int G = (int)std::floor(24.0 / std::max(occ, 0.5));
+  int G = (int)std::floor(24.0 * SG_NW / std::max(occ, 0.5));
   G = std::max(4, std::min(G, std::min(SG_GMAX, g.dims[0])));
   int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
   if (blocks > ctx->max_blocks) return 0;
@@ -281,7 +281,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       }
       bpl = bpl_s;
       nblocks = bpl * nlay;
-      k_pairs_seg<DIGEST><<<nblocks, 32, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
+      k_pairs_seg<DIGEST><<<nblocks, SG_NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
                                                       (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
                                                       nseg, bpl, layer0);
     } else if (k3_version() == 2) {
