@@ -323,7 +323,13 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 32;  // permanent far element (padding slot of the evaluation)
 constexpr int K3_STAGE = K3_CAP + 33;  // + up to S far sentinels so the filter needs no bounds checks
-constexpr int K3_QCAP = 64;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
+#ifndef K3_QCAP_OVR
+#define K3_QCAP_OVR 48
+#endif
+#ifndef K3_MINB
+#define K3_MINB 14
+#endif
+constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
 constexpr int K3_UNROLL = 8;    // filter candidates per lane between queue-full votes
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
 constexpr int K3_CELLS = 4;     // cells per warp (= per block: one warp per block)
@@ -853,7 +859,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 // cell layer, so block partials are layer-aligned and their fixed-order sums
 // are independent of timing (determinism).  grid = l3 * blocks_per_layer.
 template <typename T, bool DIGEST>
-__global__ void __launch_bounds__(32, 14)
+__global__ void __launch_bounds__(32, K3_MINB)
 k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
         const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
