@@ -252,6 +252,20 @@ nc_status nc_slab_kick(nc_ctx *ctx, void *p, const void *F, int64_t n, double dt
  * rechecks): bitwise the same as a single-device evaluation. */
 nc_status nc_slab_reduce(nc_ctx *ctx, const double *parts, int nlayers, double *U, double W[6], double stats[4]);
 
+/* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
+ * kernel).  Both evaluate the same neighborhoods, the same
+ * candidates and the same pair set; they differ in how work maps to warps:
+ *  NC_PK_AUTO    (default) segment kernel when the mean occupancy is below 4
+ *                particles per cell (WCA at rho = 0.8442: ~1.3), else per cell;
+ *  NC_PK_CELL    one warp per center cell (k_pairs);
+ *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
+ *                union of their neighborhoods (k_pairs_seg), fp64 pair forces.
+ * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT on an NC_F64 context).
+ * nc_pair_kernel_used returns the kernel of the last evaluation (1 or 2, 0 = none). */
+typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2 } nc_pair_kernel;
+nc_status nc_set_pair_kernel(nc_ctx *ctx, int which);
+int nc_pair_kernel_used(const nc_ctx *ctx);
+
 /* Number of kernel launches this context has issued so far. */
 int64_t nc_launch_count(const nc_ctx *ctx);
 

@@ -341,7 +341,6 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
   const double lo64 = g.rc2 * (1.0 - K3_BAND64), hi64 = g.rc2 * (1.0 + K3_BAND64);
   const float hi32 = (float)g.band_hi;
   const double wx64 = g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0];
-  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   const uint32_t qb = smem_u32(&sm.queue[wid][0][lane]);
   const uint32_t stage0 = smem_u32(&sm.stage[0]);
 

@@ -66,6 +66,8 @@ struct nc_ctx {
   bool last_resident = false;     // last build used the resident state
   const uint32_t* last_in_gid = nullptr;  // gid of input order (nullptr = identity)
   int last_cpb = 0, last_bpl = 0;
+  int pair_kernel = NC_PK_AUTO;   // nc_set_pair_kernel
+  int pair_kernel_used = 0;
   double host_tot[NPART];
   bool tot_valid = false;
 
@@ -148,10 +150,11 @@ int cells_per_block() { return K3_CELLS; }
 // below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~24 particles;
 // NC_SEG=0 / NC_SEG=1 force the choice (A/B runs).
 int seg_cells(const nc_ctx* ctx, const Geom& g) {
-  static int mode = [] {
+  static int env_mode = [] {
     const char* e = getenv("NC_SEG");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
   }();
+  int mode = ctx->pair_kernel == NC_PK_CELL ? 0 : (ctx->pair_kernel == NC_PK_SEGMENT ? 1 : env_mode);
   if (mode == 0) return 0;
   const double occ = (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (mode < 0 && occ >= 4.0) return 0;
@@ -281,10 +284,12 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       }
       bpl = bpl_s;
       nblocks = bpl * nlay;
+      ctx->pair_kernel_used = NC_PK_SEGMENT;
       k_pairs_seg<DIGEST><<<nblocks, SG_NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
                                                       (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
                                                       nseg, bpl, layer0);
     } else if (k3_version() == 2) {
+      ctx->pair_kernel_used = NC_PK_CELL;
       size_t smem2 = sizeof(V3Smem);
       static bool attr2[2] = {false, false};
       if (!attr2[DIGEST]) {
@@ -295,10 +300,12 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                                                     (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl,
                                                     layer0);
     } else {
+      ctx->pair_kernel_used = NC_PK_CELL;
       k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
                                                    ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
     }
   } else {
+    ctx->pair_kernel_used = NC_PK_CELL;
     k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart, ctx->dcnt,
                                                  ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
   }
@@ -669,6 +676,18 @@ const char* nc_version(void) { return "nemdcell 0.1 (sm_100a)"; }
 const char* nc_last_error(const nc_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 int64_t nc_launch_count(const nc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+nc_status nc_set_pair_kernel(nc_ctx* ctx, int which) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (which != NC_PK_AUTO && which != NC_PK_CELL && which != NC_PK_SEGMENT)
+    return fail(ctx, NC_E_ARG, "pair kernel must be NC_PK_AUTO, NC_PK_CELL or NC_PK_SEGMENT");
+  if (which == NC_PK_SEGMENT && ctx->cfg.prec != NC_F32)
+    return fail(ctx, NC_E_ARG, "the segment pair kernel is NC_F32 only");
+  ctx->pair_kernel = which;
+  return NC_OK;
+}
+
+int nc_pair_kernel_used(const nc_ctx* ctx) { return ctx ? ctx->pair_kernel_used : 0; }
 
 nc_status nc_profile(nc_ctx* ctx, int enable) {
   if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");

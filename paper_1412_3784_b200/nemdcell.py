@@ -26,7 +26,10 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_set_state", "nc_step_sllod", "nc_get_state", "nc_get_cells", "nc_get_pair_digest", "nc_get_stats",
            "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
            "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_migrate", "nc_slab_unpack",
-           "nc_slab_halo", "nc_slab_forces", "nc_slab_kick", "nc_slab_reduce"]
+           "nc_slab_halo", "nc_slab_forces", "nc_slab_kick", "nc_slab_reduce", "nc_set_pair_kernel",
+           "nc_pair_kernel_used"]
+NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
+PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
 KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
 
 
@@ -100,11 +103,14 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_slab_reduce.argtypes = [vp, vp, i32, vp, vp, vp]
         L.nc_launch_count.argtypes = [vp]
         L.nc_launch_count.restype = i64
+        L.nc_set_pair_kernel.argtypes = [vp, i32]
+        L.nc_pair_kernel_used.argtypes = [vp]
+        L.nc_pair_kernel_used.restype = i32
         L.nc_last_error.argtypes = [vp]
         L.nc_last_error.restype = ctypes.c_char_p
         L.nc_version.restype = ctypes.c_char_p
         for name in EXPORTS:
-            if name not in ("nc_destroy", "nc_launch_count", "nc_last_error", "nc_version"):
+            if name not in ("nc_destroy", "nc_launch_count", "nc_last_error", "nc_version", "nc_pair_kernel_used"):
                 getattr(L, name).restype = i32
         _lib = L
         return L
@@ -225,6 +231,15 @@ def nc_get_stencil_histogram(ctx) -> np.ndarray:
     h = np.zeros(64, dtype=np.int64)
     _check(ctx, load().nc_get_stencil_histogram(ctx, _ptr(h)))
     return h
+
+
+def nc_set_pair_kernel(ctx, which) -> None:
+    """Pair kernel of the context: "auto" | "cell" | "segment" (or NC_PK_*)."""
+    _check(ctx, load().nc_set_pair_kernel(ctx, PAIR_KERNELS.get(which, which) if isinstance(which, str) else int(which)))
+
+
+def nc_pair_kernel_used(ctx) -> str:
+    return {0: "none", 1: "cell", 2: "segment"}[load().nc_pair_kernel_used(ctx)]
 
 
 def nc_profile(ctx, enable: bool) -> None:
@@ -395,6 +410,12 @@ class CellList:
 
     def stencil_histogram(self):
         return nc_get_stencil_histogram(self.ctx)
+
+    def pair_kernel(self, which="auto"):
+        nc_set_pair_kernel(self.ctx, which)
+
+    def pair_kernel_used(self):
+        return nc_pair_kernel_used(self.ctx)
 
     def profile(self, enable=True):
         nc_profile(self.ctx, enable)

@@ -18,26 +18,30 @@ TOL = {"f64": (1e-12, 1e-12, 1e-12), "f32": (2e-5, 1e-6, 1e-6)}
 VAR = {"ds": oracle.DS, "do": oracle.DO}
 
 
-def gpu_eval(w, q, variant, prec, digest=True):
+def gpu_eval(w, q, variant, prec, digest=True, kernel="auto"):
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
 
     cl = CellList(variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, capacity=max(1, len(q)))
+    cl.pair_kernel(kernel)
     cl.set_box(w.L)
     qt = torch.from_numpy(np.ascontiguousarray(q)).cuda()
     F, U, W = cl.compute_forces(qt)
     torch.cuda.synchronize()
+    used = cl.pair_kernel_used()
+    if kernel != "auto":
+        assert used == kernel, (used, kernel)
     st = cl.stats()
     cell_of, cs, dims, wq = cl.cells(len(q), st["ncells"])
     dig = cl.digest(len(q)) if digest else None
     out = dict(F=F.double().cpu().numpy(), U=U, W=W, stats=st, cell_of=cell_of, cs=cs, dims=dims, wq=wq, dig=dig,
-               hist=cl.stencil_histogram(), launches=cl.launches())
+               hist=cl.stencil_histogram(), launches=cl.launches(), kernel=used)
     cl.close()
     return out
 
 
-def check_against_oracle(w, q, variant, prec, idx=None):
-    g = gpu_eval(w, q, variant, prec)
+def check_against_oracle(w, q, variant, prec, idx=None, kernel="auto"):
+    g = gpu_eval(w, q, variant, prec, kernel=kernel)
     qo = oracle_side(q, w.L, prec)
     # wrapped positions: bit-exact (same stored values)
     assert np.array_equal(g["wq"].astype(np.float64), qo)
@@ -85,6 +89,49 @@ def test_c0_equilibrium_fp64_vs_brute_force(variant):
 def test_c1_shear(variant, prec):
     w, q = inputs(1, prec)
     check_against_oracle(w, q, variant, prec)
+
+
+@pytest.mark.parametrize("kernel", ["cell", "segment"])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_c1_both_pair_kernels(variant, kernel):
+    """Sparse WCA cells (C1, ~1.3 per cell): the warp-per-cell and the row-segment
+    pair kernels each reproduce the oracle's pair set and forces."""
+    w, q = inputs(1, "f32")
+    g, _ = check_against_oracle(w, q, variant, "f32", kernel=kernel)
+    assert g["kernel"] == kernel
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_segment_kernel_on_dense_lj_cells(variant):
+    """The segment kernel forced onto dense LJ cells (~13 per cell): its staged
+    union overflows for long segments, so it must shrink segments down to one
+    cell and still match the oracle."""
+    w, q = inputs(2, "f32", scale=2)
+    check_against_oracle(w, q, variant, "f32", kernel="segment")
+
+
+def test_segment_kernel_deterministic_and_equal_pair_set():
+    w, q = inputs(3, "f32", scale=2)
+    a = gpu_eval(w, q, "do", "f32", kernel="segment")
+    b = gpu_eval(w, q, "do", "f32", kernel="segment")
+    c = gpu_eval(w, q, "do", "f32", kernel="cell")
+    assert np.array_equal(a["F"], b["F"]) and a["U"] == b["U"] and np.array_equal(a["W"], b["W"])
+    for x, y in zip(a["dig"], c["dig"]):
+        assert np.array_equal(x, y)
+    assert a["stats"]["candidates"] == c["stats"]["candidates"]
+    assert a["stats"]["stencil_cells"] == c["stats"]["stencil_cells"]
+    assert np.abs(a["F"] - c["F"]).max() <= 2e-5 * np.sqrt(np.mean(c["F"] ** 2))
+
+
+def test_pair_kernel_option_errors():
+    from paper_1412_3784_b200.nemdcell import CellList, NcError
+
+    cl = CellList("do", "f64", rc=2.5, capacity=16)
+    with pytest.raises(NcError, match="NC_E_ARG"):
+        cl.pair_kernel("segment")
+    with pytest.raises(NcError, match="NC_E_ARG"):
+        cl.pair_kernel(7)
+    cl.close()
 
 
 @pytest.mark.parametrize("variant", ["ds", "do"])
