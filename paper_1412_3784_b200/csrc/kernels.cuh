@@ -45,7 +45,11 @@ __device__ __forceinline__ uint32_t w_to_idx(double w) { return (uint32_t)w; }
 __device__ __forceinline__ double round_to(double v, float) { return (double)__double2float_rn(v); }
 __device__ __forceinline__ double round_to(double v, double) { return v; }
 
-__device__ __forceinline__ int floordiv(int a, int b) {
+__device__ __forceinline__ int floordiv(int a, int b) {  // floor(a / b) for b > 0
+  // neighbor offsets are small: compare-based fast paths avoid the integer-division sequence
+  if (a >= 0 && a < b) return 0;
+  if (a < 0 && a >= -b) return -1;
+  if (a >= b && a < 2 * b) return 1;
   int q = a / b;
   if ((a % b) != 0 && ((a < 0) != (b < 0))) --q;
   return q;
