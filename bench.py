@@ -128,14 +128,14 @@ def workload(k: int):
     return W.make(k)
 
 
-def oracle_sample(w, q32, sample: int, seed: int = 0):
+def oracle_sample(w, q32, sample: int, seed: int = 0, prec: str = "f32"):
     """The CPU oracle as it stands on a bounded sample of the workload: full O(N)
     DO cell-list build, pair loop for `sample` random particles; extrapolated to
     one full force evaluation.  Returns (interactions/s unordered, seconds per
     full evaluation, sample description, threads)."""
     import oracle
 
-    qo = oracle.wrap(q32.astype(np.float64), w.L, "f32")
+    qo = oracle.wrap(q32.astype(np.float64), w.L, prec)
     rng = np.random.default_rng(seed)
     idx = np.sort(rng.choice(len(qo), size=sample, replace=False))
     r = oracle.evaluate(oracle.DO, qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx, want=())
@@ -153,11 +153,12 @@ def run_reference(args):
     w = workload(args.config)
     from paper_1412_3784_b200 import workloads as W
 
-    q = W.positions(w, dtype=np.float32, k=args.config)
-    sample = args.ref_sample
+    prec = args.prec or w.prec[0]
+    q = W.positions(w, dtype=np.float32 if prec == "f32" else np.float64, k=args.config)
+    sample = min(args.ref_sample, w.n)
     vals, times = [], []
     for s in range(args.warmup + args.steps):
-        v, tf, r, thr = oracle_sample(w, q, sample, seed=s)
+        v, tf, r, thr = oracle_sample(w, q, sample, seed=s, prec=prec)
         if s >= args.warmup:
             vals.append(v)
             times.append(tf)
@@ -167,7 +168,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
-        "config": {"workload": f"C{args.config}", "n": w.n, "variant": "do", "box": "KR planar elongation"},
+        "config": {"workload": f"C{args.config}", "n": w.n, "variant": "do", "box": box_text(w)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
                          "sample": f"per step: full O(N) DO cell build + pair loop of {sample} random particles, "
                                    f"extrapolated to one force evaluation of all {w.n}"},
@@ -281,11 +282,13 @@ def run_ours(args):
 
     w = workload(args.config)
     peaks = load_peaks()
+    prec = args.prec or w.prec[0]          # the config's precision (BASELINE: C0 fp64, C1-C4 fp32)
+    npdt = np.float32 if prec == "f32" else np.float64
     # the same seeded workload per rank (independent replicas; slab decomposition is the next row)
-    q = W.positions(w, dtype=np.float32, k=args.config, r=0)
-    p = W.momenta(w, dtype=np.float32, k=args.config, r=0)
+    q = W.positions(w, dtype=npdt, k=args.config, r=0)
+    p = W.momenta(w, dtype=npdt, k=args.config, r=0)
     stream = torch.cuda.Stream(lrank)
-    cl = CellList(args.variant, "f32", rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
+    cl = CellList(args.variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
                   capacity=w.n, max_cells=0, device=lrank, stream=stream.cuda_stream)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
@@ -354,7 +357,13 @@ def run_ours(args):
     p32 = nsm * 128 * 2 * fmax                      # FP32 FMA lanes x 2 flops x clock
     p64 = p32 / 2.0                                 # B200 FP64 = 1/2 FP32
     flops = 9.0 * cand + 30.0 * inter               # SURVEY 8(d3) work model (algorithmic)
-    t_bound = 9.0 * cand / p32 + 30.0 * inter / p64  # filter in fp32, interactions in fp64
+    if prec == "f32":
+        t_bound = 9.0 * cand / p32 + 30.0 * inter / p64  # filter in fp32, interactions in fp64
+        peak_note = (f"blend of FP32 {p32/1e12:.1f} and FP64 {p64/1e12:.1f} TFLOP/s at {fmax/1e6:.0f} MHz x {nsm} SMs "
+                     f"for 9 flop/candidate (fp32) + 30 flop/interaction (fp64)")
+    else:
+        t_bound = flops / p64                           # NC_F64: every flop in fp64
+        peak_note = f"FP64 {p64/1e12:.1f} TFLOP/s at {fmax/1e6:.0f} MHz x {nsm} SMs (NC_F64: all work in fp64)"
     achieved = flops / (pairs_ms_avg * 1e-3) / 1e12
     peak = flops / t_bound / 1e12
     traffic = None
@@ -369,7 +378,7 @@ def run_ours(args):
     # e2e: the same metric through the C-ABI with HOST (pinned) buffers, copies inside the timed region
     e2e = None
     if rank == 0 or True:
-        qh = torch.from_numpy(q).pin_memory()
+        qh = torch.from_numpy(q).pin_memory()  # host positions in the run's precision
         Fh = torch.empty_like(qh).pin_memory()
         cl.set_box(cl_box(cl))
         cl.compute_forces(qh, Fh)  # warm-up
@@ -381,12 +390,12 @@ def run_ours(args):
         t1 = time.perf_counter()
         se = cl.stats()
         e2e = {"value": (se["interactions"] / 2.0) / ((t1 - t0) / reps), "unit": UNIT,
-               "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(Fh.numel() * 4 + 8 + 48),
+               "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(Fh.numel() * Fh.element_size() + 8 + 48),
                "call": "nc_compute_forces(host q -> host F, U, W)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, tf, r, thr = oracle_sample(w, q, args.ref_sample)
+        v, tf, r, thr = oracle_sample(w, q, min(args.ref_sample, w.n), prec=prec)
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
                "sample": f"full O(N) DO cell build + pair loop of {args.ref_sample} random particles of C{args.config}, "
                          f"extrapolated to one force evaluation ({tf:.1f} s)"}
@@ -395,19 +404,18 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
+            "dtype": prec, "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
             "config": {"workload": f"C{args.config}", "n_per_gpu": w.n, "variant": args.variant,
                        "box": box_text(w), "potential": pot_text(w),
-                       "precision": "fp32 storage + fp32 filter, fp64 interactions",
+                       "precision": ("fp32 storage + fp32 filter, fp32/fp64 two-tier interactions" if prec == "f32"
+                                     else "fp64 throughout"),
                        "l2": "inputs (~7 GB) >> L2 (126 MB); no flush", "parallelism": f"replicas x{ws}"},
             "particle_steps_per_s": psteps,
             "interactions_per_particle": inter / w.n, "candidates_per_particle": cand / w.n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_pairs",
                          "kernel_ms": pairs_ms_avg,
-                         "peak_note": f"blend of FP32 {p32/1e12:.1f} and FP64 {p64/1e12:.1f} TFLOP/s at "
-                                      f"{fmax/1e6:.0f} MHz x {nsm} SMs for 9 flop/candidate (fp32) + 30 "
-                                      f"flop/interaction (fp64)"},
+                         "peak_note": peak_note, "pair_kernel": cl.pair_kernel_used()},
             "kernel_ms_per_step": kernel_ms,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }
@@ -431,6 +439,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--variant", default="do", choices=["do", "ds"])
+    ap.add_argument("--prec", default=None, choices=["f32", "f64"], help="default: the config's precision")
     ap.add_argument("--ref-sample", type=int, default=200000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even on one GPU")
