@@ -688,6 +688,11 @@ __device__ __forceinline__ float4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return (uint32_t)v;
+}
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -748,13 +753,14 @@ __device__ __forceinline__ uint32_t sidx_of(const K3Smem<float>& sm, uint32_t t,
 
 template <bool DIGEST>
 __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                               int qlen, int lane, uint32_t stage0, const double4* __restrict__ u64) {
+                                               int qlen, int lane, uint32_t stage0, const double4* __restrict__ u64,
+                                               K3QT (*queue)[32]) {
   const int qmax = __reduce_max_sync(0xffffffffu, qlen);
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   const uint32_t dummy = stage0 + 16u * K3_DUMMY;
   for (int k = 0; k < qmax; k += 2) {
-    const uint32_t aa = k < qlen ? qaddr(sm.queue[k][lane], stage0) : dummy;
-    const uint32_t ab = k + 1 < qlen ? qaddr(sm.queue[k + 1][lane], stage0) : dummy;
+    const uint32_t aa = k < qlen ? qaddr(queue[k][lane], stage0) : dummy;
+    const uint32_t ab = k + 1 < qlen ? qaddr(queue[k + 1][lane], stage0) : dummy;
     const uint32_t ta = (aa - stage0) >> 4, tb = (ab - stage0) >> 4;
     const uint32_t ja = k < qlen ? sidx_of(sm, ta, pc.base_off) : pc.my;
     const uint32_t jb = k + 1 < qlen ? sidx_of(sm, tb, pc.base_off) : pc.my;
@@ -804,7 +810,7 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
 // the lower edge of the fp32 cutoff band: definitely inside, |f| small) in
 // fp32; everything else is compacted in place and goes to the fp64 tier.
 template <bool DIGEST>
-__device__ __forceinline__ void eval_pairs_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+__device__ __forceinline__ void eval_pairs_f32(K3QT (*queue)[32], const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                Acc32& a32, int qlen, int lane, uint32_t stage0,
                                                const double4* __restrict__ u64) {
   int nclose = qlen;
@@ -815,12 +821,12 @@ __device__ __forceinline__ void eval_pairs_f32(const Geom& g, const PairCtx<floa
     nclose = 0;
     for (int k = 0; k < qmax; ++k) {
       const bool valid = k < qlen;
-      const uint32_t a = valid ? qaddr(sm.queue[k][lane], stage0) : dummy;
+      const uint32_t a = valid ? qaddr(queue[k][lane], stage0) : dummy;
       const float4 v = lds128(a);
       const float dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       const bool far = valid && r2 >= split2 && r2 < lo32;
-      sm.queue[nclose][lane] = (K3QT)a;   // in-place compaction (nclose <= k)
+      queue[nclose][lane] = (K3QT)a;   // in-place compaction (nclose <= k)
       nclose += (valid && !far) ? 1 : 0;
       float ir2;
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
@@ -837,7 +843,7 @@ __device__ __forceinline__ void eval_pairs_f32(const Geom& g, const PairCtx<floa
     }
     __syncwarp();
   }
-  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64);
+  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, queue);
 }
 
 template <bool DIGEST>
@@ -880,7 +886,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
       }
     }
     __syncwarp();
-    eval_pairs_f32<DIGEST>(g, pc, sm, acc, a32, (int)((qa - q0) / K3_QSTRIDE), lane, stage0, u64);  // the single call site
+    eval_pairs_f32<DIGEST>(sm.queue, g, pc, sm, acc, a32, (int)((qa - q0) / K3_QSTRIDE), lane, stage0, u64);  // the single call site
     qa = q0;
     if (it >= iters) break;
   }

@@ -144,8 +144,8 @@ bool is_device_ptr(const void* p) {
 
 int cells_per_block() { return K3_CELLS; }
 
-// fp32 pair kernel generation: 1 = k_pairs (v11, default); 2 = k_pairs_v3 (two particles per lane,
-// packed FFMA2 filter; parity-green but slower on C4: 51-57 ms vs 41.6 ms) -- NC_K3=2 for A/B runs.
+// fp32 warp-per-cell pair kernel generation: 1 = k_pairs (one particle per lane, default); 2 = k_pairs_v4
+// (two particles per lane, packed FFMA2 filter, k_pairs' evaluation) -- NC_K3=2 for A/B runs.
 // Cells per warp of the sparse-cell kernel, 0 = use the warp-per-cell kernel.  Mean occupancy
 // below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~24 particles;
 // NC_SEG=0 / NC_SEG=1 force the choice (A/B runs).
@@ -290,13 +290,13 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                                                       nseg, bpl, layer0);
     } else if (k3_version() == 2) {
       ctx->pair_kernel_used = NC_PK_CELL;
-      size_t smem2 = sizeof(V3Smem);
-      static bool attr2[2] = {false, false};
-      if (!attr2[DIGEST]) {
-        CK(cudaFuncSetAttribute(k_pairs_v3<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        attr2[DIGEST] = true;
+      size_t smem4 = sizeof(K4Smem);
+      static bool attr4[2] = {false, false};
+      if (!attr4[DIGEST]) {
+        CK(cudaFuncSetAttribute(k_pairs_v4<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));
+        attr4[DIGEST] = true;
       }
-      k_pairs_v3<DIGEST><<<nblocks, 32, smem2, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
+      k_pairs_v4<DIGEST><<<nblocks, 32, smem4, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
                                                     (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl,
                                                     layer0);
     } else {
