@@ -1449,5 +1449,4 @@ __global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ sr
 
 }  // namespace nc
 
-#include "k3_pairs.cuh"
 #include "k3_seg.cuh"

@@ -144,11 +144,9 @@ bool is_device_ptr(const void* p) {
 
 int cells_per_block() { return K3_CELLS; }
 
-// fp32 warp-per-cell pair kernel generation: 1 = k_pairs (one particle per lane, default); 2 = k_pairs_v4
-// (two particles per lane, packed FFMA2 filter, k_pairs' evaluation) -- NC_K3=2 for A/B runs.
-// Cells per warp of the sparse-cell kernel, 0 = use the warp-per-cell kernel.  Mean occupancy
-// below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~24 particles;
-// NC_SEG=0 / NC_SEG=1 force the choice (A/B runs).
+// Cells per segment of the sparse-cell kernel, 0 = use the warp-per-cell kernel.  Mean occupancy
+// below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~48 particles (two
+// warps); nc_set_pair_kernel forces either kernel, NC_SEG=0 / NC_SEG=1 likewise (A/B runs).
 int seg_cells(const nc_ctx* ctx, const Geom& g) {
   static int env_mode = [] {
     const char* e = getenv("NC_SEG");
@@ -163,14 +161,6 @@ int seg_cells(const nc_ctx* ctx, const Geom& g) {
   int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
   if (blocks > ctx->max_blocks) return 0;
   return G;
-}
-
-int k3_version() {
-  static int v = [] {
-    const char* e = getenv("NC_K3");
-    return (e && e[0] == '2') ? 2 : 1;
-  }();
-  return v;
 }
 
 nc_status apply_box(nc_ctx* ctx, const double* L) {
@@ -288,17 +278,6 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       k_pairs_seg<DIGEST><<<nblocks, SG_NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
                                                       (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
                                                       nseg, bpl, layer0);
-    } else if (k3_version() == 2) {
-      ctx->pair_kernel_used = NC_PK_CELL;
-      size_t smem4 = sizeof(K4Smem);
-      static bool attr4[2] = {false, false};
-      if (!attr4[DIGEST]) {
-        CK(cudaFuncSetAttribute(k_pairs_v4<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));
-        attr4[DIGEST] = true;
-      }
-      k_pairs_v4<DIGEST><<<nblocks, 32, smem4, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
-                                                    (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl,
-                                                    layer0);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
       k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
