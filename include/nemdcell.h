@@ -72,7 +72,11 @@ typedef enum {
     NC_REMAP_NONE = 0, /* L_t = e^{At} L0 (Eq. 5) */
     NC_REMAP_LE = 1,   /* Lees-Edwards: shear A = eps e1 e2^T, tilt kept in [-1/2,1/2) by M of Eq. (8) */
     NC_REMAP_KR = 2,   /* Kraynik-Reinelt planar: L~ = e^{A (t mod t*)} L0 with e^{At*}L0 = L0 M (Eq. 9) */
-    NC_REMAP_GKR = 3   /* generalized KR, diagonal A: L~ = exp(diag(f1 w1 + f2 w2)) L0 (Eq. 10; R23) */
+    NC_REMAP_GKR = 3,  /* generalized KR, diagonal A: L~ = exp(diag(f1 w1 + f2 w2)) L0 (Eq. 10; R23) */
+    NC_REMAP_REDUCE = 4 /* any traceless A ("general three dimensional linear flows"): L_t = e^{A(t-t_r)} L_r,
+                           re-based by greedy pairwise Lagrange reduction (a unimodular change of basis of the same
+                           lattice) whenever a box vector can be shortened -- the LE reset for shear;
+                           R30.  Only L0 is used.  Valid while the lattice itself keeps h_k >= 3 r_c. */
 } nc_remap_kind;
 
 typedef struct {

@@ -12,6 +12,12 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
   reading R23 derives one: M1 = [[2,-1,-1],[-1,2,0],[-1,0,1]],
   M2 = (M1 - I)^2, L_0 = a V^T with V the eigenvectors of M1, centered
   representative f_k = alpha_k - floor(alpha_k + 1/2).
+* general traceless A ("general three dimensional linear flows"): the
+  lattice-reduction policy of reading R30 -- L_t = e^{A (t - t_r)} L_r, and
+  whenever a box vector can be shortened by adding an integer multiple of
+  another (greedy pairwise Lagrange reduction, a unimodular change of basis of
+  the same lattice), L_r <- the reduced basis, t_r <- t.  For shear it
+  reproduces the Lees-Edwards reset at half a lattice spacing.
 * SLLOD velocity-Verlet map on peculiar momenta (reading R19; the paper states
   only dq/dt = p/m and image consistency).
 """
@@ -127,6 +133,9 @@ class Box:
         check_flow(self.A)
         self.policy = policy
         self.t = float(t)
+        if policy == "reduce":  # R30: reduced basis Lr at time tr, L_t = e^{A (t - tr)} Lr
+            self.Lr, _ = lattice_reduce(expm(self.A, self.t) @ self.L0)
+            self.tr = self.t
         self.om1, self.om2 = om1, om2
         self.beta = beta
         self.tstar = tstar
@@ -144,6 +153,9 @@ class Box:
     def at(self, t: float) -> np.ndarray:
         if self.policy == "none":
             return expm(self.A, t) @ self.L0
+        if self.policy == "reduce":  # without committing a reduction (advance() commits)
+            L, _ = lattice_reduce(expm(self.A, t - self.tr) @ self.Lr)
+            return L
         if self.policy == "le":
             eps = self.A[0, 1]
             a_y = self.L0[1, 1]
@@ -164,8 +176,49 @@ class Box:
 
     def advance(self, dt: float) -> np.ndarray:
         self.t += dt
+        if self.policy == "reduce":
+            L, changed = lattice_reduce(expm(self.A, self.t - self.tr) @ self.Lr)
+            if changed:
+                self.Lr, self.tr = L, self.t
+            self.L = L
+            return self.L
         self.L = self.at(self.t)
         return self.L
+
+
+# ------------------------------------------------------------------ lattice reduction (R30)
+
+REDUCE_PAIRS = ((0, 1), (0, 2), (1, 0), (1, 2), (2, 0), (2, 1))
+REDUCE_MARGIN = 1e-12
+
+
+def _dot(a, b) -> float:
+    return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2]
+
+
+def lattice_reduce(L):
+    """Greedy pairwise Lagrange reduction of the COLUMNS of L (reading R30):
+    sweep the ordered pairs (i, j) = (0,1),(0,2),(1,0),(1,2),(2,0),(2,1); with
+    mu = floor(v_i.v_j / v_j.v_j + 1/2), replace v_i by v_i - mu v_j when that
+    is strictly shorter, |v_i - mu v_j|^2 < |v_i|^2 (1 - 1e-12); repeat sweeps
+    until none changes.  Column operations of this kind keep the lattice and
+    det L (M = L^-1 L' is integer with det +1).  Returns (L', changed)."""
+    v = [np.array(L[:, k], dtype=np.float64) for k in range(3)]
+    changed = False
+    for _ in range(64):
+        any_step = False
+        for i, j in REDUCE_PAIRS:
+            mu = math.floor(_dot(v[i], v[j]) / _dot(v[j], v[j]) + 0.5)
+            if mu == 0:
+                continue
+            w = np.array([v[i][0] - mu * v[j][0], v[i][1] - mu * v[j][1], v[i][2] - mu * v[j][2]])
+            if _dot(w, w) < _dot(v[i], v[i]) * (1.0 - REDUCE_MARGIN):
+                v[i] = w
+                any_step = True
+        if not any_step:
+            break
+        changed = True
+    return np.stack(v, axis=1), changed
 
 
 # ------------------------------------------------------------------ SLLOD

@@ -172,11 +172,43 @@ inline void expm3(const double* A, double s, double* E) {
 
 // Remapped box L~_t for a policy (closed forms).
 struct Policy {
-  int kind;          // 0 none, 1 LE, 2 KR, 3 GKR
+  int kind;          // 0 none, 1 LE, 2 KR, 3 GKR, 4 lattice reduction (R30)
   double L0[9];
   double tstar;
   double om1[3], om2[3], beta[2], eps;
+  double Lr[9], tr;  // kind 4: reduced basis Lr committed at time tr; L_t = e^{A (t - tr)} Lr
 };
+
+// Greedy pairwise Lagrange reduction of the columns of L (reading R30): sweep
+// the ordered pairs (0,1),(0,2),(1,0),(1,2),(2,0),(2,1); mu = floor(v_i.v_j /
+// v_j.v_j + 1/2); v_i <- v_i - mu v_j when |v_i - mu v_j|^2 < |v_i|^2 (1 - 1e-12);
+// repeat until a sweep changes nothing.  Same lattice, det unchanged (unimodular
+// column operations).  For shear it is the Lees-Edwards reset.
+inline bool lattice_reduce(double* L) {
+  static const int P[6][2] = {{0, 1}, {0, 2}, {1, 0}, {1, 2}, {2, 0}, {2, 1}};
+  double v[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int r = 0; r < 3; ++r) v[k][r] = M(L, r, k);
+  bool changed = false;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    bool step = false;
+    for (int q = 0; q < 6; ++q) {
+      const int i = P[q][0], j = P[q][1];
+      const double mu = std::floor(dot3(v[i], v[j]) / dot3(v[j], v[j]) + 0.5);
+      if (mu == 0.0) continue;
+      const double w[3] = {v[i][0] - mu * v[j][0], v[i][1] - mu * v[j][1], v[i][2] - mu * v[j][2]};
+      if (dot3(w, w) < dot3(v[i], v[i]) * (1.0 - 1e-12)) {
+        v[i][0] = w[0]; v[i][1] = w[1]; v[i][2] = w[2];
+        step = true;
+      }
+    }
+    if (!step) break;
+    changed = true;
+  }
+  for (int k = 0; k < 3; ++k)
+    for (int r = 0; r < 3; ++r) L[3 * r + k] = v[k][r];
+  return changed;
+}
 
 inline void box_at(const Policy& p, const double* A, double t, double* L) {
   if (p.kind == 1) {  // Lees-Edwards: tilt gamma0 + eps t kept in [-1/2, 1/2)
@@ -195,6 +227,13 @@ inline void box_at(const Policy& p, const double* A, double t, double* L) {
     matmul3(E, p.L0, L);
     return;
   }
+  if (p.kind == 4) {  // lattice reduction (R30), without committing (box_advance commits)
+    double E[9];
+    expm3(A, t - p.tr, E);
+    matmul3(E, p.Lr, L);
+    lattice_reduce(L);
+    return;
+  }
   if (p.kind == 3) {  // GKR, centered representative (R23)
     double f[2];
     for (int k = 0; k < 2; ++k) {
@@ -209,6 +248,22 @@ inline void box_at(const Policy& p, const double* A, double t, double* L) {
   double E[9];
   expm3(A, t, E);
   matmul3(E, p.L0, L);
+}
+
+// Box at t for the step loop: as box_at, and for kind 4 commits a reduction
+// (Lr, tr) when one happens.
+inline void box_advance(Policy& p, const double* A, double t, double* L) {
+  if (p.kind != 4) {
+    box_at(p, A, t, L);
+    return;
+  }
+  double E[9];
+  expm3(A, t - p.tr, E);
+  matmul3(E, p.Lr, L);
+  if (lattice_reduce(L)) {
+    std::memcpy(p.Lr, L, sizeof(double) * 9);
+    p.tr = t;
+  }
 }
 
 }  // namespace nc

@@ -455,7 +455,7 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
   for (int k = 0; k < nsteps; ++k) {
     // new box at t + dt (remapped) before the drift+wrap kernel
     double Lnew[9];
-    box_at(ctx->pol, ctx->A, ctx->t + dt, Lnew);
+    box_advance(ctx->pol, ctx->A, ctx->t + dt, Lnew);
     nc_status st = apply_box(ctx, Lnew);
     if (st) return st;
     ctx->t += dt;
@@ -811,7 +811,14 @@ nc_status nc_set_flow(nc_ctx* ctx, const double A[9], const nc_remap* pol, doubl
     p.beta[0] = pol->beta[0];
     p.beta[1] = pol->beta[1];
     p.eps = pol->eps;
-    if (p.kind < 0 || p.kind > 3) return fail(ctx, NC_E_ARG, "bad remap kind");
+    if (p.kind < 0 || p.kind > 4) return fail(ctx, NC_E_ARG, "bad remap kind");
+    if (p.kind == 4) {  // R30: reduce e^{At} L0 once, then carry (Lr, tr)
+      double E[9];
+      expm3(A, t, E);
+      matmul3(E, p.L0, p.Lr);
+      lattice_reduce(p.Lr);
+      p.tr = t;
+    }
     if (p.kind == 2 && !(p.tstar > 0)) return fail(ctx, NC_E_ARG, "KR needs tstar > 0");
     if (p.kind == 1 && !(A[1] != 0.0)) return fail(ctx, NC_E_ARG, "LE needs a shear flow A[0][1] != 0");
   } else {
@@ -992,7 +999,7 @@ nc_status nc_slab_kick_drift(nc_ctx* ctx, void* q, void* p, const void* F, int64
   SllodParams sp;
   sllod_params(ctx, dt, sp);
   double Lnew[9];
-  box_at(ctx->pol, ctx->A, ctx->t + dt, Lnew);
+  box_advance(ctx->pol, ctx->A, ctx->t + dt, Lnew);
   nc_status st = apply_box(ctx, Lnew);
   if (st) return st;
   ctx->t += dt;

@@ -18,7 +18,7 @@ from . import build as _build
 
 NC_DS, NC_DO = 0, 1
 NC_F32, NC_F64 = 0, 1
-NC_REMAP_NONE, NC_REMAP_LE, NC_REMAP_KR, NC_REMAP_GKR = 0, 1, 2, 3
+NC_REMAP_NONE, NC_REMAP_LE, NC_REMAP_KR, NC_REMAP_GKR, NC_REMAP_REDUCE = 0, 1, 2, 3, 4
 STATUS = {0: "NC_OK", 1: "NC_E_ARG", 2: "NC_E_BOX", 3: "NC_E_DEGENERATE", 4: "NC_E_FLOW", 5: "NC_E_STATE",
           6: "NC_E_CUDA", 7: "NC_E_NCCL", 8: "NC_E_OOM", 9: "NC_E_NONFINITE"}
 
@@ -315,7 +315,8 @@ def nc_last_error(ctx) -> str:
 # ----------------------------------------------------------------- convenience
 
 def make_remap(policy: str, L0, tstar=0.0, om1=None, om2=None, beta=None, eps=0.0) -> nc_remap | None:
-    kinds = {"none": NC_REMAP_NONE, "le": NC_REMAP_LE, "kr": NC_REMAP_KR, "gkr": NC_REMAP_GKR}
+    kinds = {"none": NC_REMAP_NONE, "le": NC_REMAP_LE, "kr": NC_REMAP_KR, "gkr": NC_REMAP_GKR,
+             "reduce": NC_REMAP_REDUCE}
     r = nc_remap()
     r.kind = kinds[policy]
     for k, v in enumerate(_d9(L0)):

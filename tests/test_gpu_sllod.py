@@ -158,3 +158,31 @@ def test_equilibrium_energy_conservation_gpu():
         Es.append(U + 0.5 * float((po ** 2).sum()))
     cl.close()
     assert max(abs(e - E0) for e in Es) < 1e-3 * abs(E0)
+
+
+@pytest.mark.parametrize("prec,variant", [("f64", "do"), ("f64", "ds"), ("f32", "do")])
+def test_sllod_general_flow_lattice_reduction(prec, variant):
+    """A general traceless, non-diagonal, non-nilpotent flow (shear plus an elliptic
+    part; "general three dimensional linear flows") under the lattice-
+    reduction remap policy (NC_REMAP_REDUCE, reading R30): C1's WCA system starting
+    from a basis at tilt 0.45, so the reduction (the LE reset) fires inside
+    the 20-step run; trajectory and box against the oracle's SLLOD map."""
+    w = W.make(1, scale=2)
+    a = w.L0[1, 1]
+    w.L0 = np.array([[a, 0.45 * a, 0.0], [0.0, a, 0.0], [0.0, 0.0, a]])
+    w.A = np.array([[0.0, 2.5, 0.3], [-0.2, 0.0, 0.0], [0.0, 0.4, 0.0]])
+    w.policy, w.t0, w.extra = "reduce", 0.0, {}
+    w.L = w.L0.copy()
+    nsteps, dt = 20, 0.002
+    dty = np.float64 if prec == "f64" else np.float32
+    q = W.positions(w, dtype=dty, k=1)
+    p = W.momenta(w, dtype=dty, k=1)
+    qg, pg, Lg, tg, Ug = run_gpu(w, q, p, prec, variant, dt, nsteps)
+    qo, po, Lo, to, Uo, resets = run_oracle(w, q, p, prec, variant, dt, nsteps)
+    assert resets >= 1
+    assert tg == pytest.approx(to, abs=1e-12)
+    assert np.abs(Lg - Lo).max() <= 1e-12 * np.abs(Lo).max()
+    tq, tp = (1e-9, 1e-9) if prec == "f64" else (1e-4, 1e-3)
+    assert np.abs(lattice_diff(qg - qo, Lo)).max() < tq
+    assert np.abs(pg - po).max() < tp * max(1.0, np.abs(po).max())
+    assert Ug == pytest.approx(Uo, rel=1e-9 if prec == "f64" else 1e-5)

@@ -473,3 +473,75 @@ def test_fig9_long_run_efficiency_matches_paper():
     assert eff_do == pytest.approx(GOLD["fig9_efficiency_do"]["value"], rel=0.04)
     # and DS never beats the equilibrium efficiency; DO approaches it for large boxes
     assert eff_ds < eff_do < oracle.search_efficiency_equilibrium()
+
+
+# ---------------------------------------------------------------- lattice reduction policy (R30)
+
+def test_lattice_reduce_is_the_lees_edwards_reset():
+    """For a sheared basis the greedy Lagrange reduction is exactly the LE remap
+    L -> L M with M = [[1,-1,0],[0,1,0],[0,0,1]] at half a lattice spacing."""
+    a = 10.0
+    for g, g_red in ((0.3, 0.3), (0.7, -0.3), (-0.7, 0.3), (1.6, -0.4), (0.49, 0.49), (-0.49, -0.49)):
+        L = np.array([[a, g * a, 0.0], [0.0, a, 0.0], [0.0, 0.0, a]])
+        Lr, changed = obox.lattice_reduce(L)
+        assert changed == (g != g_red)
+        assert Lr[0, 1] == pytest.approx(g_red * a, abs=1e-12)
+        assert np.array_equal(Lr[:, 0], L[:, 0]) and np.array_equal(Lr[:, 2], L[:, 2])
+    # a long shear run under the reduction policy reproduces the LE boxes (away from the tie)
+    A = np.zeros((3, 3))
+    A[0, 1] = 0.1
+    b = obox.Box(np.eye(3) * a, A, "reduce", 0.0)
+    le = obox.Box(np.eye(3) * a, A, "le", 0.0)
+    for _ in range(400):
+        b.advance(0.1)
+        le.advance(0.1)
+        if abs(abs(le.L[0, 1] / a) - 0.5) > 0.01:
+            assert np.abs(b.L - le.L).max() < 1e-12 * a
+
+
+def test_lattice_reduce_keeps_the_lattice():
+    """Random skewed bases: L' = L M with M integer, det M = +1 (same lattice),
+    and L' is pairwise reduced: no single step v_i - mu v_j shortens any column."""
+    rng = np.random.default_rng(30)
+    for _ in range(200):
+        L = np.eye(3) * 5.0 + rng.normal(scale=4.0, size=(3, 3))
+        if np.linalg.det(L) <= 0:
+            L[:, 0] *= -1
+        Lr, _ = obox.lattice_reduce(L)
+        M = np.linalg.solve(L, Lr)
+        assert np.abs(M - np.round(M)).max() < 1e-8
+        assert round(np.linalg.det(np.round(M))) == 1
+        assert np.linalg.det(Lr) == pytest.approx(np.linalg.det(L), rel=1e-12)
+        for i in range(3):
+            for j in range(3):
+                if i == j:
+                    continue
+                for mu in (-2, -1, 1, 2):
+                    w = Lr[:, i] - mu * Lr[:, j]
+                    assert w @ w >= Lr[:, i] @ Lr[:, i] * (1 - 1e-9)
+
+
+def test_reduce_policy_general_flow_stays_a_bounded_lattice():
+    """A general traceless, non-diagonal, non-nilpotent A (an elliptic flow with a
+    shear component): under the reduction policy the box is always e^{At} L0 times
+    an integer det-1 matrix, det L is constant, and the reduced box keeps every
+    height above 0.4 det^{1/3} over many flow periods (R30)."""
+    a = 8.0
+    A = np.array([[0.0, 0.3, 0.1], [-0.2, 0.0, 0.0], [0.0, 0.15, 0.0]])
+    L0 = np.eye(3) * a
+    b = obox.Box(L0, A, "reduce", 0.0)
+    det0 = np.linalg.det(L0)
+    nred = 0
+    Lprev = b.L.copy()
+    for k in range(3000):
+        L = b.advance(0.05)
+        M = np.linalg.solve(obox.expm(A, b.t) @ L0, L)
+        assert np.abs(M - np.round(M)).max() < 1e-6
+        assert np.linalg.det(L) == pytest.approx(det0, rel=1e-9)
+        Li = np.linalg.inv(L)
+        h = 1.0 / np.linalg.norm(Li, axis=1)
+        assert h.min() > 0.4 * det0 ** (1.0 / 3.0)
+        if np.abs(np.linalg.solve(Lprev, L) - np.eye(3)).max() > 0.5:
+            nred += 1
+        Lprev = L.copy()
+    assert nred >= 5
