@@ -78,7 +78,6 @@ struct Geom {
   double rsplit2;           // fp32-mode pairs with r^2 >= rsplit2 (and below band_lo) use fp32 force math
   // fp32 copies for the fp32 kernels (constant-bank operands; set by the host with the above)
   float f_split2, f_lo, f_hi, f_sig2, f_c48, f_m24;
-  float f_h16;  // fp16 pre-filter bound on r^2: rc^2 + band covering the fp16 rounding
 };
 
 enum { GEOM_OK = 0, GEOM_BAD_BOX = 1, GEOM_DEGENERATE = 2 };

@@ -22,7 +22,6 @@
 // __dadd_rn, __ddiv_rn) in the association order of the definition, so no
 // FMA contraction can change a decision.
 #pragma once
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -326,11 +325,8 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
 // 1e-12 relative band around r_c^2 by the canonical fp64 test of R16.
 // ---------------------------------------------------------------------------
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
-constexpr int K3_DUMMY = K3_CAP + 66;  // permanent far element (padding slot of the evaluation)
-constexpr int K3_STAGE = K3_CAP + 67;  // + up to 2S+2 far sentinels so the filters need no bounds checks
-#ifndef K3_HALF
-#define K3_HALF 1  // fp16 superset pre-filter on packed half2 pairs (fp32 evaluation decides)
-#endif
+constexpr int K3_DUMMY = K3_CAP + 32;  // permanent far element (padding slot of the evaluation)
+constexpr int K3_STAGE = K3_CAP + 33;  // + up to S far sentinels so the filter needs no bounds checks
 #ifndef K3_QCAP_OVR
 #define K3_QCAP_OVR 48
 #endif
@@ -356,9 +352,6 @@ constexpr double K3_BAND64 = 1e-12;
 template <typename T>
 struct K3Stage64 {  // fp32 mode: fp32 image brackets of the entries
   float Bf[K3_MAXE][3];
-#if K3_HALF
-  __half hx[K3_STAGE + 1], hy[K3_STAGE + 1], hz[K3_STAGE + 1];  // fp16 copies of the staged x, y, z
-#endif
 };
 template <>
 struct K3Stage64<double> {  // fp64 mode: stage holds LAB positions; packed DO home shift of each j
@@ -899,93 +892,6 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
   }
 }
 
-#if K3_HALF
-// fp16 superset pre-filter: stream s tests staged PAIRS
-// (2p, 2p+1), p = s, s+S, ..., with half2 arithmetic in the cell-local frame,
-// d = v - u_i, r^2 = d.d, against r_c^2 + band16 (the fp16 error bound of the
-// host, Geom::band16, covers every true member); both elements' fp32 addresses
-// are queued under the two predicates of one HSETP2.  The fp32 evaluation then
-// re-decides every queued pair exactly as after the fp32 filter.
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void queue_pair_h(uint32_t& qa, uint32_t a0, __half2 r2, __half2 hi) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\tsetp.lt.f16x2 p|q, %1, %2;\n\tst.shared.u16 [%0], %3;\n\t@p add.u32 %0, %0, %5;"
-      "\n\tst.shared.u16 [%0], %4;\n\t@q add.u32 %0, %0, %5;\n\t}"
-      : "+r"(qa)
-      : "r"(*reinterpret_cast<uint32_t*>(&r2)), "r"(*reinterpret_cast<uint32_t*>(&hi)), "h"((unsigned short)a0),
-        "h"((unsigned short)(a0 + 16u)), "n"(K3_QSTRIDE)
-      : "memory");
-}
-
-template <bool DIGEST>
-__device__ __forceinline__ void filter_chunk_h(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                               Acc32& a32, int s, int S, int npairs, int lane,
-                                               const double4* __restrict__ u64, bool act) {
-  static_assert(!K3_Q32, "the fp16 filter stores 16-bit queue entries");
-  const uint32_t stage0 = smem_u32(&sm.stage[0]);
-  const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
-  constexpr int UNR = K3_UNROLL / 2;                      // pairs per group: 2 UNR candidates
-  const uint32_t qlim = q0 + K3_QSTRIDE * (K3_QCAP - 2 * UNR);
-  const uint32_t hx0 = smem_u32(&sm.s64.hx[0]);
-  constexpr uint32_t HOFF = 2 * (K3_STAGE + 1);           // bytes between hx, hy, hz
-  const float far = 60000.0f;
-  const __half2 ux = __float2half2_rn(act ? pc.fx : -far), uy = __float2half2_rn(act ? pc.fy : -far),
-                uz = __float2half2_rn(act ? pc.fz : -far);
-  const __half2 hi = __float2half2_rn(g.f_h16);
-  uint32_t ha = hx0 + 4u * (uint32_t)s;                   // half2 of pair p = s at byte 4p
-  uint32_t aa = stage0 + 32u * (uint32_t)s;               // fp32 element 2p
-  const uint32_t hstep = 4u * (uint32_t)S, astep = 32u * (uint32_t)S;
-  const int iters = (npairs + S - 1) / S;
-  uint32_t qa = q0;
-  int it = 0;
-  const int main_iters = iters - iters % UNR;
-  for (;;) {
-    bool full = false;
-    while (it < main_iters) {
-      uint32_t X[UNR], Y[UNR], Z[UNR];
-#pragma unroll
-      for (int k = 0; k < UNR; ++k) {  // all loads of the group first (the asm keeps program order)
-        X[k] = lds32(ha + hstep * k);
-        Y[k] = lds32(ha + hstep * k + HOFF);
-        Z[k] = lds32(ha + hstep * k + 2 * HOFF);
-      }
-#pragma unroll
-      for (int k = 0; k < UNR; ++k) {
-        const __half2 dx = __hsub2(*reinterpret_cast<const __half2*>(&X[k]), ux);
-        const __half2 dy = __hsub2(*reinterpret_cast<const __half2*>(&Y[k]), uy);
-        const __half2 dz = __hsub2(*reinterpret_cast<const __half2*>(&Z[k]), uz);
-        const __half2 r2 = __hfma2(dz, dz, __hfma2(dy, dy, __hmul2(dx, dx)));
-        queue_pair_h(qa, aa + astep * k, r2, hi);
-      }
-      ha += hstep * UNR;
-      aa += astep * UNR;
-      it += UNR;
-      if (__any_sync(0xffffffffu, qa > qlim)) { full = true; break; }
-    }
-    if (!full) {
-      for (; it < iters; ++it) {
-        const uint32_t X = lds32(ha), Y = lds32(ha + HOFF), Z = lds32(ha + 2 * HOFF);
-        const __half2 dx = __hsub2(*reinterpret_cast<const __half2*>(&X), ux);
-        const __half2 dy = __hsub2(*reinterpret_cast<const __half2*>(&Y), uy);
-        const __half2 dz = __hsub2(*reinterpret_cast<const __half2*>(&Z), uz);
-        const __half2 r2 = __hfma2(dz, dz, __hfma2(dy, dy, __hmul2(dx, dx)));
-        queue_pair_h(qa, aa, r2, hi);
-        ha += hstep;
-        aa += astep;
-      }
-    }
-    __syncwarp();
-    eval_pairs_f32<DIGEST>(sm.queue, g, pc, sm, acc, a32, (int)((qa - q0) / K3_QSTRIDE), lane, stage0, u64);
-    qa = q0;
-    if (it >= iters) break;
-  }
-}
-#endif
-
 // One warp per block; each warp handles K3_CELLS consecutive cells of one
 // cell layer, so block partials are layer-aligned and their fixed-order sums
 // are independent of timing (determinism).  grid = l3 * blocks_per_layer.
@@ -1131,11 +1037,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
                 const float x = pp[r].x + sm.s64.Bf[ee[r]][0], y = pp[r].y + sm.s64.Bf[ee[r]][1],
                             z = pp[r].z + sm.s64.Bf[ee[r]][2];
                 sm.stage[tt[r]] = make_float4(x, y, z, fmaf(z, z, fmaf(y, y, x * x)));  // .w = |v|^2
-#if K3_HALF
-                sm.s64.hx[tt[r]] = __float2half_rn(x);
-                sm.s64.hy[tt[r]] = __float2half_rn(y);
-                sm.s64.hz[tt[r]] = __float2half_rn(z);
-#endif
               }
             }
           }
@@ -1155,28 +1056,17 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             }
           }
         }
-        // far sentinels after the chunk (S for the fp32 filter; 2S+2 for the pair-wise fp16 filter)
-        for (int q = lane; q < (sizeof(T) == 4 && K3_HALF ? 2 * S + 2 : S); q += 32) {
-          sm.stage[ctot + q] = far4<T>();
-          sm.sent[ctot + q] = 0;
-          if constexpr (sizeof(T) == 8) sm.s64.nh[ctot + q] = 0u;
-#if K3_HALF
-          if constexpr (sizeof(T) == 4) {
-            sm.s64.hx[ctot + q] = __float2half_rn(60000.0f);
-            sm.s64.hy[ctot + q] = __float2half_rn(60000.0f);
-            sm.s64.hz[ctot + q] = __float2half_rn(60000.0f);
-          }
-#endif
+        // S far sentinels after the chunk (indices ctot .. ctot+S-1)
+        if (lane < S) {
+          sm.stage[ctot + lane] = far4<T>();
+          sm.sent[ctot + lane] = 0;
+          if constexpr (sizeof(T) == 8) sm.s64.nh[ctot + lane] = 0u;
         }
         __syncwarp();
         const int iters = (int)((ctot + S - 1) / S);
         pc.base_off = base_off;
         if constexpr (sizeof(T) == 4) {
-#if K3_HALF
-          filter_chunk_h<DIGEST>(g, pc, sm, acc, a32, s, S, (int)((ctot + 1) / 2), lane, u, act);
-#else
           filter_chunk_f32<DIGEST>(g, pc, sm, acc, a32, s, S, iters, lane, u);
-#endif
         } else {
           filter_chunk<T, DIGEST>(g, pc, sm, acc, s, S, iters, lane);
         }

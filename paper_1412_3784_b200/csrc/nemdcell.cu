@@ -194,22 +194,6 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   g.f_sig2 = (float)g.sig2;
   g.f_c48 = (float)(48.0 * g.eps);
   g.f_m24 = (float)(-24.0 * g.eps);
-  {
-    // fp16 pre-filter band: staged members lie within |v| <= (cell diagonal) + rc of the cell origin;
-    // half rounding of v, u and of d = v - u is <= 1.5 ulp16(Vnear) per component, |d| <= rc, plus the
-    // rounding of the three products and two sums (<= 3 * 2^-11 rc^2 each side): take 4 times that
-    double e[3][3];  // cell edge vectors (columns of L / c for DS; DO: widths along x, y, z)
-    for (int k = 0; k < 3; ++k)
-      for (int r = 0; r < 3; ++r)
-        e[k][r] = g.variant == 0 ? M(g.L, r, k) / g.dims[k] : (r == k ? g.w[k] : 0.0);
-    double dg[3] = {e[0][0] + e[1][0] + e[2][0], e[0][1] + e[1][1] + e[2][1], e[0][2] + e[1][2] + e[2][2]};
-    double diag = std::sqrt((dg[0] * dg[0] + dg[1] * dg[1]) + dg[2] * dg[2]);  // cell diagonal
-    double vnear = diag + g.rc;
-    double ulp16 = std::ldexp(1.0, (int)std::floor(std::log2(vnear)) - 10);
-    // measured worst case on 2e6 random member pairs: 0.0243 for C4's cells (band below: 0.10)
-    double band = 1.5 * (2.0 * std::sqrt(3.0) * g.rc * 1.5 * ulp16 + 6.0 * std::ldexp(1.0, -11) * g.rc2);
-    g.f_h16 = (float)(g.rc2 + band);
-  }
   ctx->g = g;
   ctx->have_box = true;
   return NC_OK;
