@@ -377,9 +377,12 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     const int ecA = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + A;
     const uint32_t P0 = sm.e_start[ecA];
     const uint32_t P1 = sm.e_start[ecA + Gs - 1] + (uint32_t)(sm.e_off[ecA + Gs] - sm.e_off[ecA + Gs - 1]);
-    for (uint32_t pb = P0 + 32u * (uint32_t)wid; pb < P1; pb += (uint32_t)SG_NT) {
+    // each warp takes a contiguous share of the segment's particles (balanced across the block)
+    const uint32_t per = (P1 - P0 + SG_NW - 1) / SG_NW;
+    const uint32_t W0 = min(P1, P0 + per * (uint32_t)wid), W1 = min(P1, W0 + per);
+    for (uint32_t pb = W0; pb < W1; pb += 32u) {
       const uint32_t p = pb + (uint32_t)lane;
-      const bool act = p < P1;
+      const bool act = p < W1;
       // cell of p inside the segment
       int gc = 0;
       if (act) {

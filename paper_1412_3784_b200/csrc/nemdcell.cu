@@ -156,7 +156,7 @@ int seg_cells(const nc_ctx* ctx, const Geom& g) {
   if (mode == 0) return 0;
   const double occ = (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (mode < 0 && occ >= 4.0) return 0;
-  int G = (int)std::floor(24.0 * SG_NW / std::max(occ, 0.5));
+  int G = (int)std::floor(28.0 * SG_NW / std::max(occ, 0.5));  // ~28 particles per warp
   G = std::max(4, std::min(G, std::min(SG_GMAX, g.dims[0])));
   int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
   if (blocks > ctx->max_blocks) return 0;
