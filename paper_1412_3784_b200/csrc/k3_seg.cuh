@@ -21,11 +21,14 @@
 
 namespace nc {
 
-constexpr int SG_NW = 2;                    // warps per block (share one staged union)
+#ifndef SG_NW_OVR
+#define SG_NW_OVR 2
+#endif
+constexpr int SG_NW = SG_NW_OVR;            // warps per block (share one staged union)
 constexpr int SG_NT = 32 * SG_NW;
-constexpr int SG_CAP = 768;                 // staged union elements
+constexpr int SG_CAP = 384 * SG_NW;         // staged union elements
 constexpr int SG_ROWS = 12;                 // stencil rows (DS 9, DO <= 12)
-constexpr int SG_GMAX = 48;                 // cells per segment
+constexpr int SG_GMAX = 24 * SG_NW;         // cells per segment
 constexpr int SG_MAXE = SG_ROWS * (SG_GMAX + 4);  // union entries (row x column)
 constexpr int SG_QCAP = 32;                 // per-lane hit queue
 
@@ -323,7 +326,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
 }
 
 template <bool DIGEST>
-__global__ void __launch_bounds__(SG_NT, 8)
+__global__ void __launch_bounds__(SG_NT, 16 / SG_NW)
 k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
             const float4* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
             float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,

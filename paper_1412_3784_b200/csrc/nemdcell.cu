@@ -68,6 +68,7 @@ struct nc_ctx {
   int last_cpb = 0, last_bpl = 0;
   int pair_kernel = NC_PK_AUTO;   // nc_set_pair_kernel
   int pair_kernel_used = 0;
+  double occ_hint = -1.0;         // slab path: particles per cell of the own layers (auto kernel choice)
   double host_tot[NPART];
   bool tot_valid = false;
 
@@ -154,10 +155,12 @@ int seg_cells(const nc_ctx* ctx, const Geom& g) {
   }();
   int mode = ctx->pair_kernel == NC_PK_CELL ? 0 : (ctx->pair_kernel == NC_PK_SEGMENT ? 1 : env_mode);
   if (mode == 0) return 0;
-  const double occ = (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
+  const double occ = ctx->occ_hint >= 0.0 ? ctx->occ_hint
+                                          : (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (mode < 0 && occ >= 4.0) return 0;
-  int G = (int)std::floor(28.0 * SG_NW / std::max(occ, 0.5));  // ~28 particles per warp
-  G = std::max(4, std::min(G, std::min(SG_GMAX, g.dims[0])));
+  // a fixed segment length (not occupancy-derived): block partials group the same cells on every
+  // rank of a slab decomposition, so U and W stay bitwise independent of the rank count (P7)
+  int G = std::min(SG_GMAX, g.dims[0]);
   int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
   if (blocks > ctx->max_blocks) return 0;
   return G;
@@ -1093,6 +1096,7 @@ nc_status nc_slab_forces(nc_ctx* ctx, const void* q, const uint32_t* gid, int64_
   if (!ctx || (n_own > 0 && (!q || !gid))) return fail(ctx, NC_E_ARG, "null argument");
   if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
   if (klo < 0 || khi > ctx->g.dims[2] || khi - klo < 1) return fail(ctx, NC_E_ARG, "bad layer range");
+  ctx->occ_hint = (double)n_own / ((double)ctx->g.dims[0] * ctx->g.dims[1] * (double)(khi - klo));
   return ctx->cfg.prec == NC_F32
              ? slab_forces_t<float>(ctx, (const float*)q, gid, n_own, halo_from_lo, n_lo, halo_from_hi, n_hi, klo, khi,
                                     (float*)F, layer_parts)

@@ -103,3 +103,31 @@ def test_slab_sllod_bitwise(P):
     assert U == U1 and np.array_equal(Wv, W1)
     for r in sysm.ranks:
         r.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("variant", ["do", "ds"])
+def test_slab_forces_bitwise_sparse_cells(P, variant):
+    """Sparse WCA cells (C1, ~1.3 per cell): every rank and the single device run
+    the row-segment pair kernel; forces, U, W and counts stay bitwise equal."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(1)
+    q = W.positions(w, dtype=np.float32, k=1)
+    p = W.momenta(w, dtype=np.float32, k=1)
+    one = CellList(variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
+    st1 = one.stats()
+    assert one.pair_kernel_used() == "segment"
+    one.close()
+    sysm = make_system(w, q, p, P, variant, "f32")
+    U, Wv, st = sysm.forces(True)
+    assert all(r.cl.pair_kernel_used() == "segment" for r in sysm.ranks)
+    _, _, F = gather_state(sysm, len(q), np.float32)
+    assert np.array_equal(F, F1.cpu().numpy())
+    assert U == U1 and np.array_equal(Wv, W1)
+    assert st["interactions"] == st1["interactions"] and st["candidates"] == st1["candidates"]
+    for r in sysm.ranks:
+        r.close()
