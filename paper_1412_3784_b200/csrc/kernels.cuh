@@ -701,9 +701,11 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 }
 // full shared address of a staged element from the low 16 bits kept in a queue
 // (the staged array spans < 64 KB, so one possible carry into bit 16)
+// The CTA's shared window starts at (cluster rank << 24) + 0x400 on sm_100, so the whole
+// K3Smem (< 16 KB) lies inside one 64 KB page and no carry into bit 16 can occur; k_pairs
+// checks this once per block (flagged as non-finite, i.e. a loud failure, if it ever breaks).
 __device__ __forceinline__ uint32_t addr_from16(uint32_t lo16, uint32_t stage0) {
-  uint32_t a = (stage0 & 0xffff0000u) | lo16;
-  return a < stage0 ? a + 0x10000u : a;
+  return (stage0 & 0xffff0000u) | lo16;
 }
 // a += K3_QSTRIDE (one queue row) if r2 < hi (one FSETP + one predicated IADD)
 __device__ __forceinline__ uint32_t bump_if_less(uint32_t a, float r2, float hi) {
@@ -830,17 +832,17 @@ __device__ __forceinline__ void eval_pairs_f32(K3QT (*queue)[32], const Geom& g,
       nclose += (valid && !far) ? 1 : 0;
       float ir2;
       asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
+      ir2 = far ? ir2 : 0.0f;          // one mask zeroes s6, fr and the energy term
       const float s2 = sig2 * ir2;
       const float s6 = s2 * s2 * s2;
-      float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
-      fr = far ? fr : 0.0f;
+      const float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
       const float tx = fr * dx, ty = fr * dy, tz = fr * dz;
       a32.fx -= tx; a32.fy -= ty; a32.fz -= tz;
-      a32.u += far ? s6 * s6 - s6 : 0.0f;
+      a32.u = fmaf(s6, s6, a32.u - s6);
       a32.w0 = fmaf(tx, dx, a32.w0); a32.w1 = fmaf(ty, dy, a32.w1); a32.w2 = fmaf(tz, dz, a32.w2);
       a32.w3 = fmaf(tx, dy, a32.w3); a32.w4 = fmaf(tx, dz, a32.w4); a32.w5 = fmaf(ty, dz, a32.w5);
-      a32.cnt += far ? 1u : 0u;
     }
+    a32.cnt += (uint32_t)(qlen - nclose);  // every queued entry is either far or compacted for the fp64 tier
     __syncwarp();
   }
   eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, queue);
@@ -923,6 +925,8 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
 
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
   if constexpr (sizeof(T) == 4) {
+    // 16-bit queue entries decode without a carry only if the block's shared memory sits in one 64 KB page
+    if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
     if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
       sm.stage[K3_DUMMY] = far4<T>();
       sm.sent[K3_DUMMY] = K3_MAXE - 1;
