@@ -350,7 +350,8 @@ constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil 
 constexpr double K3_BAND64 = 1e-12;
 
 template <typename T>
-struct K3Stage64 {  // fp32 mode: fp32 image brackets of the entries
+struct K3Stage64 {  // fp32 mode: staged x, y, z (image bracket applied) as separate arrays, entry brackets
+  float sx[K3_STAGE], sy[K3_STAGE], sz[K3_STAGE];
   float Bf[K3_MAXE][3];
 };
 template <>
@@ -360,7 +361,7 @@ struct K3Stage64<double> {  // fp64 mode: stage holds LAB positions; packed DO h
 
 template <typename T>
 struct K3Smem {
-  typename V4<T>::t stage[K3_STAGE];  // filter copy, .w = sorted index
+  typename V4<T>::t stage[sizeof(T) == 8 ? K3_STAGE : 1];  // fp64 mode: staged lab positions, .w = sorted index
   K3Stage64<T> s64;
   K3QT queue[K3_QCAP][32];
   uint8_t sent[K3_STAGE];
@@ -731,6 +732,15 @@ __device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) {
 #endif
 }
 
+// fp32 staging is three float arrays (sx, sy, sz): a broadcast LDS.32 is one shared-memory
+// wavefront, a 16-byte LDS.128 four (the filter is bound by the shared-memory pipe)
+constexpr uint32_t K3_YOFF = 4u * K3_STAGE, K3_ZOFF = 8u * K3_STAGE;  // bytes from sx to sy, sz
+__device__ __forceinline__ float ldsf(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
 // fp32 accumulators of the far-pair tier (folded into the fp64 Acc after each evaluation)
 struct Acc32 {
   float fx, fy, fz, u, w0, w1, w2, w3, w4, w5;
@@ -759,11 +769,11 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
                                                K3QT (*queue)[32]) {
   const int qmax = __reduce_max_sync(0xffffffffu, qlen);
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
-  const uint32_t dummy = stage0 + 16u * K3_DUMMY;
+  const uint32_t dummy = stage0 + 4u * K3_DUMMY;
   for (int k = 0; k < qmax; k += 2) {
     const uint32_t aa = k < qlen ? qaddr(queue[k][lane], stage0) : dummy;
     const uint32_t ab = k + 1 < qlen ? qaddr(queue[k + 1][lane], stage0) : dummy;
-    const uint32_t ta = (aa - stage0) >> 4, tb = (ab - stage0) >> 4;
+    const uint32_t ta = (aa - stage0) >> 2, tb = (ab - stage0) >> 2;
     const uint32_t ja = k < qlen ? sidx_of(sm, ta, pc.base_off) : pc.my;
     const uint32_t jb = k + 1 < qlen ? sidx_of(sm, tb, pc.base_off) : pc.my;
     const int ea = sm.sent[ta], eb = sm.sent[tb];
@@ -819,13 +829,13 @@ __device__ __forceinline__ void eval_pairs_f32(K3QT (*queue)[32], const Geom& g,
   if (!DIGEST) {
     const int qmax = __reduce_max_sync(0xffffffffu, qlen);
     const float split2 = (float)g.rsplit2, lo32 = (float)g.band_lo, sig2 = (float)g.sig2, eps24 = (float)(24.0 * g.eps);
-    const uint32_t dummy = stage0 + 16u * K3_DUMMY;
+    const uint32_t dummy = stage0 + 4u * K3_DUMMY;
     nclose = 0;
     for (int k = 0; k < qmax; ++k) {
       const bool valid = k < qlen;
       const uint32_t a = valid ? qaddr(queue[k][lane], stage0) : dummy;
-      const float4 v = lds128(a);
-      const float dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
+      const float vx = ldsf(a), vy = ldsf(a + K3_YOFF), vz = ldsf(a + K3_ZOFF);
+      const float dx = vx - pc.fx, dy = vy - pc.fy, dz = vz - pc.fz;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       const bool far = valid && r2 >= split2 && r2 < lo32;
       queue[nclose][lane] = (K3QT)a;   // in-place compaction (nclose <= k)
@@ -852,12 +862,12 @@ template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                  Acc32& a32, int s, int S, int iters, int lane,
                                                  const double4* __restrict__ u64) {
-  const uint32_t stage0 = smem_u32(&sm.stage[0]);
+  const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
   const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
   const uint32_t qlim = q0 + K3_QSTRIDE * (K3_QCAP - K3_UNROLL);
-  const uint32_t step = 16u * (uint32_t)S;
-  const float mx = pc.m2x, my = pc.m2y, mz = pc.m2z, uu = pc.uu, hi = pc.hi;
-  uint32_t sa = stage0 + 16u * (uint32_t)s;
+  const uint32_t step = 4u * (uint32_t)S;
+  const float fx = pc.fx, fy = pc.fy, fz = pc.fz, hi = pc.hi;
+  uint32_t sa = stage0 + 4u * (uint32_t)s;
   uint32_t qa = q0;
   int it = 0;
   const int main_iters = iters - iters % K3_UNROLL;
@@ -865,23 +875,29 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     // filter groups of K3_UNROLL until some lane's queue is nearly full
     bool full = false;
     while (it < main_iters) {
+      float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
+#pragma unroll
+      for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
+        vx[k] = ldsf(sa + step * k);
+        vy[k] = ldsf(sa + step * k + K3_YOFF);
+        vz[k] = ldsf(sa + step * k + K3_ZOFF);
+      }
 #pragma unroll
       for (int k = 0; k < K3_UNROLL; ++k) {
-        float4 v = lds128(sa);
-        // r^2 = (|v|^2 + |u|^2) - 2 v.u: 1 FADD + 3 FFMA; cancellation error <~ 1e-5 sigma^2, far inside
-        // the superset band (R16 membership is decided later in fp64)
-        float r2 = fmaf(v.z, mz, fmaf(v.y, my, fmaf(v.x, mx, v.w + uu)));
-        stsq(qa, sa);
+        // difference form (3 LDS.32, 3 FADD + FMUL + 2 FFMA): d = v - u_i, r^2 = d.d
+        const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        stsq(qa, sa + step * k);
         qa = bump_if_less(qa, r2, hi);
-        sa += step;
       }
+      sa += step * K3_UNROLL;
       it += K3_UNROLL;
       if (__any_sync(0xffffffffu, qa > qlim)) { full = true; break; }
     }
     if (!full) {  // remainder (< K3_UNROLL iterations; every queue has room for them)
       for (; it < iters; ++it) {
-        float4 v = lds128(sa);
-        float r2 = fmaf(v.z, mz, fmaf(v.y, my, fmaf(v.x, mx, v.w + uu)));
+        const float dx = ldsf(sa) - fx, dy = ldsf(sa + K3_YOFF) - fy, dz = ldsf(sa + K3_ZOFF) - fz;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
         stsq(qa, sa);
         qa = bump_if_less(qa, r2, hi);
         sa += step;
@@ -928,7 +944,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     // 16-bit queue entries decode without a carry only if the block's shared memory sits in one 64 KB page
     if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
     if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
-      sm.stage[K3_DUMMY] = far4<T>();
+      sm.s64.sx[K3_DUMMY] = sm.s64.sy[K3_DUMMY] = sm.s64.sz[K3_DUMMY] = 1e30f;
       sm.sent[K3_DUMMY] = K3_MAXE - 1;
       sm.e_B[K3_MAXE - 1][0] = 1e150; sm.e_B[K3_MAXE - 1][1] = 1e150; sm.e_B[K3_MAXE - 1][2] = 1e150;
     }
@@ -1040,7 +1056,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
               if (tt[r] < ctot) {
                 const float x = pp[r].x + sm.s64.Bf[ee[r]][0], y = pp[r].y + sm.s64.Bf[ee[r]][1],
                             z = pp[r].z + sm.s64.Bf[ee[r]][2];
-                sm.stage[tt[r]] = make_float4(x, y, z, fmaf(z, z, fmaf(y, y, x * x)));  // .w = |v|^2
+                sm.s64.sx[tt[r]] = x;
+                sm.s64.sy[tt[r]] = y;
+                sm.s64.sz[tt[r]] = z;
               }
             }
           }
@@ -1062,9 +1080,13 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         }
         // S far sentinels after the chunk (indices ctot .. ctot+S-1)
         if (lane < S) {
-          sm.stage[ctot + lane] = far4<T>();
+          if constexpr (sizeof(T) == 8) {
+            sm.stage[ctot + lane] = far4<T>();
+            sm.s64.nh[ctot + lane] = 0u;
+          } else {
+            sm.s64.sx[ctot + lane] = sm.s64.sy[ctot + lane] = sm.s64.sz[ctot + lane] = 1e30f;
+          }
           sm.sent[ctot + lane] = 0;
-          if constexpr (sizeof(T) == 8) sm.s64.nh[ctot + lane] = 0u;
         }
         __syncwarp();
         const int iters = (int)((ctot + S - 1) / S);
