@@ -41,10 +41,11 @@ struct SgSmem {
   uint8_t e_ci[SG_MAXE];                    // column index inside the row's union range
   uint16_t rg[SG_GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
   uint16_t queue[SG_NW][SG_QCAP][32];
-  uint32_t ssum[SG_NW];                     // block scan scratch
+  uint32_t wtot[SG_NW][SG_ROWS];            // per-warp row totals (block scan)
   double part[SG_NW][NPART];                // per-warp partials (fixed-order combine)
   uint32_t cst[SG_GMAX];                    // first sorted particle of each segment cell
   uint16_t ct0[SG_GMAX];                    // staged offset of each segment cell
+  uint16_t nsz[SG_GMAX];                    // neighborhood size (cells) of each segment cell
   // rows
   int r_lo[SG_ROWS], r_n[SG_ROWS], r_eb[SG_ROWS + 1], r_base[SG_ROWS];
   int r_ny[SG_ROWS], r_nz[SG_ROWS];         // image shifts of the row (DO n2, n3; DS n1, n2)
@@ -145,54 +146,56 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
   const int nrows = sm.nrows;
   const int E = sm.r_eb[nrows];
   if (E > SG_MAXE) return false;
-  // ---- entries (row, column): all cell-start loads issued first, then a block scan of the counts
-  constexpr int SG_EPT = (SG_MAXE + SG_NT - 1) / SG_NT;
-  uint32_t est[SG_EPT], ecn[SG_EPT];
+  // ---- entries (row, column), row-major: thread tid owns column tid of every row (a row spans at
+  // most G + 4 <= SG_NT columns).  All cell-start loads first; then per-row warp scans and one
+  // barrier give every entry's staging offset (entries numbered row by row, e = r_eb[r] + ci).
+  static_assert(SG_GMAX + 4 <= SG_NT, "a union row must fit one column per thread");
+  uint32_t est[SG_ROWS], ecn[SG_ROWS];
 #pragma unroll
-  for (int k = 0; k < SG_EPT; ++k) {
-    const int e = k * SG_NT + tid;
-    est[k] = 0u;
-    ecn[k] = 0u;
-    if (e < E) {
-      int r = 0;
-      while (r + 1 < nrows && sm.r_eb[r + 1] <= e) ++r;
-      const int ci = e - sm.r_eb[r];
-      const int col = sm.r_lo[r] + ci;
+  for (int r = 0; r < SG_ROWS; ++r) {
+    est[r] = 0u;
+    ecn[r] = 0u;
+    if (r < nrows && tid < sm.r_n[r]) {
+      const int col = sm.r_lo[r] + tid;
       const int nx = fdiv_fast(col, l1);
       const uint32_t cell = (uint32_t)sm.r_base[r] + (uint32_t)(col - nx * l1);
-      est[k] = cs[cell];
-      ecn[k] = cs[cell + 1];
+      est[r] = cs[cell];
+      ecn[r] = cs[cell + 1];
+      const int e = sm.r_eb[r] + tid;
       sm.e_row[e] = (uint8_t)r;
-      sm.e_ci[e] = (uint8_t)ci;
+      sm.e_ci[e] = (uint8_t)tid;
     }
   }
-  uint32_t tot = 0;
+  uint32_t incl[SG_ROWS];
 #pragma unroll
-  for (int k = 0; k < SG_EPT; ++k) {
-    if (k * SG_NT >= E) break;
-    const int e = k * SG_NT + tid;
-    const uint32_t cnt = ecn[k] - est[k];
-    uint32_t y = cnt;
+  for (int r = 0; r < SG_ROWS; ++r) {
+    uint32_t y = ecn[r] - est[r];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
       if (lane >= o) y += z;
     }
-    if (lane == 31) sm.ssum[wid] = y;
-    __syncthreads();
-    uint32_t before = tot, all = 0;
+    incl[r] = y;
+    if (lane == 31) sm.wtot[wid][r] = y;
+  }
+  __syncthreads();
+  uint32_t tot = 0;
+#pragma unroll
+  for (int r = 0; r < SG_ROWS; ++r) {
+    if (r >= nrows) break;
+    uint32_t before = tot, rowtot = 0;
 #pragma unroll
     for (int w = 0; w < SG_NW; ++w) {
-      const uint32_t v = sm.ssum[w];
+      const uint32_t v = sm.wtot[w][r];
       if (w < wid) before += v;
-      all += v;
+      rowtot += v;
     }
-    if (e < E) {
-      sm.e_start[e] = est[k];
-      sm.e_off[e] = (uint16_t)min(before + y - cnt, 65535u);
+    if (tid < sm.r_n[r]) {
+      const int e = sm.r_eb[r] + tid;
+      sm.e_start[e] = est[r];
+      sm.e_off[e] = (uint16_t)min(before + incl[r] - (ecn[r] - est[r]), 65535u);
     }
-    tot += all;
-    __syncthreads();
+    tot += rowtot;
   }
   if (tid == 0) sm.e_off[E] = (uint16_t)min(tot, 65535u);
   __syncthreads();
@@ -230,6 +233,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
   // ---- per cell and row: the cell's own sub-range of the union row (exact stencil of k_pairs)
   if (tid < G) {
     const int a0 = A + tid;
+    int ns = 0;
     for (int r = 0; r < nrows; ++r) {
       int c0, c1;
       if (g.variant == 0) {
@@ -239,10 +243,12 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
         c0 = (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
         c1 = (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r]));
       }
+      ns += c1 - c0;
       const int eb = sm.r_eb[r] - sm.r_lo[r];
       sm.rg[tid][r][0] = sm.e_off[eb + c0];
       sm.rg[tid][r][1] = sm.e_off[eb + c1];
     }
+    sm.nsz[tid] = (uint16_t)ns;
     const int ec = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + a0;
     sm.cst[tid] = sm.e_start[ec];
     sm.ct0[tid] = sm.e_off[ec];
@@ -363,19 +369,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     }
     const int nrows = sm.nrows;
     // neighborhood size of every cell (instrumentation: k_pairs' tS)
-    if (tid < Gs) {
-      int ns = 0;
-      for (int r = 0; r < nrows; ++r) {
-        // cells of the sub-range = columns; recover from the entry offsets is not possible for empty cells,
-        // so count columns directly
-        if (g.variant == 0) ns += 3;
-        else {
-          const int a0 = A + tid;
-          ns += (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r])) - (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
-        }
-      }
-      tS += (double)ns;
-    }
+    if (tid < Gs) tS += (double)sm.nsz[tid];
     // particles of the segment: contiguous in the center row
     const int ecA = sm.r_eb[sm.r0] - sm.r_lo[sm.r0] + A;
     const uint32_t P0 = sm.e_start[ecA];
