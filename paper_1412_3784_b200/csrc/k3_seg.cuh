@@ -55,13 +55,6 @@ struct SgSmem {
   int nrows, r0;                            // row count; the center row (dy = dz = 0)
 };
 
-__device__ __forceinline__ int fdiv_fast(int m, int l) {  // floor(m / l), l > 0; |m| small in practice
-  if (m >= 0 && m < l) return 0;
-  if (m < 0 && m >= -l) return -1;
-  if (m >= l && m < 2 * l) return 1;
-  return floordiv(m, l);
-}
-
 // Stencil rows of the segment [A, A+G) in row (a1, a2): union column ranges, brackets,
 // staged union, per-cell sub-ranges.  All SG_NT threads of the block call it.  Returns
 // false (uniformly) if the union holds more than SG_CAP elements (caller shrinks G).
@@ -157,7 +150,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
     ecn[r] = 0u;
     if (r < nrows && tid < sm.r_n[r]) {
       const int col = sm.r_lo[r] + tid;
-      const int nx = fdiv_fast(col, l1);
+      const int nx = floordiv(col, l1);
       const uint32_t cell = (uint32_t)sm.r_base[r] + (uint32_t)(col - nx * l1);
       est[r] = cs[cell];
       ecn[r] = cs[cell + 1];
@@ -223,7 +216,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
       if (tt[r] < tot) {
         const int row = sm.e_row[ee[r]];
         const int col = sm.r_lo[row] + sm.e_ci[ee[r]];
-        const int nx = fdiv_fast(col, l1);
+        const int nx = floordiv(col, l1);
         const float bx = (float)(col - A) * wx + (float)nx * ex + sm.r_bf[row][0];
         sm.stage[tt[r]] = make_float4(pp[r].x + bx, pp[r].y + sm.r_bf[row][1], pp[r].z + sm.r_bf[row][2],
                                       __uint_as_float(jj[r]));
@@ -285,7 +278,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
       const uint32_t j = jj[h];
       const int row = sm.e_row[ee[h]];
       const int col = sm.r_lo[row] + sm.e_ci[ee[h]];
-      const int nx = fdiv_fast(col, l1);
+      const int nx = floordiv(col, l1);
       const double bx = (double)(col - A) * wx64 + (g.variant == 1 ? (double)nx * g.e[0] : 0.0) + sm.r_b[row][0];
       const double dx = (uj[h].x + bx) - uix, dy = (uj[h].y + sm.r_b[row][1]) - uiy,
                    dz = (uj[h].z + sm.r_b[row][2]) - uiz;

@@ -559,41 +559,23 @@ __device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32
   }
 }
 
-// Evaluate ONE queued survivor t of this lane (fp32 mode: fp64 rotated
-// cell-local coordinates; fp64 mode: exact lab-frame displacement).
+// NC_F64: evaluate ONE queued survivor t of this lane.  The filter already
+// applied the canonical membership test (R16); d is formed error-free in the lab
+// frame.  (NC_F32 uses eval_pairs_f32 / eval_close_f64.)
 template <typename T, bool DIGEST>
 __device__ __forceinline__ void eval_one(const Geom& g, const PairCtx<T>& pc, const K3Smem<T>& sm, Acc& acc,
                                          uint32_t t, double sig2, double eps24) {
-  if constexpr (sizeof(T) == 4) {
-    uint32_t j = w_to_idx(sm.stage[t].w);
-    double dx = sm.s64.x[t] - pc.ux, dy = sm.s64.y[t] - pc.uy, dz = sm.s64.z[t] - pc.uz;
-    double r2 = dx * dx + dy * dy + dz * dz;
-    bool ok = (j != pc.my) && (r2 < pc.hi64);
-    int n0 = 0, n1 = 0, n2 = 0;
-    if (ok && (DIGEST || r2 >= pc.lo64)) {
-      image_of<T>(g, sm, t, g.variant == 1 ? pc.nh[j] : 0u, pc.nh_i, n0, n1, n2);
-      if (r2 >= pc.lo64) {
-        ok = canonical_in<T>(g, pc.qs, pc.my, j, n0, n1, n2);
-        acc.nrc++;
-      }
-    }
-    if (ok) {
-      lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
-      digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
-    }
-  } else {
-    // fp64 mode: the filter already applied the canonical test; exact d for the force
-    typename V4<T>::t v = sm.stage[t];
-    uint32_t j = w_to_idx(v.w);
-    int n0, n1, n2;
-    image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
-    double dx = exact_d(g, 0, v.x, pc.ux, n0, n1, n2);
-    double dy = exact_d(g, 1, v.y, pc.uy, n0, n1, n2);
-    double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
-    double r2 = dx * dx + dy * dy + dz * dz;
-    lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
-    digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
-  }
+  static_assert(sizeof(T) == 8, "generic evaluation is the NC_F64 path");
+  typename V4<T>::t v = sm.stage[t];
+  uint32_t j = w_to_idx(v.w);
+  int n0, n1, n2;
+  image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
+  double dx = exact_d(g, 0, v.x, pc.ux, n0, n1, n2);
+  double dy = exact_d(g, 1, v.y, pc.uy, n0, n1, n2);
+  double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
+  double r2 = dx * dx + dy * dy + dz * dz;
+  lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
+  digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
 }
 
 // Evaluate the queued filter survivors of every lane (warp-uniform loop, two
@@ -609,20 +591,15 @@ __device__ __forceinline__ void eval_queue(const Geom& g, const PairCtx<T>& pc, 
   }
 }
 
-// One filter step for staged element t (valid lanes only): true if (i, t) may interact.
+// NC_F64 filter step for staged element t: the canonical fp64 membership test (R16).
 template <typename T>
 __device__ __forceinline__ bool filter_one(const Geom& g, const PairCtx<T>& pc, const K3Smem<T>& sm, uint32_t t) {
+  static_assert(sizeof(T) == 8, "generic filter is the NC_F64 path");
   typename V4<T>::t v = sm.stage[t];
-  if constexpr (sizeof(T) == 4) {
-    T dx = v.x - pc.fx, dy = v.y - pc.fy, dz = v.z - pc.fz;
-    T r2 = dx * dx + dy * dy + dz * dz;
-    return r2 < pc.hi;
-  } else {
-    int n0, n1, n2;
-    image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
-    double r2 = canonical_r2(g, v.x, v.y, v.z, pc.ux, pc.uy, pc.uz, n0, n1, n2);
-    return r2 < g.rc2 && w_to_idx(v.w) != pc.my;
-  }
+  int n0, n1, n2;
+  image_of<T>(g, sm, t, sm.s64.nh[t], pc.nh_i, n0, n1, n2);
+  double r2 = canonical_r2(g, v.x, v.y, v.z, pc.ux, pc.uy, pc.uz, n0, n1, n2);
+  return r2 < g.rc2 && w_to_idx(v.w) != pc.my;
 }
 
 __device__ __forceinline__ double shfl_comb(double x, int src, bool take) {
@@ -693,9 +670,6 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
   return (uint32_t)v;
-}
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
