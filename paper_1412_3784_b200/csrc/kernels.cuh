@@ -12,7 +12,7 @@
 //                           shared memory, filters r^2 < r_c^2 into per-lane
 //                           queues, evaluates LJ/WCA for the queued pairs,
 //                           full i-side accumulation, no atomics
-//   K3r k_reduce_layers   : deterministic fixed-order reduction of partials
+//   K3r k_reduce          : deterministic fixed-order reduction of partials (one launch)
 //   K4  k_kick_drift_key  : SLLOD half kick + flow factor + drift, fused with K1
 //       k_kick            : SLLOD flow factor + half kick
 //
@@ -264,6 +264,51 @@ __global__ void k_scan_apply(const uint32_t* __restrict__ in, int64_t m, const u
     run += v[k];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) out[m] = *tot;
+}
+
+// Small inputs (m <= SCAN_SMALL): the whole exclusive scan in one block, one launch instead of
+// three (C1's 24k cells, slab migration blocks, ...): rows of 1024 coalesced elements, each a
+// block scan, with a running carry.  out[m] = total.
+constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_R = 32, SCAN_SMALL = SCAN_SMALL_R * SCAN_SMALL_T;
+__global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __restrict__ in, int64_t m,
+                                                             uint32_t* __restrict__ out) {
+  __shared__ uint32_t wsum[SCAN_SMALL_T / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rows = (int)((m + SCAN_SMALL_T - 1) / SCAN_SMALL_T);
+  uint32_t v[SCAN_SMALL_R];
+#pragma unroll
+  for (int r = 0; r < SCAN_SMALL_R; ++r) {  // every load in flight before the first scan
+    const int64_t i = (int64_t)r * SCAN_SMALL_T + tid;
+    v[r] = (r < rows && i < m) ? in[i] : 0u;
+  }
+  uint32_t carry = 0;
+#pragma unroll
+  for (int r = 0; r < SCAN_SMALL_R; ++r) {
+    if (r >= rows) break;
+    uint32_t x = v[r];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      uint32_t w = wsum[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    const int64_t i = (int64_t)r * SCAN_SMALL_T + tid;
+    if (i < m) out[i] = carry + (wid > 0 ? wsum[wid - 1] : 0u) + x - v[r];
+    carry += wsum[31];
+    __syncthreads();  // wsum is rewritten by the next row
+  }
+  if (tid == 0) out[m] = carry;
 }
 
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
@@ -1148,35 +1193,52 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
 // tree), then the total in layer order.  Deterministic and layer-aligned, so
 // identical for any assignment of layers to devices.
 constexpr int K3R_T = 256;
-__global__ void __launch_bounds__(K3R_T) k_reduce_layers(const double* __restrict__ bpart, int bpl, int nlayers,
-                                                         double* __restrict__ lpart) {
-  __shared__ double red[K3R_T];
-  const int layer = blockIdx.x;
+// One launch: block l sums layer l's block partials (thread t takes blocks t, t+256, ... in order;
+// a fixed warp-shuffle tree, then the 8 warp sums in order), all NPART components at once; the last
+// block to finish (device-scope counter) sums the layers in layer order into tot and acc (acc[NPART]
+// counts evaluations) and re-arms the counter.  Deterministic: no order depends on timing.
+__global__ void __launch_bounds__(K3R_T) k_reduce(const double* __restrict__ bpart, int bpl, int nlayers,
+                                                  double* __restrict__ lpart, double* __restrict__ tot,
+                                                  double* __restrict__ acc, unsigned int* __restrict__ counter) {
+  __shared__ double wred[K3R_T / 32][NPART];
+  __shared__ bool last;
+  const int layer = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const double* base = bpart + (int64_t)layer * bpl * NPART;
+  double v[NPART];
+#pragma unroll
+  for (int c = 0; c < NPART; ++c) v[c] = 0.0;
+  for (int b = tid; b < bpl; b += K3R_T)
+#pragma unroll
+    for (int c = 0; c < NPART; ++c) v[c] += base[(int64_t)b * NPART + c];
+#pragma unroll
   for (int c = 0; c < NPART; ++c) {
-    double v = 0.0;
-    for (int b = threadIdx.x; b < bpl; b += K3R_T) v += base[(int64_t)b * NPART + c];
-    red[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = K3R_T / 2; o > 0; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) lpart[(int64_t)layer * NPART + c] = red[0];
-    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
   }
-}
-
-// total in layer order; also accumulates into acc[0..NPART) and counts evaluations in acc[NPART]
-__global__ void k_reduce_total(const double* __restrict__ lpart, int nlayers, double* __restrict__ tot,
-                               double* __restrict__ acc) {
-  int c = threadIdx.x;
-  if (c > NPART) return;
-  if (c == NPART) { acc[NPART] += 1.0; return; }
-  double v = 0;
-  for (int l = 0; l < nlayers; ++l) v += lpart[(int64_t)l * NPART + c];
-  tot[c] = v;
-  acc[c] += v;
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < NPART; ++c) wred[wid][c] = v[c];
+  __syncthreads();
+  if (tid < NPART) {
+    double s = 0.0;
+    for (int w = 0; w < K3R_T / 32; ++w) s += wred[w][tid];
+    lpart[(int64_t)layer * NPART + tid] = s;
+    __threadfence();
+  }
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(counter, 1u) == (unsigned)(nlayers - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < NPART) {
+    double s = 0.0;
+    for (int l = 0; l < nlayers; ++l) s += __ldcg(&lpart[(int64_t)l * NPART + tid]);
+    tot[tid] = s;
+    acc[tid] += s;
+  } else if (tid == NPART) {
+    acc[NPART] += 1.0;
+    *counter = 0u;
+  }
 }
 
 // neighborhood-size histogram (instrumentation): one warp per block

@@ -56,6 +56,7 @@ struct nc_ctx {
   uint32_t *gin = nullptr, *sidx = nullptr, *pbcnt = nullptr, *pboff = nullptr, *ptot = nullptr;
   uint8_t* cls = nullptr;
   double *bpart = nullptr, *lpart = nullptr, *part_tot = nullptr, *part_acc = nullptr;
+  unsigned int* rcount = nullptr;  // k_reduce's last-block counter (kept at 0 between launches)
   // digest
   uint32_t* dcnt = nullptr;
   uint64_t *dhs = nullptr, *dhx = nullptr;
@@ -202,6 +203,31 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   return NC_OK;
 }
 
+// exclusive scan of m counts into out[0..m] (out[m] = total); one launch for small m
+nc_status launch_scan_raw(nc_ctx* ctx, const uint32_t* in, int64_t m, uint32_t* out) {
+  cudaStream_t s = ctx->stream;
+  if (m <= SCAN_SMALL) {
+    k_scan_small<<<1, SCAN_SMALL_T, 0, s>>>(in, m, out);
+    LAUNCHED();
+  } else {
+    const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
+    k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(in, m, ctx->bsum);
+    LAUNCHED();
+    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
+    LAUNCHED();
+    k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, m, ctx->bsum, out, ctx->tot);
+    LAUNCHED();
+  }
+  return NC_OK;
+}
+nc_status launch_scan(nc_ctx* ctx, const uint32_t* in, int64_t m, uint32_t* out) {
+  prof_begin(ctx);
+  nc_status st = launch_scan_raw(ctx, in, m, out);
+  if (st) return st;
+  prof_end(ctx, NC_K_SCAN);
+  return NC_OK;
+}
+
 template <typename T>
 nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t* qwrap, int64_t n,
                        const uint32_t* gid_in, const typename V4<T>::t* p_in, typename V4<T>::t* q_out,
@@ -216,19 +242,10 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
     LAUNCHED();
     prof_end(ctx, NC_K_WRAPKEY);
   }
-  int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
-  prof_begin(ctx);
-  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
-  LAUNCHED();
-  prof_end(ctx, NC_K_SCAN);
-  prof_begin(ctx);
-  k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
-  LAUNCHED();
-  prof_end(ctx, NC_K_SCAN);
-  prof_begin(ctx);
-  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
-  LAUNCHED();
-  prof_end(ctx, NC_K_SCAN);
+  {
+    nc_status sst = launch_scan(ctx, ctx->counts, C, ctx->cs);
+    if (sst) return sst;
+  }
   if (n > 0) {
     prof_begin(ctx);
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, gid_in, ctx->tmp, ctx->tmpgid);
@@ -295,11 +312,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   prof_end(ctx, NC_K_PAIRS);
   int nl = nlay;
   prof_begin(ctx);
-  k_reduce_layers<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart);
-  LAUNCHED();
-  prof_end(ctx, NC_K_REDUCE);
-  prof_begin(ctx);
-  k_reduce_total<<<1, 32, 0, s>>>(ctx->lpart, nl, ctx->part_tot, ctx->part_acc);
+  k_reduce<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart, ctx->part_tot, ctx->part_acc, ctx->rcount);
   LAUNCHED();
   prof_end(ctx, NC_K_REDUCE);
   ctx->last_cpb = cpb;
@@ -475,19 +488,10 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
       prof_end(ctx, NC_K_WRAPKEY);
     }
     int64_t C = g.ncells;
-    int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
-    prof_begin(ctx);
-    k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
-    LAUNCHED();
-    prof_end(ctx, NC_K_SCAN);
-    prof_begin(ctx);
-    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
-    LAUNCHED();
-    prof_end(ctx, NC_K_SCAN);
-    prof_begin(ctx);
-    k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
-    LAUNCHED();
-    prof_end(ctx, NC_K_SCAN);
+    {
+      nc_status sst = launch_scan(ctx, ctx->counts, C, ctx->cs);
+      if (sst) return sst;
+    }
     if (n > 0) {
       prof_begin(ctx);
       k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->st_gid[c], ctx->tmp, ctx->tmpgid);
@@ -570,10 +574,8 @@ nc_status partition(nc_ctx* ctx, int64_t n, const T* q, const T* p, const uint32
     k_class_count<<<(unsigned)nb, PART_T, 0, s>>>(n, nb, ctx->cls, ctx->pbcnt);
     LAUNCHED();
     const int64_t m = 4 * nb;
-    const int64_t sb = (m + SCAN_TILE - 1) / SCAN_TILE;
-    k_scan_reduce<<<(unsigned)sb, SCAN_T, 0, s>>>(ctx->pbcnt, m, ctx->bsum);
-    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, sb, ctx->tot);
-    k_scan_apply<<<(unsigned)sb, SCAN_T, 0, s>>>(ctx->pbcnt, m, ctx->bsum, ctx->pboff, ctx->tot);
+    nc_status sst = launch_scan_raw(ctx, ctx->pbcnt, m, ctx->pboff);
+    if (sst) return sst;
     k_class_totals<<<1, 32, 0, s>>>(ctx->pboff, nb, ctx->ptot);
     LAUNCHED();
     k_class_scatter<T><<<(unsigned)nb, PART_T, 0, s>>>(n, ctx->cls, ctx->pboff, q, p, gid, q0, p0, g0, r1, r2, words);
@@ -609,13 +611,10 @@ nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_
                                                     ctx->key, ctx->slot, ctx->counts, g);
   LAUNCHED();
   prof_end(ctx, NC_K_WRAPKEY);
-  int64_t nb = (C + SCAN_TILE - 1) / SCAN_TILE;
-  prof_begin(ctx);
-  k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum);
-  k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
-  k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(ctx->counts, C, ctx->bsum, ctx->cs, ctx->tot);
-  LAUNCHED();
-  prof_end(ctx, NC_K_SCAN);
+  {
+    nc_status sst = launch_scan(ctx, ctx->counts, C, ctx->cs);
+    if (sst) return sst;
+  }
   if (n > 0) {
     prof_begin(ctx);
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp, ctx->tmpgid);
@@ -740,6 +739,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {(void**)&ctx->bpart, sizeof(double) * NPART * (size_t)ctx->max_blocks},
       {(void**)&ctx->lpart, sizeof(double) * NPART * (size_t)ctx->max_layers},
       {(void**)&ctx->part_tot, sizeof(double) * NPART}, {(void**)&ctx->part_acc, sizeof(double) * (NPART + 1)},
+      {(void**)&ctx->rcount, 16},
       {(void**)&ctx->dcnt, 4 * N_}, {(void**)&ctx->dhs, 8 * N_}, {(void**)&ctx->dhx, 8 * N_},
       {(void**)&ctx->hist, 8 * 64},
       {(void**)&ctx->gin, 4 * N_}, {(void**)&ctx->sidx, 4 * N_}, {(void**)&ctx->cls, N_},
@@ -756,6 +756,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
     }
   }
   e = cudaMemset(ctx->part_acc, 0, sizeof(double) * (NPART + 1));
+  if (e == cudaSuccess) e = cudaMemset(ctx->rcount, 0, 16);
   if (e != cudaSuccess) {
     nc_destroy(ctx);
     return fail(nullptr, NC_E_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
@@ -1121,7 +1122,7 @@ nc_status nc_slab_kick(nc_ctx* ctx, void* p, const void* F, int64_t n, double dt
 
 nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* U, double W[6], double stats[4]) {
   if (!ctx || !parts || nlayers < 1) return fail(ctx, NC_E_ARG, "null argument");
-  // the same fixed-order sum as k_reduce_total, then the same frame rotation as a single-device evaluation
+  // the same fixed-order layer sum as k_reduce, then the same frame rotation as a single-device evaluation
   for (int c = 0; c < NPART; ++c) {
     double v = 0;
     for (int l = 0; l < nlayers; ++l) v += parts[(int64_t)l * NPART + c];
