@@ -386,6 +386,23 @@ typedef uint32_t K3QT;
 #else
 typedef uint16_t K3QT;
 #endif
+#ifndef K3_MASK
+#define K3_MASK 1  // fp32 filter records hits as bits of per-lane 32-step mask words (no per-candidate store)
+#endif
+#ifndef K3_DOT
+#define K3_DOT 0   // mask filter in the dot form: r^2 - |u|^2 = |v|^2 - 2 u.v (4 LDS.32 + 3 FFMA per candidate)
+#endif
+#ifndef K3_PACK
+#define K3_PACK 1  // difference-form mask filter on packed fp32x2 (two candidates per FADD2/FFMA2)
+#endif
+#ifndef K3_PACKE
+#define K3_PACKE 1  // mask evaluation two hits per iteration on packed fp32x2
+#endif
+#if K3_DOT && !K3_MASK
+#error "K3_DOT needs K3_MASK"
+#endif
+constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 filter steps of one chunk
+constexpr int K3_CQ = 24;   // close-tier queue entries per lane (mask mode); flushed when nearly full
 constexpr uint32_t K3_QSTRIDE = 32u * sizeof(K3QT);  // bytes between consecutive entries of one lane
 constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
 constexpr int K3_UNROLL = 8;    // filter candidates per lane between queue-full votes
@@ -397,6 +414,9 @@ constexpr double K3_BAND64 = 1e-12;
 template <typename T>
 struct K3Stage64 {  // fp32 mode: staged x, y, z (image bracket applied) as separate arrays, entry brackets
   float sx[K3_STAGE], sy[K3_STAGE], sz[K3_STAGE];
+#if K3_DOT
+  float sw[K3_STAGE];  // |v|^2 of each staged element (dot-form filter)
+#endif
   float Bf[K3_MAXE][3];
 };
 template <>
@@ -408,7 +428,8 @@ template <typename T>
 struct K3Smem {
   typename V4<T>::t stage[sizeof(T) == 8 ? K3_STAGE : 1];  // fp64 mode: staged lab positions, .w = sorted index
   K3Stage64<T> s64;
-  K3QT queue[K3_QCAP][32];
+  K3QT queue[(sizeof(T) == 4 && K3_MASK) ? K3_CQ : K3_QCAP][32];
+  uint32_t mq[(sizeof(T) == 4 && K3_MASK) ? K3_MW : 1][32];  // fp32 mask mode: hit words mq[w][lane]
   uint8_t sent[K3_STAGE];
   uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
   int32_t e_n[K3_MAXE][3];
@@ -754,10 +775,45 @@ __device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) {
 // fp32 staging is three float arrays (sx, sy, sz): a broadcast LDS.32 is one shared-memory
 // wavefront, a 16-byte LDS.128 four (the filter is bound by the shared-memory pipe)
 constexpr uint32_t K3_YOFF = 4u * K3_STAGE, K3_ZOFF = 8u * K3_STAGE;  // bytes from sx to sy, sz
+constexpr uint32_t K3_WOFF = 12u * K3_STAGE;                          // bytes from sx to sw (K3_DOT)
 __device__ __forceinline__ float ldsf(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
+}
+
+// packed fp32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2, round-to-nearest like the scalar ops)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t ldsu(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void stsu(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
 // fp32 accumulators of the far-pair tier (folded into the fp64 Acc after each evaluation)
@@ -877,6 +933,7 @@ __device__ __forceinline__ void eval_pairs_f32(K3QT (*queue)[32], const Geom& g,
   eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, queue);
 }
 
+#if !K3_MASK
 template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                  Acc32& a32, int s, int S, int iters, int lane,
@@ -928,6 +985,245 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     if (it >= iters) break;
   }
 }
+#endif
+
+#if K3_MASK
+// Far-tier evaluation straight from the hit masks: each lane pops its hits (words in order, bits
+// from the top), evaluates far pairs in fp32 and compacts the rest into the close queue, which is
+// handed to the fp64 tier whenever some lane's queue is nearly full, and at the end.
+template <bool DIGEST>
+__device__ __forceinline__ void eval_masks_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                               Acc32& a32, int qits, int nhit, int nw, uint32_t sa0, uint32_t step,
+                                               int lane, uint32_t stage0, const double4* __restrict__ u64) {
+  // qits = this lane's hits + empty words (an empty word costs one idle iteration)
+  const int qmax = __reduce_max_sync(0xffffffffu, qits);
+  const float split2 = g.f_split2, lo32 = g.f_lo, sig2 = g.f_sig2, eps24 = -g.f_m24;
+  const uint32_t wstep = 32u * step;  // bytes of staged elements covered by one mask word
+  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
+  const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
+  uint32_t cur = nw > 0 ? ldsu(mq0) : 0u, wa = sa0, wq = mq0 + 128u, wend = mq0 + 128u * (uint32_t)nw;
+  uint32_t qc = qc0;  // next close-queue slot
+  int nclose_all = 0;
+  for (int k = 0; k < qmax; ++k) {
+    const bool valid = cur != 0;
+    uint32_t b;
+    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));  // highest hit of the word (0xffffffff if none)
+    b = valid ? b : 0u;                              // idle lanes read step 0 of their word: finite, masked
+    cur ^= valid ? (1u << b) : 0u;
+    const uint32_t a = wa + step * b;
+    if (cur == 0 && wq < wend) {  // next word (one predicated load, no loop)
+      cur = ldsu(wq);
+      wq += 128u;
+      wa += wstep;
+    }
+    const float vx = ldsf(a), vy = ldsf(a + K3_YOFF), vz = ldsf(a + K3_ZOFF);
+    const float dx = vx - pc.fx, dy = vy - pc.fy, dz = vz - pc.fz;
+    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    const bool far = !DIGEST && r2 >= split2 && r2 < lo32;
+    stsq(qc, a);
+    qc += (valid && !far) ? K3_QSTRIDE : 0u;
+    float ir2;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
+    ir2 = (valid && far) ? ir2 : 0.0f;  // one mask zeroes s6, fr and the energy term
+    const float s2 = sig2 * ir2;
+    const float s6 = s2 * s2 * s2;
+    const float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
+    const float tx = fr * dx, ty = fr * dy, tz = fr * dz;
+    a32.fx -= tx; a32.fy -= ty; a32.fz -= tz;
+    a32.u = fmaf(s6, s6, a32.u - s6);
+    a32.w0 = fmaf(tx, dx, a32.w0); a32.w1 = fmaf(ty, dy, a32.w1); a32.w2 = fmaf(tz, dz, a32.w2);
+    a32.w3 = fmaf(tx, dy, a32.w3); a32.w4 = fmaf(tx, dz, a32.w4); a32.w5 = fmaf(ty, dz, a32.w5);
+    if ((k & 7) == 7 && __any_sync(0xffffffffu, qc > qclim)) {
+      __syncwarp();
+      const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
+      eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
+      __syncwarp();
+      nclose_all += nclose;
+      qc = qc0;
+    }
+  }
+  __syncwarp();
+  const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
+  a32.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
+  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
+}
+
+#if K3_PACK
+// pop this lane's next hit (highest bit of the current word) and refill the word when it empties
+__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step,
+                                            uint32_t wstep, bool& valid) {
+  valid = cur != 0;
+  uint32_t b;
+  asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));
+  b = valid ? b : 0u;  // idle lanes read step 0 of their word: finite, masked
+  cur ^= valid ? (1u << b) : 0u;
+  const uint32_t a = wa + step * b;
+  if (cur == 0 && wq < wend) {
+    cur = ldsu(wq);
+    wq += 128u;
+    wa += wstep;
+  }
+  return a;
+}
+
+// Two hits per iteration: the far-tier math runs on packed fp32x2 (FADD2/FMUL2/FFMA2) with packed
+// accumulators, folded into the fp64 Acc once per chunk.
+template <bool DIGEST>
+__device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                                 int qits, int nhit, int nw, uint32_t sa0, uint32_t step, int lane,
+                                                 uint32_t stage0, const double4* __restrict__ u64) {
+  const int qmax = __reduce_max_sync(0xffffffffu, qits);
+  const float split2 = g.f_split2, lo32 = g.f_lo;
+  const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
+  const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), EPS24 = pk2(-g.f_m24, -g.f_m24), TWO = pk2(2.0f, 2.0f),
+                 NEG1 = pk2(-1.0f, -1.0f);
+  const uint32_t wstep = 32u * step;
+  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
+  const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
+  uint32_t cur = nw > 0 ? ldsu(mq0) : 0u, wa = sa0, wq = mq0 + 128u, wend = mq0 + 128u * (uint32_t)nw;
+  uint32_t qc = qc0;
+  int nclose_all = 0;
+  uint64_t Fx = 0, Fy = 0, Fz = 0, Uq = 0, W0 = 0, W1 = 0, W2 = 0, W3 = 0, W4 = 0, W5 = 0;  // packed partial sums
+  for (int k = 0; k < qmax; k += 2) {
+    bool va, vb;
+    const uint32_t aa = pop_hit(cur, wa, wq, wend, step, wstep, va);
+    const uint32_t ab = pop_hit(cur, wa, wq, wend, step, wstep, vb);
+    const uint64_t DX = add2(pk2(ldsf(aa), ldsf(ab)), nfx), DY = add2(pk2(ldsf(aa + K3_YOFF), ldsf(ab + K3_YOFF)), nfy),
+                   DZ = add2(pk2(ldsf(aa + K3_ZOFF), ldsf(ab + K3_ZOFF)), nfz);
+    float r2a, r2b;
+    upk2(fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX))), r2a, r2b);
+    const bool fa = !DIGEST && r2a >= split2 && r2a < lo32, fb = !DIGEST && r2b >= split2 && r2b < lo32;
+    stsq(qc, aa);
+    qc += (va && !fa) ? K3_QSTRIDE : 0u;
+    stsq(qc, ab);
+    qc += (vb && !fb) ? K3_QSTRIDE : 0u;
+    float ia, ib;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(r2a));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(r2b));
+    const uint64_t IR = pk2((va && fa) ? ia : 0.0f, (vb && fb) ? ib : 0.0f);  // one mask per pair
+    const uint64_t S2 = mul2(SIG2, IR);
+    const uint64_t S6 = mul2(mul2(S2, S2), S2);
+    const uint64_t FR = mul2(mul2(mul2(EPS24, S6), fma2(TWO, S6, NEG1)), IR);
+    const uint64_t TX = mul2(FR, DX), TY = mul2(FR, DY), TZ = mul2(FR, DZ);
+    Fx = add2(Fx, TX); Fy = add2(Fy, TY); Fz = add2(Fz, TZ);
+    Uq = fma2(S6, add2(S6, NEG1), Uq);
+    W0 = fma2(TX, DX, W0); W1 = fma2(TY, DY, W1); W2 = fma2(TZ, DZ, W2);
+    W3 = fma2(TX, DY, W3); W4 = fma2(TX, DZ, W4); W5 = fma2(TY, DZ, W5);
+    if ((k & 6) == 6 && __any_sync(0xffffffffu, qc > qclim)) {  // every 8 hits
+      __syncwarp();
+      const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
+      eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
+      __syncwarp();
+      nclose_all += nclose;
+      qc = qc0;
+    }
+  }
+  auto fold = [](uint64_t v) { float a, b; upk2(v, a, b); return (double)a + (double)b; };
+  acc.fx -= fold(Fx); acc.fy -= fold(Fy); acc.fz -= fold(Fz); acc.u += fold(Uq);
+  acc.w0 += fold(W0); acc.w1 += fold(W1); acc.w2 += fold(W2);
+  acc.w3 += fold(W3); acc.w4 += fold(W4); acc.w5 += fold(W5);
+  __syncwarp();
+  const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
+  acc.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
+  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
+}
+#endif
+
+// Mask filter: lane (i, s) tests staged elements s, s+S, ... in blocks of 32 steps; hit k of a
+// block sets bit k of a register word (FSETP + predicated LOP3: no shared-memory store per
+// candidate); one STS.32 per block.  K3_MW words hold a whole chunk, so the evaluation runs once.
+template <bool DIGEST>
+__device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                                 Acc32& a32, int s, int S, int iters, int lane,
+                                                 const double4* __restrict__ u64) {
+  static_assert(32 * K3_MW >= K3_CAP + 32, "mask words must cover one chunk");
+  const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
+  const uint32_t step = 4u * (uint32_t)S;
+#if K3_DOT
+  const float m2x = pc.m2x, m2y = pc.m2y, m2z = pc.m2z, thr = pc.hi - pc.uu;  // -inf for ghost lanes
+#else
+  const float fx = pc.fx, fy = pc.fy, fz = pc.fz, hi = pc.hi;
+#if K3_PACK
+  const uint64_t nfx = pk2(-fx, -fx), nfy = pk2(-fy, -fy), nfz = pk2(-fz, -fz);
+#endif
+#endif
+  const uint32_t sa0 = stage0 + 4u * (uint32_t)s;
+  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
+  uint32_t sa = sa0;
+  int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation iterations this lane needs)
+  const int nfull = iters >> 5;
+  for (; w < nfull; ++w) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int g8 = 0; g8 < 32; g8 += K3_UNROLL) {
+      float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
+#if K3_DOT
+      float vw[K3_UNROLL];
+#endif
+#pragma unroll
+      for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
+        vx[k] = ldsf(sa + step * k);
+        vy[k] = ldsf(sa + step * k + K3_YOFF);
+        vz[k] = ldsf(sa + step * k + K3_ZOFF);
+#if K3_DOT
+        vw[k] = ldsf(sa + step * k + K3_WOFF);
+#endif
+      }
+#pragma unroll
+      for (int k = 0; k < K3_UNROLL; ++k) {
+#if K3_DOT
+        const float t = fmaf(m2z, vz[k], fmaf(m2y, vy[k], fmaf(m2x, vx[k], vw[k])));
+        m |= (t < thr) ? (1u << (g8 + k)) : 0u;
+#elif K3_PACK
+        if (k & 1) continue;
+        // two candidates per packed op (FADD2/FMUL2/FFMA2: same rounding as the scalar form)
+        const uint64_t dx = add2(pk2(vx[k], vx[k + 1]), nfx), dy = add2(pk2(vy[k], vy[k + 1]), nfy),
+                       dz = add2(pk2(vz[k], vz[k + 1]), nfz);
+        float r2a, r2b;
+        upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
+        m |= (r2a < hi) ? (1u << (g8 + k)) : 0u;
+        m |= (r2b < hi) ? (1u << (g8 + k + 1)) : 0u;
+#else
+        const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        m |= (r2 < hi) ? (1u << (g8 + k)) : 0u;
+#endif
+      }
+      sa += step * K3_UNROLL;
+    }
+    stsu(mq0 + 128u * (uint32_t)w, m);
+    const int c = __popc(m);
+    nhit += c;
+    qlen += c ? c : 1;
+  }
+  const int rem = iters & 31;
+  if (rem) {
+    uint32_t m = 0;
+    for (int k = 0; k < rem; ++k) {
+#if K3_DOT
+      const float t = fmaf(m2z, ldsf(sa + K3_ZOFF), fmaf(m2y, ldsf(sa + K3_YOFF), fmaf(m2x, ldsf(sa), ldsf(sa + K3_WOFF))));
+      m |= (t < thr) ? (1u << k) : 0u;
+#else
+      const float dx = ldsf(sa) - fx, dy = ldsf(sa + K3_YOFF) - fy, dz = ldsf(sa + K3_ZOFF) - fz;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      m |= (r2 < hi) ? (1u << k) : 0u;
+#endif
+      sa += step;
+    }
+    stsu(mq0 + 128u * (uint32_t)w, m);
+    const int c = __popc(m);
+    nhit += c;
+    qlen += c ? c : 1;
+    ++w;
+  }
+  __syncwarp();
+#if K3_PACK && K3_PACKE
+  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step, lane, stage0, u64);
+#else
+  eval_masks_f32<DIGEST>(g, pc, sm, acc, a32, qlen, nhit, w, sa0, step, lane, stage0, u64);
+#endif
+}
+#endif
 
 // One warp per block; each warp handles K3_CELLS consecutive cells of one
 // cell layer, so block partials are layer-aligned and their fixed-order sums
@@ -964,6 +1260,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
     if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
       sm.s64.sx[K3_DUMMY] = sm.s64.sy[K3_DUMMY] = sm.s64.sz[K3_DUMMY] = 1e30f;
+#if K3_DOT
+      sm.s64.sw[K3_DUMMY] = __int_as_float(0x7f800000);
+#endif
       sm.sent[K3_DUMMY] = K3_MAXE - 1;
       sm.e_B[K3_MAXE - 1][0] = 1e150; sm.e_B[K3_MAXE - 1][1] = 1e150; sm.e_B[K3_MAXE - 1][2] = 1e150;
     }
@@ -1078,6 +1377,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
                 sm.s64.sx[tt[r]] = x;
                 sm.s64.sy[tt[r]] = y;
                 sm.s64.sz[tt[r]] = z;
+#if K3_DOT
+                sm.s64.sw[tt[r]] = fmaf(z, z, fmaf(y, y, x * x));
+#endif
               }
             }
           }
@@ -1104,6 +1406,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             sm.s64.nh[ctot + lane] = 0u;
           } else {
             sm.s64.sx[ctot + lane] = sm.s64.sy[ctot + lane] = sm.s64.sz[ctot + lane] = 1e30f;
+#if K3_DOT
+            sm.s64.sw[ctot + lane] = __int_as_float(0x7f800000);  // +inf: never below any threshold
+#endif
           }
           sm.sent[ctot + lane] = 0;
         }
