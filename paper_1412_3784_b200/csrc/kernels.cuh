@@ -395,6 +395,9 @@ typedef uint16_t K3QT;
 #ifndef K3_PACK
 #define K3_PACK 1  // difference-form mask filter on packed fp32x2 (two candidates per FADD2/FFMA2)
 #endif
+#ifndef K3_STGR
+#define K3_STGR 4  // staging: global loads in flight per lane
+#endif
 #ifndef K3_PACKE
 #define K3_PACKE 1  // mask evaluation two hits per iteration on packed fp32x2
 #endif
@@ -405,7 +408,10 @@ constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 fi
 constexpr int K3_CQ = 24;   // close-tier queue entries per lane (mask mode); flushed when nearly full
 constexpr uint32_t K3_QSTRIDE = 32u * sizeof(K3QT);  // bytes between consecutive entries of one lane
 constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
-constexpr int K3_UNROLL = 8;    // filter candidates per lane between queue-full votes
+#ifndef K3_UNROLL_OVR
+#define K3_UNROLL_OVR 8
+#endif
+constexpr int K3_UNROLL = K3_UNROLL_OVR;  // filter steps per group (loads of a group issued together)
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
 constexpr int K3_CELLS = 4;     // cells per warp (= per block: one warp per block)
 constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, nonfinite
@@ -845,14 +851,8 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
   const int qmax = __reduce_max_sync(0xffffffffu, qlen);
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   const uint32_t dummy = stage0 + 4u * K3_DUMMY;
-  for (int k = 0; k < qmax; k += 2) {
-    const uint32_t aa = k < qlen ? qaddr(queue[k][lane], stage0) : dummy;
-    const uint32_t ab = k + 1 < qlen ? qaddr(queue[k + 1][lane], stage0) : dummy;
-    const uint32_t ta = (aa - stage0) >> 2, tb = (ab - stage0) >> 2;
-    const uint32_t ja = k < qlen ? sidx_of(sm, ta, pc.base_off) : pc.my;
-    const uint32_t jb = k + 1 < qlen ? sidx_of(sm, tb, pc.base_off) : pc.my;
-    const int ea = sm.sent[ta], eb = sm.sent[tb];
-    const double4 pa = u64[ja], pb = u64[jb];
+  auto pair2 = [&](uint32_t ta, uint32_t tb, uint32_t ja, uint32_t jb, int ea, int eb, const double4& pa,
+                   const double4& pb) {
     const double dxa = (pa.x + sm.e_B[ea][0]) - pc.ux, dya = (pa.y + sm.e_B[ea][1]) - pc.uy,
                  dza = (pa.z + sm.e_B[ea][2]) - pc.uz;
     const double dxb = (pb.x + sm.e_B[eb][0]) - pc.ux, dyb = (pb.y + sm.e_B[eb][1]) - pc.uy,
@@ -890,6 +890,20 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
       if (oka) digest_add<DIGEST>(acc, pc.gid, ja, na0, na1, na2);
       if (okb) digest_add<DIGEST>(acc, pc.gid, jb, nb0, nb1, nb2);
     }
+  };
+  // queue entry k of this lane -> staged index t, sorted index j (pc.my + dummy for none), entry e
+  auto item = [&](int k, uint32_t& t, uint32_t& j, int& e) {
+    const uint32_t a = k < qlen ? qaddr(queue[k][lane], stage0) : dummy;
+    t = (a - stage0) >> 2;
+    j = k < qlen ? sidx_of(sm, t, pc.base_off) : pc.my;
+    e = sm.sent[t];
+  };
+  for (int k = 0; k < qmax; k += 2) {
+    uint32_t ta, tb, ja, jb;
+    int ea, eb;
+    item(k, ta, ja, ea); item(k + 1, tb, jb, eb);
+    const double4 pa = u64[ja], pb = u64[jb];
+    pair2(ta, tb, ja, jb, ea, eb, pa, pb);
   }
 }
 
@@ -1356,13 +1370,13 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             }
           }
           __syncwarp();
-          // four elements per lane in flight: all index lookups and loads first, then the stores
-          for (uint32_t t0 = 0; t0 < ctot; t0 += 128) {
-            uint32_t tt[4], jj[4];
-            int ee[4];
-            float4 pp[4];
+          // K3_STGR elements per lane in flight: all index lookups and loads first, then the stores
+          for (uint32_t t0 = 0; t0 < ctot; t0 += 32 * K3_STGR) {
+            uint32_t tt[K3_STGR], jj[K3_STGR];
+            int ee[K3_STGR];
+            float4 pp[K3_STGR];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < K3_STGR; ++r) {
               tt[r] = t0 + 32u * r + lane;
               const bool v = tt[r] < ctot;
               ee[r] = v ? sm.sent[tt[r]] : e0;
@@ -1370,7 +1384,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
               pp[r] = v ? u32[jj[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < K3_STGR; ++r) {
               if (tt[r] < ctot) {
                 const float x = pp[r].x + sm.s64.Bf[ee[r]][0], y = pp[r].y + sm.s64.Bf[ee[r]][1],
                             z = pp[r].z + sm.s64.Bf[ee[r]][2];
