@@ -389,9 +389,6 @@ typedef uint16_t K3QT;
 #ifndef K3_MASK
 #define K3_MASK 1  // fp32 filter records hits as bits of per-lane 32-step mask words (no per-candidate store)
 #endif
-#ifndef K3_DOT
-#define K3_DOT 0   // mask filter in the dot form: r^2 - |u|^2 = |v|^2 - 2 u.v (4 LDS.32 + 3 FFMA per candidate)
-#endif
 #ifndef K3_PACK
 #define K3_PACK 1  // difference-form mask filter on packed fp32x2 (two candidates per FADD2/FFMA2)
 #endif
@@ -400,9 +397,6 @@ typedef uint16_t K3QT;
 #endif
 #ifndef K3_PACKE
 #define K3_PACKE 1  // mask evaluation two hits per iteration on packed fp32x2
-#endif
-#if K3_DOT && !K3_MASK
-#error "K3_DOT needs K3_MASK"
 #endif
 constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 filter steps of one chunk
 constexpr int K3_CQ = 24;   // close-tier queue entries per lane (mask mode); flushed when nearly full
@@ -420,9 +414,6 @@ constexpr double K3_BAND64 = 1e-12;
 template <typename T>
 struct K3Stage64 {  // fp32 mode: staged x, y, z (image bracket applied) as separate arrays, entry brackets
   float sx[K3_STAGE], sy[K3_STAGE], sz[K3_STAGE];
-#if K3_DOT
-  float sw[K3_STAGE];  // |v|^2 of each staged element (dot-form filter)
-#endif
   float Bf[K3_MAXE][3];
 };
 template <>
@@ -781,7 +772,6 @@ __device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) {
 // fp32 staging is three float arrays (sx, sy, sz): a broadcast LDS.32 is one shared-memory
 // wavefront, a 16-byte LDS.128 four (the filter is bound by the shared-memory pipe)
 constexpr uint32_t K3_YOFF = 4u * K3_STAGE, K3_ZOFF = 8u * K3_STAGE;  // bytes from sx to sy, sz
-constexpr uint32_t K3_WOFF = 12u * K3_STAGE;                          // bytes from sx to sw (K3_DOT)
 __device__ __forceinline__ float ldsf(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -1153,56 +1143,49 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
   static_assert(32 * K3_MW >= K3_CAP + 32, "mask words must cover one chunk");
   const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
   const uint32_t step = 4u * (uint32_t)S;
-#if K3_DOT
-  const float m2x = pc.m2x, m2y = pc.m2y, m2z = pc.m2z, thr = pc.hi - pc.uu;  // -inf for ghost lanes
-#else
   const float fx = pc.fx, fy = pc.fy, fz = pc.fz, hi = pc.hi;
 #if K3_PACK
   const uint64_t nfx = pk2(-fx, -fx), nfy = pk2(-fy, -fy), nfz = pk2(-fz, -fz);
-#endif
 #endif
   const uint32_t sa0 = stage0 + 4u * (uint32_t)s;
   const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
   uint32_t sa = sa0;
   int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation iterations this lane needs)
   const int nfull = iters >> 5;
+  // one group of K3_UNROLL steps from staged address sa: hit k sets bit sh + k
+  auto group = [&](uint32_t sa, int sh) -> uint32_t {
+    float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
+#pragma unroll
+    for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
+      vx[k] = ldsf(sa + step * k);
+      vy[k] = ldsf(sa + step * k + K3_YOFF);
+      vz[k] = ldsf(sa + step * k + K3_ZOFF);
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < K3_UNROLL; ++k) {
+#if K3_PACK
+      if (k & 1) continue;
+      // two candidates per packed op (FADD2/FMUL2/FFMA2: same rounding as the scalar form)
+      const uint64_t dx = add2(pk2(vx[k], vx[k + 1]), nfx), dy = add2(pk2(vy[k], vy[k + 1]), nfy),
+                     dz = add2(pk2(vz[k], vz[k + 1]), nfz);
+      float r2a, r2b;
+      upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
+      m |= (r2a < hi) ? (1u << (sh + k)) : 0u;
+      m |= (r2b < hi) ? (1u << (sh + k + 1)) : 0u;
+#else
+      const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
+      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+      m |= (r2 < hi) ? (1u << (sh + k)) : 0u;
+#endif
+    }
+    return m;
+  };
   for (; w < nfull; ++w) {
     uint32_t m = 0;
 #pragma unroll
     for (int g8 = 0; g8 < 32; g8 += K3_UNROLL) {
-      float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
-#if K3_DOT
-      float vw[K3_UNROLL];
-#endif
-#pragma unroll
-      for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
-        vx[k] = ldsf(sa + step * k);
-        vy[k] = ldsf(sa + step * k + K3_YOFF);
-        vz[k] = ldsf(sa + step * k + K3_ZOFF);
-#if K3_DOT
-        vw[k] = ldsf(sa + step * k + K3_WOFF);
-#endif
-      }
-#pragma unroll
-      for (int k = 0; k < K3_UNROLL; ++k) {
-#if K3_DOT
-        const float t = fmaf(m2z, vz[k], fmaf(m2y, vy[k], fmaf(m2x, vx[k], vw[k])));
-        m |= (t < thr) ? (1u << (g8 + k)) : 0u;
-#elif K3_PACK
-        if (k & 1) continue;
-        // two candidates per packed op (FADD2/FMUL2/FFMA2: same rounding as the scalar form)
-        const uint64_t dx = add2(pk2(vx[k], vx[k + 1]), nfx), dy = add2(pk2(vy[k], vy[k + 1]), nfy),
-                       dz = add2(pk2(vz[k], vz[k + 1]), nfz);
-        float r2a, r2b;
-        upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
-        m |= (r2a < hi) ? (1u << (g8 + k)) : 0u;
-        m |= (r2b < hi) ? (1u << (g8 + k + 1)) : 0u;
-#else
-        const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        m |= (r2 < hi) ? (1u << (g8 + k)) : 0u;
-#endif
-      }
+      m |= group(sa, g8);
       sa += step * K3_UNROLL;
     }
     stsu(mq0 + 128u * (uint32_t)w, m);
@@ -1211,17 +1194,17 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     qlen += c ? c : 1;
   }
   const int rem = iters & 31;
-  if (rem) {
+  if (rem) {  // last word: whole groups, then single steps
     uint32_t m = 0;
-    for (int k = 0; k < rem; ++k) {
-#if K3_DOT
-      const float t = fmaf(m2z, ldsf(sa + K3_ZOFF), fmaf(m2y, ldsf(sa + K3_YOFF), fmaf(m2x, ldsf(sa), ldsf(sa + K3_WOFF))));
-      m |= (t < thr) ? (1u << k) : 0u;
-#else
+    int k = 0;
+    for (; k + K3_UNROLL <= rem; k += K3_UNROLL) {
+      m |= group(sa, 0) << k;
+      sa += step * K3_UNROLL;
+    }
+    for (; k < rem; ++k) {
       const float dx = ldsf(sa) - fx, dy = ldsf(sa + K3_YOFF) - fy, dz = ldsf(sa + K3_ZOFF) - fz;
       const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
       m |= (r2 < hi) ? (1u << k) : 0u;
-#endif
       sa += step;
     }
     stsu(mq0 + 128u * (uint32_t)w, m);
@@ -1274,9 +1257,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
     if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
       sm.s64.sx[K3_DUMMY] = sm.s64.sy[K3_DUMMY] = sm.s64.sz[K3_DUMMY] = 1e30f;
-#if K3_DOT
-      sm.s64.sw[K3_DUMMY] = __int_as_float(0x7f800000);
-#endif
       sm.sent[K3_DUMMY] = K3_MAXE - 1;
       sm.e_B[K3_MAXE - 1][0] = 1e150; sm.e_B[K3_MAXE - 1][1] = 1e150; sm.e_B[K3_MAXE - 1][2] = 1e150;
     }
@@ -1391,9 +1371,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
                 sm.s64.sx[tt[r]] = x;
                 sm.s64.sy[tt[r]] = y;
                 sm.s64.sz[tt[r]] = z;
-#if K3_DOT
-                sm.s64.sw[tt[r]] = fmaf(z, z, fmaf(y, y, x * x));
-#endif
               }
             }
           }
@@ -1420,9 +1397,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             sm.s64.nh[ctot + lane] = 0u;
           } else {
             sm.s64.sx[ctot + lane] = sm.s64.sy[ctot + lane] = sm.s64.sz[ctot + lane] = 1e30f;
-#if K3_DOT
-            sm.s64.sw[ctot + lane] = __int_as_float(0x7f800000);  // +inf: never below any threshold
-#endif
           }
           sm.sent[ctot + lane] = 0;
         }
