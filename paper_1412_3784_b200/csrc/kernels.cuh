@@ -370,8 +370,8 @@ __global__ void k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const
 // 1e-12 relative band around r_c^2 by the canonical fp64 test of R16.
 // ---------------------------------------------------------------------------
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
-constexpr int K3_DUMMY = K3_CAP + 32;  // permanent far element (padding slot of the evaluation)
-constexpr int K3_STAGE = K3_CAP + 33;  // + up to S far sentinels so the filter needs no bounds checks
+constexpr int K3_DUMMY = K3_CAP + 64;  // permanent far element (padding slot of the evaluation)
+constexpr int K3_STAGE = K3_CAP + 66;  // + up to 2S far sentinels so the filter needs no bounds checks (even: 8-byte pairs)
 #ifndef K3_QCAP_OVR
 #define K3_QCAP_OVR 48
 #endif
@@ -389,14 +389,8 @@ typedef uint16_t K3QT;
 #ifndef K3_MASK
 #define K3_MASK 1  // fp32 filter records hits as bits of per-lane 32-step mask words (no per-candidate store)
 #endif
-#ifndef K3_PACK
-#define K3_PACK 1  // difference-form mask filter on packed fp32x2 (two candidates per FADD2/FFMA2)
-#endif
 #ifndef K3_STGR
 #define K3_STGR 4  // staging: global loads in flight per lane
-#endif
-#ifndef K3_PACKE
-#define K3_PACKE 1  // mask evaluation two hits per iteration on packed fp32x2
 #endif
 constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 filter steps of one chunk
 constexpr int K3_CQ = 24;   // close-tier queue entries per lane (mask mode); flushed when nearly full
@@ -992,76 +986,21 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 #endif
 
 #if K3_MASK
-// Far-tier evaluation straight from the hit masks: each lane pops its hits (words in order, bits
-// from the top), evaluates far pairs in fp32 and compacts the rest into the close queue, which is
-// handed to the fp64 tier whenever some lane's queue is nearly full, and at the end.
-template <bool DIGEST>
-__device__ __forceinline__ void eval_masks_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                               Acc32& a32, int qits, int nhit, int nw, uint32_t sa0, uint32_t step,
-                                               int lane, uint32_t stage0, const double4* __restrict__ u64) {
-  // qits = this lane's hits + empty words (an empty word costs one idle iteration)
-  const int qmax = __reduce_max_sync(0xffffffffu, qits);
-  const float split2 = g.f_split2, lo32 = g.f_lo, sig2 = g.f_sig2, eps24 = -g.f_m24;
-  const uint32_t wstep = 32u * step;  // bytes of staged elements covered by one mask word
-  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
-  const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
-  uint32_t cur = nw > 0 ? ldsu(mq0) : 0u, wa = sa0, wq = mq0 + 128u, wend = mq0 + 128u * (uint32_t)nw;
-  uint32_t qc = qc0;  // next close-queue slot
-  int nclose_all = 0;
-  for (int k = 0; k < qmax; ++k) {
-    const bool valid = cur != 0;
-    uint32_t b;
-    asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));  // highest hit of the word (0xffffffff if none)
-    b = valid ? b : 0u;                              // idle lanes read step 0 of their word: finite, masked
-    cur ^= valid ? (1u << b) : 0u;
-    const uint32_t a = wa + step * b;
-    if (cur == 0 && wq < wend) {  // next word (one predicated load, no loop)
-      cur = ldsu(wq);
-      wq += 128u;
-      wa += wstep;
-    }
-    const float vx = ldsf(a), vy = ldsf(a + K3_YOFF), vz = ldsf(a + K3_ZOFF);
-    const float dx = vx - pc.fx, dy = vy - pc.fy, dz = vz - pc.fz;
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const bool far = !DIGEST && r2 >= split2 && r2 < lo32;
-    stsq(qc, a);
-    qc += (valid && !far) ? K3_QSTRIDE : 0u;
-    float ir2;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
-    ir2 = (valid && far) ? ir2 : 0.0f;  // one mask zeroes s6, fr and the energy term
-    const float s2 = sig2 * ir2;
-    const float s6 = s2 * s2 * s2;
-    const float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
-    const float tx = fr * dx, ty = fr * dy, tz = fr * dz;
-    a32.fx -= tx; a32.fy -= ty; a32.fz -= tz;
-    a32.u = fmaf(s6, s6, a32.u - s6);
-    a32.w0 = fmaf(tx, dx, a32.w0); a32.w1 = fmaf(ty, dy, a32.w1); a32.w2 = fmaf(tz, dz, a32.w2);
-    a32.w3 = fmaf(tx, dy, a32.w3); a32.w4 = fmaf(tx, dz, a32.w4); a32.w5 = fmaf(ty, dz, a32.w5);
-    if ((k & 7) == 7 && __any_sync(0xffffffffu, qc > qclim)) {
-      __syncwarp();
-      const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
-      eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
-      __syncwarp();
-      nclose_all += nclose;
-      qc = qc0;
-    }
-  }
-  __syncwarp();
-  const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
-  a32.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
-  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
-}
+// Mask mode.  Lane (i, s) of an i-batch with S streams filters the staged element PAIRS
+// {2k, 2k+1}, k = s, s+S, ... (one "pair step" = one LDS.64 per coordinate: the S lanes of a step
+// read S distinct 8-byte words, one shared-memory wavefront for S <= 2).  Hits are bits of per-lane
+// 32-bit words, bit 2q + h for element 2(s + S(16w + q)) + h of word w; one STS.32 per word.
 
-#if K3_PACK
-// pop this lane's next hit (highest bit of the current word) and refill the word when it empties
-__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step,
+// pop this lane's next hit (highest bit of the current word; returns its staged address) and
+// refill the word when it empties
+__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step2,
                                             uint32_t wstep, bool& valid) {
   valid = cur != 0;
   uint32_t b;
   asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));
-  b = valid ? b : 0u;  // idle lanes read step 0 of their word: finite, masked
+  b = valid ? b : 0u;  // idle lanes read element 0 of their word: finite, masked
   cur ^= valid ? (1u << b) : 0u;
-  const uint32_t a = wa + step * b;
+  const uint32_t a = wa + step2 * (b >> 1) + ((b & 1u) << 2);
   if (cur == 0 && wq < wend) {
     cur = ldsu(wq);
     wq += 128u;
@@ -1070,18 +1009,21 @@ __device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_
   return a;
 }
 
-// Two hits per iteration: the far-tier math runs on packed fp32x2 (FADD2/FMUL2/FFMA2) with packed
-// accumulators, folded into the fp64 Acc once per chunk.
+// Far tier straight from the hit words, two hits per iteration on packed fp32x2 (FADD2/FMUL2/FFMA2)
+// with packed partial sums folded into the fp64 Acc once per chunk.  Everything else (r < r_split,
+// the cutoff band, every hit in digest mode) is compacted into the close queue, which is handed
+// to the fp64 tier whenever some lane's queue is nearly full, and at the end.
 template <bool DIGEST>
 __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 int qits, int nhit, int nw, uint32_t sa0, uint32_t step, int lane,
+                                                 int qits, int nhit, int nw, uint32_t sa0, uint32_t step2, int lane,
                                                  uint32_t stage0, const double4* __restrict__ u64) {
+  // qits = this lane's hits + empty words (an empty word costs one idle pop)
   const int qmax = __reduce_max_sync(0xffffffffu, qits);
   const float split2 = g.f_split2, lo32 = g.f_lo;
   const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
   const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), EPS24 = pk2(-g.f_m24, -g.f_m24), TWO = pk2(2.0f, 2.0f),
                  NEG1 = pk2(-1.0f, -1.0f);
-  const uint32_t wstep = 32u * step;
+  const uint32_t wstep = 16u * step2;  // bytes of staged elements covered by one hit word
   const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
   const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
   uint32_t cur = nw > 0 ? ldsu(mq0) : 0u, wa = sa0, wq = mq0 + 128u, wend = mq0 + 128u * (uint32_t)nw;
@@ -1090,8 +1032,8 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   uint64_t Fx = 0, Fy = 0, Fz = 0, Uq = 0, W0 = 0, W1 = 0, W2 = 0, W3 = 0, W4 = 0, W5 = 0;  // packed partial sums
   for (int k = 0; k < qmax; k += 2) {
     bool va, vb;
-    const uint32_t aa = pop_hit(cur, wa, wq, wend, step, wstep, va);
-    const uint32_t ab = pop_hit(cur, wa, wq, wend, step, wstep, vb);
+    const uint32_t aa = pop_hit(cur, wa, wq, wend, step2, wstep, va);
+    const uint32_t ab = pop_hit(cur, wa, wq, wend, step2, wstep, vb);
     const uint64_t DX = add2(pk2(ldsf(aa), ldsf(ab)), nfx), DY = add2(pk2(ldsf(aa + K3_YOFF), ldsf(ab + K3_YOFF)), nfy),
                    DZ = add2(pk2(ldsf(aa + K3_ZOFF), ldsf(ab + K3_ZOFF)), nfz);
     float r2a, r2b;
@@ -1131,94 +1073,88 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   acc.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
   eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
 }
-#endif
 
-// Mask filter: lane (i, s) tests staged elements s, s+S, ... in blocks of 32 steps; hit k of a
-// block sets bit k of a register word (FSETP + predicated LOP3: no shared-memory store per
-// candidate); one STS.32 per block.  K3_MW words hold a whole chunk, so the evaluation runs once.
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
+// Mask filter over pair steps (see above): per pair step three LDS.64 (x, y, z of elements 2k, 2k+1,
+// already packed for FADD2) and three packed ops give both r^2; hit bits are set with immediates.
 template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                  Acc32& a32, int s, int S, int iters, int lane,
                                                  const double4* __restrict__ u64) {
-  static_assert(32 * K3_MW >= K3_CAP + 32, "mask words must cover one chunk");
+  static_assert(32 * K3_MW >= K3_CAP + 32, "hit words must cover one chunk (ceil(K3_CAP / 32) words at S = 1)");
+  static_assert(K3_UNROLL % 2 == 0 && 32 % K3_UNROLL == 0, "groups of whole pair steps");
+  constexpr int G2 = K3_UNROLL / 2;  // pair steps per group
   const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
-  const uint32_t step = 4u * (uint32_t)S;
-  const float fx = pc.fx, fy = pc.fy, fz = pc.fz, hi = pc.hi;
-#if K3_PACK
-  const uint64_t nfx = pk2(-fx, -fx), nfy = pk2(-fy, -fy), nfz = pk2(-fz, -fz);
-#endif
-  const uint32_t sa0 = stage0 + 4u * (uint32_t)s;
+  const uint32_t step2 = 8u * (uint32_t)S;  // bytes between a lane's consecutive pair steps
+  const float hi = pc.hi;
+  const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
+  const uint32_t sa0 = stage0 + 8u * (uint32_t)s;
   const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
+  const int iters2 = (iters + 1) >> 1;  // pair steps: ceil(ctot / 2S)
   uint32_t sa = sa0;
-  int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation iterations this lane needs)
-  const int nfull = iters >> 5;
-  // one group of K3_UNROLL steps from staged address sa: hit k sets bit sh + k
+  int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation pops this lane needs)
+  // G2 pair steps from staged address sa: hit (q, h) sets bit sh + 2q + h
   auto group = [&](uint32_t sa, int sh) -> uint32_t {
-    float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
+    uint64_t X[G2], Y[G2], Z[G2];
 #pragma unroll
-    for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
-      vx[k] = ldsf(sa + step * k);
-      vy[k] = ldsf(sa + step * k + K3_YOFF);
-      vz[k] = ldsf(sa + step * k + K3_ZOFF);
+    for (int q = 0; q < G2; ++q) {  // all loads of the group first (asm keeps program order)
+      X[q] = lds64(sa + step2 * q);
+      Y[q] = lds64(sa + step2 * q + K3_YOFF);
+      Z[q] = lds64(sa + step2 * q + K3_ZOFF);
     }
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < K3_UNROLL; ++k) {
-#if K3_PACK
-      if (k & 1) continue;
-      // two candidates per packed op (FADD2/FMUL2/FFMA2: same rounding as the scalar form)
-      const uint64_t dx = add2(pk2(vx[k], vx[k + 1]), nfx), dy = add2(pk2(vy[k], vy[k + 1]), nfy),
-                     dz = add2(pk2(vz[k], vz[k + 1]), nfz);
+    for (int q = 0; q < G2; ++q) {
+      const uint64_t dx = add2(X[q], nfx), dy = add2(Y[q], nfy), dz = add2(Z[q], nfz);
       float r2a, r2b;
       upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
-      m |= (r2a < hi) ? (1u << (sh + k)) : 0u;
-      m |= (r2b < hi) ? (1u << (sh + k + 1)) : 0u;
-#else
-      const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      m |= (r2 < hi) ? (1u << (sh + k)) : 0u;
-#endif
+      m |= (r2a < hi) ? (1u << (sh + 2 * q)) : 0u;
+      m |= (r2b < hi) ? (1u << (sh + 2 * q + 1)) : 0u;
     }
     return m;
   };
-  for (; w < nfull; ++w) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int g8 = 0; g8 < 32; g8 += K3_UNROLL) {
-      m |= group(sa, g8);
-      sa += step * K3_UNROLL;
-    }
-    stsu(mq0 + 128u * (uint32_t)w, m);
-    const int c = __popc(m);
-    nhit += c;
-    qlen += c ? c : 1;
-  }
-  const int rem = iters & 31;
-  if (rem) {  // last word: whole groups, then single steps
-    uint32_t m = 0;
-    int k = 0;
-    for (; k + K3_UNROLL <= rem; k += K3_UNROLL) {
-      m |= group(sa, 0) << k;
-      sa += step * K3_UNROLL;
-    }
-    for (; k < rem; ++k) {
-      const float dx = ldsf(sa) - fx, dy = ldsf(sa + K3_YOFF) - fy, dz = ldsf(sa + K3_ZOFF) - fz;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      m |= (r2 < hi) ? (1u << k) : 0u;
-      sa += step;
-    }
+  auto put = [&](uint32_t m) {
     stsu(mq0 + 128u * (uint32_t)w, m);
     const int c = __popc(m);
     nhit += c;
     qlen += c ? c : 1;
     ++w;
+  };
+  const int nfull = iters2 >> 4;
+  while (w < nfull) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int g8 = 0; g8 < 32; g8 += 2 * G2) {
+      m |= group(sa, g8);
+      sa += step2 * G2;
+    }
+    put(m);
+  }
+  const int rem = iters2 & 15;
+  if (rem) {  // last word: whole groups, then single pair steps
+    uint32_t m = 0;
+    int q = 0;
+    for (; q + G2 <= rem; q += G2) {
+      m |= group(sa, 0) << (2 * q);
+      sa += step2 * G2;
+    }
+    for (; q < rem; ++q) {
+      const uint64_t dx = add2(lds64(sa), nfx), dy = add2(lds64(sa + K3_YOFF), nfy), dz = add2(lds64(sa + K3_ZOFF), nfz);
+      float r2a, r2b;
+      upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
+      m |= ((r2a < hi) ? 1u : 0u) << (2 * q);
+      m |= ((r2b < hi) ? 2u : 0u) << (2 * q);
+      sa += step2;
+    }
+    put(m);
   }
   __syncwarp();
-#if K3_PACK && K3_PACKE
-  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step, lane, stage0, u64);
-#else
-  eval_masks_f32<DIGEST>(g, pc, sm, acc, a32, qlen, nhit, w, sa0, step, lane, stage0, u64);
-#endif
+  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step2, lane, stage0, u64);
 }
 #endif
 
@@ -1390,15 +1326,15 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             }
           }
         }
-        // S far sentinels after the chunk (indices ctot .. ctot+S-1)
-        if (lane < S) {
+        // far sentinels after the chunk: S (fp64 streams), 2S (fp32 pair steps)
+        for (int t = lane; t < (sizeof(T) == 8 ? S : 2 * S); t += 32) {
           if constexpr (sizeof(T) == 8) {
-            sm.stage[ctot + lane] = far4<T>();
-            sm.s64.nh[ctot + lane] = 0u;
+            sm.stage[ctot + t] = far4<T>();
+            sm.s64.nh[ctot + t] = 0u;
           } else {
-            sm.s64.sx[ctot + lane] = sm.s64.sy[ctot + lane] = sm.s64.sz[ctot + lane] = 1e30f;
+            sm.s64.sx[ctot + t] = sm.s64.sy[ctot + t] = sm.s64.sz[ctot + t] = 1e30f;
           }
-          sm.sent[ctot + lane] = 0;
+          sm.sent[ctot + t] = 0;
         }
         __syncwarp();
         const int iters = (int)((ctot + S - 1) / S);
