@@ -989,7 +989,7 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 // Mask mode.  Lane (i, s) of an i-batch with S streams filters the staged element PAIRS
 // {2k, 2k+1}, k = s, s+S, ... (one "pair step" = one LDS.64 per coordinate: the S lanes of a step
 // read S distinct 8-byte words, one shared-memory wavefront for S <= 2).  Hits are bits of per-lane
-// 32-bit words, bit 2q + h for element 2(s + S(16w + q)) + h of word w; one STS.32 per word.
+// 32-bit words, bit 31 - (2q + h) for element 2(s + S(16w + q)) + h of word w; one STS.32 per word.
 
 // pop this lane's next hit (highest bit of the current word; returns its staged address) and
 // refill the word when it empties
@@ -998,9 +998,10 @@ __device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_
   valid = cur != 0;
   uint32_t b;
   asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));
-  b = valid ? b : 0u;  // idle lanes read element 0 of their word: finite, masked
+  b = valid ? b : 31u;  // idle lanes read element 0 of their word: finite, masked
   cur ^= valid ? (1u << b) : 0u;
-  const uint32_t a = wa + step2 * (b >> 1) + ((b & 1u) << 2);
+  const uint32_t c = 31u - b;  // candidate index in the word (2q + h)
+  const uint32_t a = wa + step2 * (c >> 1) + ((c & 1u) << 2);
   if (cur == 0 && wq < wend) {
     cur = ldsu(wq);
     wq += 128u;
@@ -1074,6 +1075,12 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
 }
 
+// (m << 1) | (v >> 31): one funnel shift
+__device__ __forceinline__ uint32_t shl_in(uint32_t m, uint32_t v) {
+  uint32_t r;
+  asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(r) : "r"(v), "r"(m));
+  return r;
+}
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   uint64_t v;
   asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
@@ -1098,8 +1105,18 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
   const int iters2 = (iters + 1) >> 1;  // pair steps: ceil(ctot / 2S)
   uint32_t sa = sa0;
   int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation pops this lane needs)
-  // G2 pair steps from staged address sa: hit (q, h) sets bit sh + 2q + h
-  auto group = [&](uint32_t sa, int sh) -> uint32_t {
+  // hit bits are shifted in from the right: (r^2 - hi) is formed inside the packed FMA chain
+  // (dx^2 - hi first) and its sign bit enters the word with one funnel shift per candidate,
+  // so candidate c of a word (c = 2q + h, 0..31) ends at bit 31 - c
+  const uint64_t NHI = pk2(-hi, -hi);
+  auto pair_step = [&](uint64_t X, uint64_t Y, uint64_t Z, uint32_t& m) {
+    const uint64_t dx = add2(X, nfx), dy = add2(Y, nfy), dz = add2(Z, nfz);
+    float ea, eb;  // r^2 - hi (sign bit set: hit)
+    upk2(fma2(dz, dz, fma2(dy, dy, fma2(dx, dx, NHI))), ea, eb);
+    m = shl_in(m, __float_as_uint(ea));
+    m = shl_in(m, __float_as_uint(eb));
+  };
+  auto group = [&](uint32_t sa, uint32_t& m) {
     uint64_t X[G2], Y[G2], Z[G2];
 #pragma unroll
     for (int q = 0; q < G2; ++q) {  // all loads of the group first (asm keeps program order)
@@ -1107,16 +1124,8 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
       Y[q] = lds64(sa + step2 * q + K3_YOFF);
       Z[q] = lds64(sa + step2 * q + K3_ZOFF);
     }
-    uint32_t m = 0;
 #pragma unroll
-    for (int q = 0; q < G2; ++q) {
-      const uint64_t dx = add2(X[q], nfx), dy = add2(Y[q], nfy), dz = add2(Z[q], nfz);
-      float r2a, r2b;
-      upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
-      m |= (r2a < hi) ? (1u << (sh + 2 * q)) : 0u;
-      m |= (r2b < hi) ? (1u << (sh + 2 * q + 1)) : 0u;
-    }
-    return m;
+    for (int q = 0; q < G2; ++q) pair_step(X[q], Y[q], Z[q], m);
   };
   auto put = [&](uint32_t m) {
     stsu(mq0 + 128u * (uint32_t)w, m);
@@ -1130,28 +1139,24 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     uint32_t m = 0;
 #pragma unroll
     for (int g8 = 0; g8 < 32; g8 += 2 * G2) {
-      m |= group(sa, g8);
+      group(sa, m);
       sa += step2 * G2;
     }
     put(m);
   }
   const int rem = iters2 & 15;
-  if (rem) {  // last word: whole groups, then single pair steps
+  if (rem) {  // last word: whole groups, then single pair steps, then aligned to bit 31
     uint32_t m = 0;
     int q = 0;
     for (; q + G2 <= rem; q += G2) {
-      m |= group(sa, 0) << (2 * q);
+      group(sa, m);
       sa += step2 * G2;
     }
     for (; q < rem; ++q) {
-      const uint64_t dx = add2(lds64(sa), nfx), dy = add2(lds64(sa + K3_YOFF), nfy), dz = add2(lds64(sa + K3_ZOFF), nfz);
-      float r2a, r2b;
-      upk2(fma2(dz, dz, fma2(dy, dy, mul2(dx, dx))), r2a, r2b);
-      m |= ((r2a < hi) ? 1u : 0u) << (2 * q);
-      m |= ((r2b < hi) ? 2u : 0u) << (2 * q);
+      pair_step(lds64(sa), lds64(sa + K3_YOFF), lds64(sa + K3_ZOFF), m);
       sa += step2;
     }
-    put(m);
+    put(m << (32 - 2 * rem));
   }
   __syncwarp();
   eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step2, lane, stage0, u64);
