@@ -993,15 +993,14 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 
 // pop this lane's next hit (highest bit of the current word; returns its staged address) and
 // refill the word when it empties
-__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step2,
+__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step2m8,
                                             uint32_t wstep, bool& valid) {
   valid = cur != 0;
-  uint32_t b;
-  asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(cur));
-  b = valid ? b : 31u;  // idle lanes read element 0 of their word: finite, masked
-  cur ^= valid ? (1u << b) : 0u;
-  const uint32_t c = 31u - b;  // candidate index in the word (2q + h)
-  const uint32_t a = wa + step2 * (c >> 1) + ((c & 1u) << 2);
+  const uint32_t c = (uint32_t)__clz(cur);  // candidate 2q + h of the highest hit (32 if none)
+  cur ^= 0x80000000u >> c;                  // shift by 32 gives 0: nothing to clear
+  const uint32_t cc = valid ? c : 0u;       // idle lanes read element 0 of their word: finite, masked
+  // element 2(s + S(16w + q)) + h lies at wa + 8 S q + 4 h = wa + 4 cc + (8 S - 8) q
+  const uint32_t a = wa + 4u * cc + step2m8 * (cc >> 1);
   if (cur == 0 && wq < wend) {
     cur = ldsu(wq);
     wq += 128u;
@@ -1022,7 +1021,7 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   const int qmax = __reduce_max_sync(0xffffffffu, qits);
   const float split2 = g.f_split2, lo32 = g.f_lo;
   const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
-  const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), EPS24 = pk2(-g.f_m24, -g.f_m24), TWO = pk2(2.0f, 2.0f),
+  const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), C48 = pk2(g.f_c48, g.f_c48), M24 = pk2(g.f_m24, g.f_m24),
                  NEG1 = pk2(-1.0f, -1.0f);
   const uint32_t wstep = 16u * step2;  // bytes of staged elements covered by one hit word
   const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
@@ -1033,8 +1032,8 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   uint64_t Fx = 0, Fy = 0, Fz = 0, Uq = 0, W0 = 0, W1 = 0, W2 = 0, W3 = 0, W4 = 0, W5 = 0;  // packed partial sums
   for (int k = 0; k < qmax; k += 2) {
     bool va, vb;
-    const uint32_t aa = pop_hit(cur, wa, wq, wend, step2, wstep, va);
-    const uint32_t ab = pop_hit(cur, wa, wq, wend, step2, wstep, vb);
+    const uint32_t aa = pop_hit(cur, wa, wq, wend, step2 - 8u, wstep, va);
+    const uint32_t ab = pop_hit(cur, wa, wq, wend, step2 - 8u, wstep, vb);
     const uint64_t DX = add2(pk2(ldsf(aa), ldsf(ab)), nfx), DY = add2(pk2(ldsf(aa + K3_YOFF), ldsf(ab + K3_YOFF)), nfy),
                    DZ = add2(pk2(ldsf(aa + K3_ZOFF), ldsf(ab + K3_ZOFF)), nfz);
     float r2a, r2b;
@@ -1050,7 +1049,7 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
     const uint64_t IR = pk2((va && fa) ? ia : 0.0f, (vb && fb) ? ib : 0.0f);  // one mask per pair
     const uint64_t S2 = mul2(SIG2, IR);
     const uint64_t S6 = mul2(mul2(S2, S2), S2);
-    const uint64_t FR = mul2(mul2(mul2(EPS24, S6), fma2(TWO, S6, NEG1)), IR);
+    const uint64_t FR = mul2(mul2(fma2(C48, S6, M24), S6), IR);  // (48 eps s6 - 24 eps) s6 / r^2
     const uint64_t TX = mul2(FR, DX), TY = mul2(FR, DY), TZ = mul2(FR, DZ);
     Fx = add2(Fx, TX); Fy = add2(Fy, TY); Fz = add2(Fz, TZ);
     Uq = fma2(S6, add2(S6, NEG1), Uq);
