@@ -401,7 +401,13 @@ constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (
 #endif
 constexpr int K3_UNROLL = K3_UNROLL_OVR;  // filter steps per group (loads of a group issued together)
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
-constexpr int K3_CELLS = 4;     // cells per warp (= per block: one warp per block)
+#ifndef K3_CELLS_OVR
+#define K3_CELLS_OVR 4
+#endif
+constexpr int K3_CELLS = K3_CELLS_OVR;  // fewest cells per warp (= per block: one warp per block)
+#ifndef K3_CELLS_MAX
+#define K3_CELLS_MAX 16  // most cells per block (large layers; host cells_per_block)
+#endif
 constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, nonfinite
 constexpr double K3_BAND64 = 1e-12;
 
