@@ -411,7 +411,10 @@ typedef uint16_t K3QT;
 #define K3_STGR 4  // staging: global loads in flight per lane
 #endif
 constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 filter steps of one chunk
-constexpr int K3_CQ = 24;   // close-tier queue entries per lane (mask mode); flushed when nearly full
+#ifndef K3_CQ_OVR
+#define K3_CQ_OVR 24
+#endif
+constexpr int K3_CQ = K3_CQ_OVR;  // close-tier queue entries per lane (mask mode); flushed when nearly full
 constexpr uint32_t K3_QSTRIDE = 32u * sizeof(K3QT);  // bytes between consecutive entries of one lane
 constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (low 16 bits of shared addresses / staged indices)
 #ifndef K3_UNROLL_OVR
