@@ -423,7 +423,7 @@ constexpr int K3_QCAP = K3_QCAP_OVR;     // per-lane queue of filter survivors (
 constexpr int K3_UNROLL = K3_UNROLL_OVR;  // filter steps per group (loads of a group issued together)
 constexpr int K3_MAXE = 40;     // neighborhood entries (<= 36)
 #ifndef K3_CELLS_OVR
-#define K3_CELLS_OVR 4
+#define K3_CELLS_OVR 1
 #endif
 constexpr int K3_CELLS = K3_CELLS_OVR;  // fewest cells per warp (= per block: one warp per block)
 #ifndef K3_CELLS_MAX

@@ -144,14 +144,15 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-// Cells per k_pairs block (one warp): more cells amortize the block prologue/epilogue (measured on
-// C4 DO: 4 / 8 / 16 cells -> 32.6 / 31.9 / 31.7 ms), fewer keep small grids filling the GPU.  Chosen
-// from the cells per LAYER only, so every rank of a slab decomposition groups the same cells
-// (bitwise-equal partial sums for any rank count).
+// Cells per k_pairs block (one warp): more cells amortize the block prologue/epilogue (C4 DO: 4 / 8 /
+// 16 cells -> 32.6 / 31.9 / 31.7 ms), fewer keep small grids busy (C0: 1 cell 0.089 ms vs 4 cells
+// 0.315 ms; C2: 0.163 vs 0.178 ms).  The largest power of two <= K3_CELLS_MAX that still leaves
+// K3_MIN_BLOCKS blocks (~32 waves of resident warps).  It depends on the global grid only, so
+// every rank of a slab decomposition groups the same cells (bitwise-equal partial sums).
+constexpr int64_t K3_MIN_BLOCKS = 75776;
 int cells_per_block(const Geom& g) {
-  const int64_t per_layer = (int64_t)g.dims[0] * g.dims[1];
   int cpb = K3_CELLS;
-  while (cpb * 2 <= K3_CELLS_MAX && per_layer >= (int64_t)(cpb * 2) * 1024) cpb *= 2;
+  while (cpb * 2 <= K3_CELLS_MAX && g.ncells / (cpb * 2) >= K3_MIN_BLOCKS) cpb *= 2;
   return cpb;
 }
 
@@ -729,10 +730,10 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
   int64_t N = std::max<int64_t>(cfg->capacity, 1);
   ctx->cap = N;
   ctx->max_cells = cfg->max_cells > 0 ? cfg->max_cells : 2 * N + 4096;
-  int cpb = K3_CELLS;  // the smallest cells per block: the most blocks
   ctx->max_layers = 1 << 16;
-  // blocks = sum over layers of ceil(l1 l2 / cpb) <= C/cpb + layers
-  ctx->max_blocks = ctx->max_cells / cpb + ctx->max_layers + 16;
+  // blocks = sum over layers of ceil(l1 l2 / cpb) <= C/cpb + layers, and cells_per_block keeps C/cpb
+  // below 2 K3_MIN_BLOCKS unless cpb = K3_CELLS_MAX
+  ctx->max_blocks = std::max<int64_t>(2 * K3_MIN_BLOCKS, ctx->max_cells / K3_CELLS_MAX) + ctx->max_layers + 16;
   size_t v4 = v4size(ctx), ts = tsize(ctx);
   int64_t C1 = ctx->max_cells + 1;
   const size_t N_ = (size_t)N;
