@@ -113,6 +113,13 @@ def dist_setup(backend):
     return rank, lrank, ws
 
 
+def l2_text(n):
+    mb = n * 190 / 1e6  # resident bytes per particle in fp32 mode
+    if mb > 126:
+        return f"inputs (~{mb / 1e3:.1f} GB) >> L2 (126 MB); no flush"
+    return f"inputs (~{mb:.0f} MB) fit in L2 (126 MB), no flush: a per-config line, not the bench workload"
+
+
 def box_text(w):
     return {"none": "equilibrium cube", "le": "Lees-Edwards shear", "kr": "KR planar elongation",
             "gkr": "generalized KR " + str(w.extra.get("flow", ""))}[w.policy] + f", dt={w.dt}"
@@ -301,8 +308,18 @@ def run_ours(args):
     cl.set_state(qd, pd)
     del qd, pd
     dt = w.dt
-    for _ in range(args.warmup):
-        cl.step(dt, 1, want_uw=False)
+    # --steps-per-call: SLLOD steps per nc_step_sllod call (the API takes a step count); 1 = one call
+    # per step (default), 0 = all K timed steps in one call (measured equal on C0-C4: the host
+    # overhead per call is hidden behind the queued launches)
+    spc = args.steps_per_call if args.steps_per_call > 0 else max(args.steps, 1)
+
+    def run_steps(k):
+        while k > 0:
+            m = min(k, spc)
+            cl.step(dt, m, want_uw=False)
+            k -= m
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
 
     import torch.distributed as dist
@@ -321,8 +338,7 @@ def run_ours(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
-        cl.step(dt, 1, want_uw=False)
+    run_steps(args.steps)
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
@@ -409,7 +425,7 @@ def run_ours(args):
                        "box": box_text(w), "potential": pot_text(w),
                        "precision": ("fp32 storage + fp32 filter, fp32/fp64 two-tier interactions" if prec == "f32"
                                      else "fp64 throughout"),
-                       "l2": "inputs (~7 GB) >> L2 (126 MB); no flush", "parallelism": f"replicas x{ws}"},
+                       "l2": l2_text(w.n), "parallelism": f"replicas x{ws}", "steps_per_call": spc},
             "particle_steps_per_s": psteps,
             "interactions_per_particle": inter / w.n, "candidates_per_particle": cand / w.n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -442,6 +458,8 @@ def main():
     ap.add_argument("--prec", default=None, choices=["f32", "f64"], help="default: the config's precision")
     ap.add_argument("--ref-sample", type=int, default=100000)  # ~20 s of oracle work on the C4 sample
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--steps-per-call", type=int, default=1,
+                    help="SLLOD steps per nc_step_sllod call (0 = all timed steps in one call; measured the same)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
