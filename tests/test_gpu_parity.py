@@ -257,3 +257,31 @@ def test_c4_full_size_sampled(variant):
     assert np.abs(g["F"][idx] - r.F).max() <= 2e-5 * rms
     # Newton's third law over the whole system
     assert np.abs(g["F"].sum(axis=0)).max() < 1e-3 * rms * np.sqrt(len(q))
+
+
+def _cluster_workload(prec):
+    """A sheared box (L = 14 sigma, l = 5 DO cells per side) holding a dense jittered cube of 9^3 = 729
+    particles at spacing 0.4 sigma next to 400 uniformly spread ones: cells of ~150-300 particles
+    (staging in several chunks, i-batches of 32 with one stream, survivors queued well past the
+    close-tier queue), beside ordinary cells.  Seeded; no physics intended."""
+    from paper_1412_3784_b200 import workloads as W
+
+    rng = W.rng_for(90, 0)
+    L = np.array([[14.0, 3.1, 0.0], [0.0, 14.0, 0.0], [0.0, 0.0, 14.0]])
+    g = np.arange(9) * 0.4
+    cube = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3) + 4.3
+    cube += rng.uniform(-0.04, 0.04, cube.shape)
+    lam = rng.uniform(0.0, 1.0, (400, 3))
+    q = np.concatenate([cube, lam @ L.T]).astype(np.float32 if prec == "f32" else np.float64)
+    w = W.Workload(name="cluster", n=len(q), L0=L, A=np.zeros((3, 3)), policy="none", t0=0.0, L=L, rc=2.5)
+    return w, q
+
+
+@pytest.mark.parametrize("variant", ["ds", "do"])
+@pytest.mark.parametrize("prec", ["f32", "f64"])
+def test_dense_cluster_stress(variant, prec):
+    """Overcrowded cells: pair sets bit-exact and forces within the bars through the multi-chunk,
+    one-stream and queue-flush paths of k_pairs (and of the fp64 kernel)."""
+    w, q = _cluster_workload(prec)
+    g, r = check_against_oracle(w, q, variant, prec, kernel="cell")
+    assert r.interactions > 100000  # the cluster really is dense
