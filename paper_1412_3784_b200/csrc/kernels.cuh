@@ -396,17 +396,7 @@ constexpr int K3_STAGE = K3_CAP + 66;  // + up to 2S far sentinels so the filter
 #ifndef K3_MINB
 #define K3_MINB 14
 #endif
-#ifndef K3_Q32
-#define K3_Q32 0   // 1: 32-bit queue entries (conflict-free stores, +3 KB smem/warp): measured 40.6 vs 39.8 ms on C4
-#endif
-#if K3_Q32
-typedef uint32_t K3QT;
-#else
-typedef uint16_t K3QT;
-#endif
-#ifndef K3_MASK
-#define K3_MASK 1  // fp32 filter records hits as bits of per-lane 32-step mask words (no per-candidate store)
-#endif
+typedef uint16_t K3QT;  // queue entries: low 16 bits of shared addresses (see addr_from16)
 #ifndef K3_STGR
 #define K3_STGR 4  // staging: global loads in flight per lane
 #endif
@@ -446,8 +436,8 @@ template <typename T>
 struct K3Smem {
   typename V4<T>::t stage[sizeof(T) == 8 ? K3_STAGE : 1];  // fp64 mode: staged lab positions, .w = sorted index
   K3Stage64<T> s64;
-  K3QT queue[(sizeof(T) == 4 && K3_MASK) ? K3_CQ : K3_QCAP][32];
-  uint32_t mq[(sizeof(T) == 4 && K3_MASK) ? K3_MW : 1][32];  // fp32 mask mode: hit words mq[w][lane]
+  K3QT queue[sizeof(T) == 4 ? K3_CQ : K3_QCAP][32];  // fp32: close-tier queue; fp64: survivor queue
+  uint32_t mq[sizeof(T) == 4 ? K3_MW : 1][32];         // fp32: hit words mq[w][lane]
   uint8_t sent[K3_STAGE];
   uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
   int32_t e_n[K3_MAXE][3];
@@ -645,7 +635,7 @@ __device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32
 
 // NC_F64: evaluate ONE queued survivor t of this lane.  The filter already
 // applied the canonical membership test (R16); d is formed error-free in the lab
-// frame.  (NC_F32 uses eval_pairs_f32 / eval_close_f64.)
+// frame.  (NC_F32 uses filter_chunk_f32 / eval_masks_f32x2 / eval_close_f64.)
 template <typename T, bool DIGEST>
 __device__ __forceinline__ void eval_one(const Geom& g, const PairCtx<T>& pc, const K3Smem<T>& sm, Acc& acc,
                                          uint32_t t, double sig2, double eps24) {
@@ -766,29 +756,11 @@ __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
 __device__ __forceinline__ uint32_t addr_from16(uint32_t lo16, uint32_t stage0) {
   return (stage0 & 0xffff0000u) | lo16;
 }
-// a += K3_QSTRIDE (one queue row) if r2 < hi (one FSETP + one predicated IADD)
-__device__ __forceinline__ uint32_t bump_if_less(uint32_t a, float r2, float hi) {
-  asm("{\n\t.reg .pred p;\n\tsetp.lt.f32 p, %1, %2;\n\t@p add.u32 %0, %0, %3;\n\t}"
-      : "+r"(a)
-      : "f"(r2), "f"(hi), "n"(K3_QSTRIDE));
-  return a;
-}
 __device__ __forceinline__ void stsq(uint32_t a, uint32_t v) {
-#if K3_Q32
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-#else
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
-#endif
 }
 // shared address of a queued staged element
-__device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) {
-#if K3_Q32
-  (void)stage0;
-  return e;
-#else
-  return addr_from16(e, stage0);
-#endif
-}
+__device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) { return addr_from16(e, stage0); }
 
 // fp32 staging is three float arrays (sx, sy, sz): a broadcast LDS.32 is one shared-memory
 // wavefront, a 16-byte LDS.128 four (the filter is bound by the shared-memory pipe)
@@ -833,18 +805,6 @@ __device__ __forceinline__ void stsu(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 
-// fp32 accumulators of the far-pair tier (folded into the fp64 Acc after each evaluation)
-struct Acc32 {
-  float fx, fy, fz, u, w0, w1, w2, w3, w4, w5;
-  uint32_t cnt;
-};
-
-__device__ __forceinline__ void fold32(Acc& acc, Acc32& a) {
-  acc.fx += a.fx; acc.fy += a.fy; acc.fz += a.fz; acc.u += a.u;
-  acc.w0 += a.w0; acc.w1 += a.w1; acc.w2 += a.w2; acc.w3 += a.w3; acc.w4 += a.w4; acc.w5 += a.w5;
-  acc.cnt += a.cnt;
-  a = Acc32{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u};
-}
 
 // Close tier: survivors with r < r_split (large forces), in the r_c band, or
 // all survivors in digest mode -- fp64 from the fp64 staged coordinates,
@@ -918,101 +878,6 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
   }
 }
 
-// Evaluate this lane's queued survivors.  Far tier (r_split^2 <= r^2 below
-// the lower edge of the fp32 cutoff band: definitely inside, |f| small) in
-// fp32; everything else is compacted in place and goes to the fp64 tier.
-template <bool DIGEST>
-__device__ __forceinline__ void eval_pairs_f32(K3QT (*queue)[32], const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                               Acc32& a32, int qlen, int lane, uint32_t stage0,
-                                               const double4* __restrict__ u64) {
-  int nclose = qlen;
-  if (!DIGEST) {
-    const int qmax = __reduce_max_sync(0xffffffffu, qlen);
-    const float split2 = (float)g.rsplit2, lo32 = (float)g.band_lo, sig2 = (float)g.sig2, eps24 = (float)(24.0 * g.eps);
-    const uint32_t dummy = stage0 + 4u * K3_DUMMY;
-    nclose = 0;
-    for (int k = 0; k < qmax; ++k) {
-      const bool valid = k < qlen;
-      const uint32_t a = valid ? qaddr(queue[k][lane], stage0) : dummy;
-      const float vx = ldsf(a), vy = ldsf(a + K3_YOFF), vz = ldsf(a + K3_ZOFF);
-      const float dx = vx - pc.fx, dy = vy - pc.fy, dz = vz - pc.fz;
-      const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-      const bool far = valid && r2 >= split2 && r2 < lo32;
-      queue[nclose][lane] = (K3QT)a;   // in-place compaction (nclose <= k)
-      nclose += (valid && !far) ? 1 : 0;
-      float ir2;
-      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ir2) : "f"(r2));
-      ir2 = far ? ir2 : 0.0f;          // one mask zeroes s6, fr and the energy term
-      const float s2 = sig2 * ir2;
-      const float s6 = s2 * s2 * s2;
-      const float fr = (eps24 * s6) * (2.0f * s6 - 1.0f) * ir2;
-      const float tx = fr * dx, ty = fr * dy, tz = fr * dz;
-      a32.fx -= tx; a32.fy -= ty; a32.fz -= tz;
-      a32.u = fmaf(s6, s6, a32.u - s6);
-      a32.w0 = fmaf(tx, dx, a32.w0); a32.w1 = fmaf(ty, dy, a32.w1); a32.w2 = fmaf(tz, dz, a32.w2);
-      a32.w3 = fmaf(tx, dy, a32.w3); a32.w4 = fmaf(tx, dz, a32.w4); a32.w5 = fmaf(ty, dz, a32.w5);
-    }
-    a32.cnt += (uint32_t)(qlen - nclose);  // every queued entry is either far or compacted for the fp64 tier
-    __syncwarp();
-  }
-  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, queue);
-}
-
-#if !K3_MASK
-template <bool DIGEST>
-__device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 Acc32& a32, int s, int S, int iters, int lane,
-                                                 const double4* __restrict__ u64) {
-  const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
-  const uint32_t q0 = smem_u32(&sm.queue[0][lane]);
-  const uint32_t qlim = q0 + K3_QSTRIDE * (K3_QCAP - K3_UNROLL);
-  const uint32_t step = 4u * (uint32_t)S;
-  const float fx = pc.fx, fy = pc.fy, fz = pc.fz, hi = pc.hi;
-  uint32_t sa = stage0 + 4u * (uint32_t)s;
-  uint32_t qa = q0;
-  int it = 0;
-  const int main_iters = iters - iters % K3_UNROLL;
-  for (;;) {
-    // filter groups of K3_UNROLL until some lane's queue is nearly full
-    bool full = false;
-    while (it < main_iters) {
-      float vx[K3_UNROLL], vy[K3_UNROLL], vz[K3_UNROLL];
-#pragma unroll
-      for (int k = 0; k < K3_UNROLL; ++k) {  // all loads of the group first (asm keeps program order)
-        vx[k] = ldsf(sa + step * k);
-        vy[k] = ldsf(sa + step * k + K3_YOFF);
-        vz[k] = ldsf(sa + step * k + K3_ZOFF);
-      }
-#pragma unroll
-      for (int k = 0; k < K3_UNROLL; ++k) {
-        // difference form (3 LDS.32, 3 FADD + FMUL + 2 FFMA): d = v - u_i, r^2 = d.d
-        const float dx = vx[k] - fx, dy = vy[k] - fy, dz = vz[k] - fz;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        stsq(qa, sa + step * k);
-        qa = bump_if_less(qa, r2, hi);
-      }
-      sa += step * K3_UNROLL;
-      it += K3_UNROLL;
-      if (__any_sync(0xffffffffu, qa > qlim)) { full = true; break; }
-    }
-    if (!full) {  // remainder (< K3_UNROLL iterations; every queue has room for them)
-      for (; it < iters; ++it) {
-        const float dx = ldsf(sa) - fx, dy = ldsf(sa + K3_YOFF) - fy, dz = ldsf(sa + K3_ZOFF) - fz;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        stsq(qa, sa);
-        qa = bump_if_less(qa, r2, hi);
-        sa += step;
-      }
-    }
-    __syncwarp();
-    eval_pairs_f32<DIGEST>(sm.queue, g, pc, sm, acc, a32, (int)((qa - q0) / K3_QSTRIDE), lane, stage0, u64);  // the single call site
-    qa = q0;
-    if (it >= iters) break;
-  }
-}
-#endif
-
-#if K3_MASK
 // Mask mode.  Lane (i, s) of an i-batch with S streams filters the staged element PAIRS
 // {2k, 2k+1}, k = s, s+S, ... (one "pair step" = one LDS.64 per coordinate: the S lanes of a step
 // read S distinct 8-byte words, one shared-memory wavefront for S <= 2).  Hits are bits of per-lane
@@ -1117,7 +982,7 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
 // already packed for FADD2) and three packed ops give both r^2; hit bits are set with immediates.
 template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 Acc32& a32, int s, int S, int iters, int lane,
+                                                 int s, int S, int iters, int lane,
                                                  const double4* __restrict__ u64) {
   static_assert(32 * K3_MW >= K3_CAP + 32, "hit words must cover one chunk (ceil(K3_CAP / 32) words at S = 1)");
   static_assert(K3_UNROLL % 2 == 0 && 32 % K3_UNROLL == 0, "groups of whole pair steps");
@@ -1187,7 +1052,6 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
   __syncwarp();
   eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step2, lane, stage0, u64);
 }
-#endif
 
 // One warp per block; each warp handles K3_CELLS consecutive cells of one
 // cell layer, so block partials are layer-aligned and their fixed-order sums
@@ -1286,7 +1150,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
       }
       pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
       Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
-      Acc32 a32 = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u};
 
       int e0 = 0;
       while (e0 < nst) {
@@ -1371,7 +1234,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         const int iters = (int)((ctot + S - 1) / S);
         pc.base_off = base_off;
         if constexpr (sizeof(T) == 4) {
-          filter_chunk_f32<DIGEST>(g, pc, sm, acc, a32, s, S, iters, lane, u);
+          filter_chunk_f32<DIGEST>(g, pc, sm, acc, s, S, iters, lane, u);
         } else {
           filter_chunk<T, DIGEST>(g, pc, sm, acc, s, S, iters, lane);
         }
@@ -1379,7 +1242,6 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         e0 = e1;
       }
 
-      if constexpr (sizeof(T) == 4) fold32(acc, a32);
       // combine the S streams of each i: fixed binary tree over s (log2 S shuffle steps)
       for (int o = 1; o < S; o <<= 1) {
         const int src_s = s + o;
