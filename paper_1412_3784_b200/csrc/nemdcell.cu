@@ -284,12 +284,6 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
-  static bool attr_set[2][2] = {{false, false}, {false, false}};
-  bool& as = attr_set[sizeof(T) == 8][DIGEST];
-  if (!as) {
-    CK(cudaFuncSetAttribute(k_pairs<T, DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    as = true;
-  }
   prof_begin(ctx);
   if constexpr (sizeof(T) == 4) {
     const int Gseg = seg_cells(ctx, g);
@@ -297,11 +291,6 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       const int nseg = (g.dims[0] + Gseg - 1) / Gseg;
       const int bpl_s = nseg * g.dims[1];
       const size_t smem_s = sizeof(SgSmem);
-      static bool attr_s[2] = {false, false};
-      if (!attr_s[DIGEST]) {
-        CK(cudaFuncSetAttribute(k_pairs_seg<DIGEST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
-        attr_s[DIGEST] = true;
-      }
       bpl = bpl_s;
       nblocks = bpl * nlay;
       ctx->pair_kernel_used = NC_PK_SEGMENT;
@@ -772,6 +761,23 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
     return fail(nullptr, NC_E_CUDA, std::string("cudaMemset: ") + cudaGetErrorString(e));
   }
   ctx->pol.kind = 0;
+  // kernel attributes once per context (the launch paths set nothing)
+  {
+    struct KA { const void* f; size_t smem; } ka[] = {
+        {(const void*)k_pairs<float, false>, sizeof(K3Smem<float>)},
+        {(const void*)k_pairs<float, true>, sizeof(K3Smem<float>)},
+        {(const void*)k_pairs<double, false>, sizeof(K3Smem<double>)},
+        {(const void*)k_pairs<double, true>, sizeof(K3Smem<double>)},
+        {(const void*)k_pairs_seg<false>, sizeof(SgSmem)},
+        {(const void*)k_pairs_seg<true>, sizeof(SgSmem)}};
+    for (const KA& a : ka) {
+      cudaError_t e = cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
+      if (e != cudaSuccess) {
+        nc_destroy(ctx);
+        return fail(nullptr, NC_E_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+      }
+    }
+  }
   *out = ctx;
   return NC_OK;
 }

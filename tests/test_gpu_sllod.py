@@ -19,23 +19,34 @@ from paper_1412_3784_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(w, q, p, prec, variant, dt, nsteps):
+def run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=None):
+    """SLLOD on the GPU on a side (non-default) stream: one nc_step_sllod call of nsteps or, with
+    per_call = k, nsteps / k calls."""
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
 
+    side = torch.cuda.Stream()
+    torch.cuda.synchronize()
     cl = CellList(variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
-                  capacity=len(q), max_cells=4 * len(q) + 4096)
+                  capacity=len(q), max_cells=4 * len(q) + 4096, stream=side.cuda_stream)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
     if w.policy == "gkr":
         kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
     cl.set_flow(w.A, w.policy, w.t0, **kw)
-    cl.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
-    Ugpu, Wgpu = cl.step(dt, nsteps)
-    qo = torch.empty_like(torch.from_numpy(q)).cuda()
+    qd, pd = torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()
+    qo = torch.empty_like(qd)
     po = torch.empty_like(qo)
+    torch.cuda.synchronize()
+    cl.set_state(qd, pd)
+    if per_call is None:
+        Ugpu, Wgpu = cl.step(dt, nsteps)
+    else:
+        for _ in range(nsteps // per_call):
+            Ugpu, Wgpu = cl.step(dt, per_call)
     n, L, t, gid = cl.get_state(qo, po, want_gid=True)
+    side.synchronize()
     cl.close()
     assert np.array_equal(gid, np.arange(len(q)))
     return qo.double().cpu().numpy(), po.double().cpu().numpy(), L, t, Ugpu
@@ -186,3 +197,20 @@ def test_sllod_general_flow_lattice_reduction(prec, variant):
     assert np.abs(lattice_diff(qg - qo, Lo)).max() < tq
     assert np.abs(pg - po).max() < tp * max(1.0, np.abs(po).max())
     assert Ug == pytest.approx(Uo, rel=1e-9 if prec == "f64" else 1e-5)
+
+
+
+@pytest.mark.parametrize("prec,variant", [("f64", "do"), ("f32", "ds")])
+def test_one_call_equals_stepwise(prec, variant):
+    """One nc_step_sllod call of 20 steps equals 20 calls of one step bit for bit (C2, KR, a
+    remap inside the run): the host-side step state carries nothing between calls."""
+    w = W.make(2, scale=2)
+    nsteps, dt = 20, 0.002
+    w = near_reset(w, nsteps, dt)
+    dty = np.float64 if prec == "f64" else np.float32
+    q = W.positions(w, dtype=dty, k=2)
+    p = W.momenta(w, dtype=dty, k=2)
+    a = run_gpu(w, q, p, prec, variant, dt, nsteps)
+    b = run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[2], b[2]) and a[3] == b[3] and a[4] == b[4]
