@@ -393,6 +393,9 @@ constexpr int K3_STAGE = K3_CAP + 66;  // + up to 2S far sentinels so the filter
 #ifndef K3_QCAP_OVR
 #define K3_QCAP_OVR 48
 #endif
+#ifndef K3_MAXNREG
+#define K3_MAXNREG 0  // nonzero: register cap for k_pairs instead of K3_MINB
+#endif
 #ifndef K3_MINB
 #define K3_MINB 14
 #endif
@@ -400,7 +403,10 @@ typedef uint16_t K3QT;  // queue entries: low 16 bits of shared addresses (see a
 #ifndef K3_STGR
 #define K3_STGR 4  // staging: global loads in flight per lane
 #endif
-constexpr int K3_MW = 15;   // mask words per lane: 32 * K3_MW >= K3_CAP + 32 filter steps of one chunk
+#ifndef K3_MW_OVR
+#define K3_MW_OVR 15
+#endif
+constexpr int K3_MW = K3_MW_OVR;  // hit words per lane (static_assert in filter_chunk_f32: enough for one chunk)
 #ifndef K3_CQ_OVR
 #define K3_CQ_OVR 24
 #endif
@@ -984,7 +990,7 @@ template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                  int s, int S, int iters, int lane,
                                                  const double4* __restrict__ u64) {
-  static_assert(32 * K3_MW >= K3_CAP + 32, "hit words must cover one chunk (ceil(K3_CAP / 32) words at S = 1)");
+  static_assert(16 * K3_MW >= (K3_CAP + 1) / 2, "hit words must cover one chunk (S = 1: ceil(K3_CAP / 2) pair steps)");
   static_assert(K3_UNROLL % 2 == 0 && 32 % K3_UNROLL == 0, "groups of whole pair steps");
   constexpr int G2 = K3_UNROLL / 2;  // pair steps per group
   const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
@@ -1057,7 +1063,11 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
 // cell layer, so block partials are layer-aligned and their fixed-order sums
 // are independent of timing (determinism).  grid = l3 * blocks_per_layer.
 template <typename T, bool DIGEST>
+#if K3_MAXNREG
+__global__ void __maxnreg__(K3_MAXNREG)
+#else
 __global__ void __launch_bounds__(32, K3_MINB)
+#endif
 k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
         const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
