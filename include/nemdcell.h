@@ -162,7 +162,10 @@ nc_status nc_set_state(nc_ctx *ctx, const void *q, const void *p, const int64_t 
  * dt (R19): kick + flow factor, drift with e^{A dt}, box update and remap
  * (P:342, 349, 380, 428, 433), rewrap, cell rebuild, forces, flow
  * factor + kick.  U, W (host, may be NULL) receive the values after the
- * last step.  Errors: NC_E_STATE, NC_E_DEGENERATE, NC_E_NONFINITE,
+ * last step.  The closing half kick of the last step may be held back and
+ * fused into the next call's first kick (same arithmetic, bit for bit);
+ * nc_get_state applies it first, so the state a caller reads is always the
+ * complete step.  Errors: NC_E_STATE, NC_E_DEGENERATE, NC_E_NONFINITE,
  * NC_E_CUDA. */
 nc_status nc_step_sllod(nc_ctx *ctx, double dt, int nsteps, double *U, double W[6]);
 

@@ -1433,6 +1433,12 @@ __device__ __forceinline__ void mv3(const double* E, double x, double y, double 
   oz = E[6] * x + E[7] * y + E[8] * z;
 }
 
+// A deferred closing half kick of a SLLOD step, p <- e^{-A dt/2} p + dt/2 F (what k_kick does)
+struct K3Kick {
+  double Em[9];  // e^{-A dt/2} of the step that deferred it
+  double hd;     // its dt / 2
+};
+
 // p <- E(-dt/2)(p + dt/2 F); q <- E(dt) q + dt E(dt/2) p / m; then K1 on the
 // new box (wrap + key + histogram), in place on q and p.
 #ifndef KDK_MINB
@@ -1441,10 +1447,16 @@ __device__ __forceinline__ void mv3(const double* E, double x, double y, double 
 template <typename T>
 __global__ void __launch_bounds__(256, KDK_MINB) k_kick_drift_key(int64_t n, typename V4<T>::t* __restrict__ q, typename V4<T>::t* __restrict__ p,
                                  const typename V4<T>::t* __restrict__ F, SllodParams sp, const __grid_constant__ Geom g,
-                                 uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts) {
+                                 uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
+                                 int pending = 0, const K3Kick pk = K3Kick{}) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   typename V4<T>::t qi = q[i], pi = p[i], fi = F[i];
+  if (pending) {  // the previous step's closing half kick (k_kick's arithmetic, same F, same rounding)
+    double ax, ay, az;
+    mv3(pk.Em, (double)pi.x, (double)pi.y, (double)pi.z, ax, ay, az);
+    pi = mk4((T)(ax + pk.hd * (double)fi.x), (T)(ay + pk.hd * (double)fi.y), (T)(az + pk.hd * (double)fi.z), (T)0);
+  }
   double hd = 0.5 * sp.dt;
   double px = (double)pi.x + hd * (double)fi.x, py = (double)pi.y + hd * (double)fi.y,
          pz = (double)pi.z + hd * (double)fi.z;

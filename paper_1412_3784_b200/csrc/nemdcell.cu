@@ -67,6 +67,10 @@ struct nc_ctx {
   bool last_resident = false;     // last build used the resident state
   const uint32_t* last_in_gid = nullptr;  // gid of input order (nullptr = identity)
   int last_cpb = 0, last_bpl = 0;
+  // SLLOD: the closing half kick of the last step is deferred (leapfrog-style) into the next
+  // step's kick-drift kernel, or applied by k_kick when the resident state is read
+  bool kick_pending = false;
+  K3Kick pend{};
   int pair_kernel = NC_PK_AUTO;   // nc_set_pair_kernel
   int pair_kernel_used = 0;
   double occ_hint = -1.0;         // slab path: particles per cell of the own layers (auto kernel choice)
@@ -142,6 +146,15 @@ bool is_device_ptr(const void* p) {
   cudaError_t e = cudaPointerGetAttributes(&a, p);
   if (e != cudaSuccess) { cudaGetLastError(); return false; }
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// NC_DEFER_KICK=0 launches k_kick at the end of every step (A/B runs)
+bool defer_kick() {
+  static const bool on = [] {
+    const char* e = getenv("NC_DEFER_KICK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 // Cells per k_pairs block (one warp): more cells amortize the block prologue/epilogue (C4 DO: 4 / 8 /
@@ -482,8 +495,9 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
       k_kick_drift_key<T><<<nblk(n, 256), 256, 0, s>>>(n, (typename V4<T>::t*)ctx->st_q[c],
                                                       (typename V4<T>::t*)ctx->st_p[c],
                                                       (const typename V4<T>::t*)ctx->st_F, sp, g, ctx->key,
-                                                      ctx->slot, ctx->counts);
+                                                      ctx->slot, ctx->counts, ctx->kick_pending ? 1 : 0, ctx->pend);
       LAUNCHED();
+      ctx->kick_pending = false;
       prof_end(ctx, NC_K_WRAPKEY);
     }
     int64_t C = g.ncells;
@@ -513,7 +527,13 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
     st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->st_q[o], ctx->st_gid[o],
                                 (typename V4<T>::t*)ctx->st_F);
     if (st) return st;
-    if (n > 0) {
+    // closing half kick p <- E(-dt/2) p + dt/2 F: deferred into the next step's kick-drift pass
+    // (same arithmetic; k_kick applies it instead when the state is read, see materialize_kick)
+    if (n > 0 && defer_kick()) {
+      for (int e = 0; e < 9; ++e) ctx->pend.Em[e] = sp.Em[e];
+      ctx->pend.hd = 0.5 * dt;
+      ctx->kick_pending = true;
+    } else if (n > 0) {
       prof_begin(ctx);
       k_kick<T><<<nblk(n, 256), 256, 0, s>>>(n, (typename V4<T>::t*)ctx->st_p[o], (const typename V4<T>::t*)ctx->st_F, sp);
       LAUNCHED();
@@ -526,6 +546,29 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
     totals_to_UW(ctx, U, W);
   }
   return NC_OK;
+}
+
+// Apply a deferred closing half kick to the resident momenta (k_kick with the deferring step's
+// E(-dt/2) and dt/2; bitwise what the fused path computes).
+template <typename T>
+nc_status materialize_kick_t(nc_ctx* ctx) {
+  if (!ctx->kick_pending) return NC_OK;
+  const int64_t n = ctx->n_state;
+  SllodParams sp{};
+  for (int e = 0; e < 9; ++e) sp.Em[e] = ctx->pend.Em[e];
+  sp.dt = 2.0 * ctx->pend.hd;
+  ctx->kick_pending = false;
+  if (n > 0) {
+    prof_begin(ctx);
+    k_kick<T><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (typename V4<T>::t*)ctx->st_p[ctx->cur],
+                                                      (const typename V4<T>::t*)ctx->st_F, sp);
+    LAUNCHED();
+    prof_end(ctx, NC_K_KICK);
+  }
+  return NC_OK;
+}
+nc_status materialize_kick(nc_ctx* ctx) {
+  return ctx->cfg.prec == NC_F32 ? materialize_kick_t<float>(ctx) : materialize_kick_t<double>(ctx);
 }
 
 template <typename T>
@@ -880,6 +923,7 @@ nc_status nc_set_state(nc_ctx* ctx, const void* q, const void* p, const int64_t*
   if (gid)
     for (int64_t i = 0; i < n; ++i)
       if (gid[i] < 0 || gid[i] > 0xFFFFFFFFLL) return fail(ctx, NC_E_ARG, "gid out of range");
+  ctx->kick_pending = false;  // the new state replaces the momenta the deferred kick belonged to
   return ctx->cfg.prec == NC_F32 ? set_state_t<float>(ctx, q, p, gid, n) : set_state_t<double>(ctx, q, p, gid, n);
 }
 
@@ -893,6 +937,10 @@ nc_status nc_step_sllod(nc_ctx* ctx, double dt, int nsteps, double* U, double W[
 nc_status nc_get_state(nc_ctx* ctx, void* q, void* p, int64_t* gid, int64_t* n, double L[9], double* t) {
   if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
   if (!ctx->have_state) return fail(ctx, NC_E_STATE, "no resident state");
+  {
+    nc_status mst = materialize_kick(ctx);
+    if (mst) return mst;
+  }
   int64_t m = ctx->n_state;
   int c = ctx->cur;
   nc_status st;
