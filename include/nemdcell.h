@@ -117,6 +117,8 @@ typedef struct {
     double acc_evals;          /* force evaluations since the last nc_profile(ctx, 1) */
     double acc_interactions;   /* their summed interactions */
     double acc_candidates;     /* their summed candidates */
+    double interactions_fp32;  /* of interactions: evaluated in the fp32 far tier (counted in nc_profile mode 3 only) */
+    double acc_interactions_fp32; /* their summed fp32-tier interactions (roofline accounting) */
 } nc_stats;
 
 /* Create a context on cfg->device; allocates all buffers for cfg->capacity
@@ -194,7 +196,9 @@ nc_status nc_get_stats(nc_ctx *ctx, nc_stats *out);
 nc_status nc_get_stencil_histogram(nc_ctx *ctx, int64_t hist[64]);
 
 /* Live per-kernel timing with CUDA events recorded on cfg.stream around
- * every launch of the path (enable = 1 starts a fresh accumulation, 0 stops).
+ * every launch of the path (enable = 1 starts a fresh accumulation, 0 stops;
+ * enable = 3 also makes k_pairs count its fp32-tier interactions, reported in
+ * nc_stats.interactions_fp32 -- a separate, ~1% slower instantiation).
  * nc_profile_read synchronizes the stream and returns, per kernel id
  * (NC_K_*), the summed device milliseconds and the launch counts. */
 enum { NC_K_WRAPKEY = 0, NC_K_SCAN = 1, NC_K_SCATTER = 2, NC_K_RANKGATHER = 3, NC_K_PAIRS = 4, NC_K_REDUCE = 5,
@@ -244,9 +248,10 @@ nc_status nc_slab_halo(nc_ctx *ctx, void *q, const uint32_t *gid, int64_t n, int
 
 /* Forces on the n_own own particles (output F in their input order) with the
  * halo records received from the lower and upper neighbour; K3 runs over the
- * own layers [klo, khi) only.  layer_parts (host, (khi-klo) x 12 doubles, may
+ * own layers [klo, khi) only.  layer_parts (host, (khi-klo) x 13 doubles, may
  * be NULL) receives the per-layer partials (U, W0..W5, interactions,
- * candidates, stencil cells, rechecks, non-finite) for nc_slab_reduce. */
+ * candidates, stencil cells, rechecks, fp32-tier interactions, non-finite)
+ * for nc_slab_reduce. */
 nc_status nc_slab_forces(nc_ctx *ctx, const void *q, const uint32_t *gid, int64_t n_own, const void *halo_from_lo,
                          int64_t n_lo, const void *halo_from_hi, int64_t n_hi, int klo, int khi, void *F,
                          double *layer_parts);

@@ -459,6 +459,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     else if (lane == 8) v = tC;
     else if (lane == 9) v = tS;
     else if (lane == 10) v = tR;
+    else if (lane == 11) v = 0.0;  // every interaction of this kernel is evaluated in fp64
     else v = tNF;
     sm.part[wid][lane] = v;
   }

@@ -425,7 +425,7 @@ constexpr int K3_CELLS = K3_CELLS_OVR;  // fewest cells per warp (= per block: o
 #ifndef K3_CELLS_MAX
 #define K3_CELLS_MAX 16  // most cells per block (large layers; host cells_per_block)
 #endif
-constexpr int NPART = 12;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, nonfinite
+constexpr int NPART = 13;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, fp32-tier interactions, nonfinite
 constexpr double K3_BAND64 = 1e-12;
 
 template <typename T>
@@ -913,8 +913,9 @@ __device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_
 // to the fp64 tier whenever some lane's queue is nearly full, and at the end.
 template <bool DIGEST>
 __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 int qits, int nhit, int nw, uint32_t sa0, uint32_t step2, int lane,
-                                                 uint32_t stage0, const double4* __restrict__ u64) {
+                                                 uint32_t& nfar, int qits, int nhit, int nw, uint32_t sa0,
+                                                 uint32_t step2, int lane, uint32_t stage0,
+                                                 const double4* __restrict__ u64) {
   // qits = this lane's hits + empty words (an empty word costs one idle pop)
   const int qmax = __reduce_max_sync(0xffffffffu, qits);
   const float split2 = g.f_split2, lo32 = g.f_lo;
@@ -969,6 +970,7 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
   __syncwarp();
   const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
   acc.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
+  nfar += (uint32_t)(nhit - nclose_all - nclose);      // this lane's fp32-tier count (roofline accounting)
   eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
 }
 
@@ -988,7 +990,7 @@ __device__ __forceinline__ uint64_t lds64(uint32_t a) {
 // already packed for FADD2) and three packed ops give both r^2; hit bits are set with immediates.
 template <bool DIGEST>
 __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 int s, int S, int iters, int lane,
+                                                 uint32_t& nfar, int s, int S, int iters, int lane,
                                                  const double4* __restrict__ u64) {
   static_assert(16 * K3_MW >= (K3_CAP + 1) / 2, "hit words must cover one chunk (S = 1: ceil(K3_CAP / 2) pair steps)");
   static_assert(K3_UNROLL % 2 == 0 && 32 % K3_UNROLL == 0, "groups of whole pair steps");
@@ -1056,13 +1058,13 @@ __device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<fl
     put(m << (32 - 2 * rem));
   }
   __syncwarp();
-  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, qlen, nhit, w, sa0, step2, lane, stage0, u64);
+  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, nfar, qlen, nhit, w, sa0, step2, lane, stage0, u64);
 }
 
 // One warp per block; each warp handles K3_CELLS consecutive cells of one
 // cell layer, so block partials are layer-aligned and their fixed-order sums
 // are independent of timing (determinism).  grid = l3 * blocks_per_layer.
-template <typename T, bool DIGEST>
+template <typename T, bool DIGEST, bool COUNT = false>
 #if K3_MAXNREG
 __global__ void __maxnreg__(K3_MAXNREG)
 #else
@@ -1093,6 +1095,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   pc.gid = gid;
 
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+  uint32_t tFu = 0;  // this lane's fp32-tier interactions (< 2^32 per lane)
   if constexpr (sizeof(T) == 4) {
     // 16-bit queue entries decode without a carry only if the block's shared memory sits in one 64 KB page
     if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
@@ -1244,7 +1247,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         const int iters = (int)((ctot + S - 1) / S);
         pc.base_off = base_off;
         if constexpr (sizeof(T) == 4) {
-          filter_chunk_f32<DIGEST>(g, pc, sm, acc, s, S, iters, lane, u);
+          filter_chunk_f32<DIGEST>(g, pc, sm, acc, tFu, s, S, iters, lane, u);
         } else {
           filter_chunk<T, DIGEST>(g, pc, sm, acc, s, S, iters, lane);
         }
@@ -1301,6 +1304,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
   tI = warp_sum_d(tI);
   tR = warp_sum_d(tR);
+  // fp32-tier interactions only in the counting instantiation (nc_profile mode 2): the counter's
+  // register costs the hot kernel ~1%
+  const double tF = COUNT ? warp_sum_d((double)tFu) : 0.0;
   tNF = warp_sum_d(tNF);
   if (lane < NPART) {
     double v = 0;
@@ -1315,6 +1321,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     else if (lane == 8) v = tC;
     else if (lane == 9) v = tS;
     else if (lane == 10) v = tR;
+    else if (lane == 11) v = tF;
     else v = tNF;
     bpart[(int64_t)blockIdx.x * NPART + lane] = v;
   }

@@ -70,6 +70,7 @@ struct nc_ctx {
   // SLLOD: the closing half kick of the last step is deferred (leapfrog-style) into the next
   // step's kick-drift kernel, or applied by k_kick when the resident state is read
   bool kick_pending = false;
+  bool count_tiers = false;  // nc_profile mode 2: k_pairs counts its fp32-tier interactions
   K3Kick pend{};
   int pair_kernel = NC_PK_AUTO;   // nc_set_pair_kernel
   int pair_kernel_used = 0;
@@ -312,8 +313,12 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                                                       nseg, bpl, layer0);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
-      k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
-                                                   ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+      if (!DIGEST && ctx->count_tiers)
+        k_pairs<T, DIGEST, true><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
+                                                           ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+      else
+        k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
+                                                     ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
     }
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
@@ -363,7 +368,7 @@ void totals_to_UW(const nc_ctx* ctx, double* U, double* W) {
 nc_status check_finite(nc_ctx* ctx) {
   nc_status st = fetch_totals(ctx);
   if (st) return st;
-  bool ok = ctx->host_tot[11] == 0.0;
+  bool ok = ctx->host_tot[NPART - 1] == 0.0;
   for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
   if (!ok) return fail(ctx, NC_E_NONFINITE, "non-finite force, energy or virial");
   return NC_OK;
@@ -724,6 +729,7 @@ nc_status nc_profile(nc_ctx* ctx, int enable) {
     CK(cudaMemsetAsync(ctx->part_acc, 0, sizeof(double) * (NPART + 1), ctx->stream));
   }
   ctx->prof = enable != 0;
+  ctx->count_tiers = (enable & 2) != 0;
   if (enable) ctx->prof_ev.reserve(4096);
   return NC_OK;
 }
@@ -808,6 +814,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
   {
     struct KA { const void* f; size_t smem; } ka[] = {
         {(const void*)k_pairs<float, false>, sizeof(K3Smem<float>)},
+        {(const void*)k_pairs<float, false, true>, sizeof(K3Smem<float>)},
         {(const void*)k_pairs<float, true>, sizeof(K3Smem<float>)},
         {(const void*)k_pairs<double, false>, sizeof(K3Smem<double>)},
         {(const void*)k_pairs<double, true>, sizeof(K3Smem<double>)},
@@ -1028,6 +1035,8 @@ nc_status nc_get_stats(nc_ctx* ctx, nc_stats* out) {
   out->acc_evals = acc[NPART];
   out->acc_interactions = acc[7];
   out->acc_candidates = acc[8];
+  out->interactions_fp32 = ctx->host_tot[11];
+  out->acc_interactions_fp32 = acc[11];
   return NC_OK;
 }
 
@@ -1194,7 +1203,7 @@ nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* 
   }
   ctx->tot_valid = true;
   ctx->have_eval = true;
-  bool ok = ctx->host_tot[11] == 0.0;
+  bool ok = ctx->host_tot[NPART - 1] == 0.0;
   for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
   totals_to_UW(ctx, U, W);
   if (stats) { stats[0] = ctx->host_tot[7]; stats[1] = ctx->host_tot[8]; stats[2] = ctx->host_tot[9]; stats[3] = ctx->host_tot[10]; }

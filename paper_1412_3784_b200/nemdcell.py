@@ -52,12 +52,16 @@ class nc_remap(ctypes.Structure):
                 ("eps", ctypes.c_double)]
 
 
+NPART = 13  # per-layer partials: U, W0..W5, interactions, candidates, stencil cells, rechecks, fp32-tier interactions, non-finite
+
+
 class nc_stats(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("dims", ctypes.c_int32 * 3), ("ncells", ctypes.c_int64),
                 ("candidates", ctypes.c_double), ("interactions", ctypes.c_double),
                 ("stencil_cells", ctypes.c_double), ("rechecks", ctypes.c_double), ("U", ctypes.c_double),
                 ("W", ctypes.c_double * 6), ("acc_evals", ctypes.c_double), ("acc_interactions", ctypes.c_double),
-                ("acc_candidates", ctypes.c_double)]
+                ("acc_candidates", ctypes.c_double), ("interactions_fp32", ctypes.c_double),
+                ("acc_interactions_fp32", ctypes.c_double)]
 
 
 _lib = None
@@ -224,7 +228,8 @@ def nc_get_stats(ctx) -> dict:
     return {"n": s.n, "dims": tuple(s.dims), "ncells": s.ncells, "candidates": s.candidates,
             "interactions": s.interactions, "stencil_cells": s.stencil_cells, "rechecks": s.rechecks,
             "U": s.U, "W": np.array(list(s.W)), "acc_evals": s.acc_evals, "acc_interactions": s.acc_interactions,
-            "acc_candidates": s.acc_candidates}
+            "acc_candidates": s.acc_candidates, "interactions_fp32": s.interactions_fp32,
+            "acc_interactions_fp32": s.acc_interactions_fp32}
 
 
 def nc_get_stencil_histogram(ctx) -> np.ndarray:
@@ -242,8 +247,10 @@ def nc_pair_kernel_used(ctx) -> str:
     return {0: "none", 1: "cell", 2: "segment"}[load().nc_pair_kernel_used(ctx)]
 
 
-def nc_profile(ctx, enable: bool) -> None:
-    _check(ctx, load().nc_profile(ctx, 1 if enable else 0))
+def nc_profile(ctx, enable) -> None:
+    """enable: False / True, or the mode (3 = timing + fp32-tier interaction counts)."""
+    mode = int(enable) if not isinstance(enable, bool) else (1 if enable else 0)
+    _check(ctx, load().nc_profile(ctx, mode))
 
 
 def nc_profile_read(ctx) -> dict:
@@ -285,7 +292,7 @@ def nc_slab_halo(ctx, q, gid, n, klo, khi, halo_lo, halo_hi, cap):
 
 
 def nc_slab_forces(ctx, q, gid, n_own, h_lo, n_lo, h_hi, n_hi, klo, khi, F, want_parts=True):
-    parts = np.zeros((khi - klo, 12)) if want_parts else None
+    parts = np.zeros((khi - klo, NPART)) if want_parts else None
     _check(ctx, load().nc_slab_forces(ctx, _ptr(q), _ptr(gid), int(n_own), _ptr(h_lo), int(n_lo), _ptr(h_hi),
                                       int(n_hi), int(klo), int(khi), _ptr(F), _ptr(parts)))
     return parts

@@ -29,7 +29,7 @@ import numpy as np
 
 from . import nemdcell as nc
 
-NPART = 12
+NPART = 13
 
 
 class SlabRank:

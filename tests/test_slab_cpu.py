@@ -92,7 +92,9 @@ class NumpyRank:
         self.F = r.F
         self.halo_gids = np.concatenate([h_lo[:n_lo, 3].numpy(), h_hi[:n_hi, 3].numpy()]).astype(np.int64)
         lay = self._layer(self.q) - klo
-        parts = np.zeros((khi - klo, 12))
+        from paper_1412_3784_b200.slab import NPART
+
+        parts = np.zeros((khi - klo, NPART))
         np.add.at(parts[:, 0], lay, r.U_i)
         for k in range(6):
             np.add.at(parts[:, 1 + k], lay, r.W_i[:, k])
