@@ -268,6 +268,54 @@ def run_slab(args):
     ms_max = float(tmax[0])
     inter = float(t[1])
     value = inter / 2.0 / (ms_max * 1e-3)
+
+    # roofline of rank 0's pair kernel (its own cells: flops from its stats, time from its events)
+    evals = max(st["acc_evals"], 1)
+    pairs_ms, pairs_n = prof["pairs"]
+    cand0, inter0 = st["acc_candidates"] / evals, st["acc_interactions"] / evals
+    sr.cl.profile(3)  # one untimed step with k_pairs' tier counting (all ranks step together)
+    with torch.cuda.stream(stream):
+        sysm.step(w.dt, False)
+    stream.synchronize()
+    st3 = sr.cl.stats()
+    sr.cl.profile(False)
+    split = st3["acc_interactions_fp32"] / max(st3["acc_interactions"], 1.0)
+    nsm = torch.cuda.get_device_properties(lrank).multi_processor_count
+    fmax = (load_peaks().get("sm_max_mhz") or 1965.0) * 1e6
+    p32 = nsm * 128 * 2 * fmax
+    p64 = p32 / 2.0
+    flops0 = 9.0 * cand0 + 30.0 * inter0
+    t_bound = (9.0 * cand0 + 30.0 * inter0 * split) / p32 + 30.0 * inter0 * (1.0 - split) / p64
+    achieved = flops0 / (pairs_ms / max(pairs_n, 1) * 1e-3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": flops0 / t_bound / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / (flops0 / t_bound / 1e12), "traffic": None, "kernel": "k_pairs (rank 0)",
+            "kernel_ms": pairs_ms / max(pairs_n, 1),
+            "peak_note": f"FP32/FP64 blend as the 1-GPU line; {split:.1%} of rank 0's interactions in the fp32 tier"}
+
+    # end to end through the slab API: every step each rank copies its own positions from pinned
+    # host memory into its resident buffer, runs the halo exchange + forces, and reads F back
+    n_own = sr.n
+    qh = torch.empty((n_own, 3), dtype=torch.float32, pin_memory=True)
+    Fh = torch.empty((n_own, 3), dtype=torch.float32, pin_memory=True)
+    qh.copy_(sr.q[:n_own])
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(args.steps):
+            sr.q[:n_own].copy_(qh, non_blocking=True)
+            sysm.forces(False)
+            Fh.copy_(sr.F[:n_own], non_blocking=True)
+        e1.record(stream)
+    e1.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=f"cuda:{lrank}")
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = {"value": inter / 2.0 / (float(te[0]) * 1e-3),  # as many evaluations as the timed steps
+           "unit": UNIT, "h2d_bytes_per_step": int(12 * w.n), "d2h_bytes_per_step": int(12 * w.n),
+           "call": "slab forces from host q to host F (all ranks; H2D/D2H of each rank's own particles)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -280,7 +328,7 @@ def run_slab(args):
                                                                    "NCCL P2P halo + migration"},
             "particle_steps_per_s": w.n * args.steps / (ms_max * 1e-3),
             "kernel_ms_per_step_rank0": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
-            "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": int(t[3]), "clocks": clocks,
+            "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(t[3]), "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     sr.close()
