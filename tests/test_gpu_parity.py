@@ -285,3 +285,35 @@ def test_dense_cluster_stress(variant, prec):
     w, q = _cluster_workload(prec)
     g, r = check_against_oracle(w, q, variant, prec, kernel="cell")
     assert r.interactions > 100000  # the cluster really is dense
+
+
+def test_tier_counting_mode():
+    """nc_profile mode 3 runs k_pairs' counting instantiation: the fp32-tier share of the
+    interactions is reported, the results equal the plain kernel's bit for bit, and fp64 /
+    sparse-cell (all-fp64) evaluations report no fp32-tier interactions."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w, q = inputs(2, "f32", scale=2)
+    qt = torch.from_numpy(q).cuda()
+    cl = CellList("do", "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    cl.set_box(w.L)
+    F0, U0, W0 = cl.compute_forces(qt)
+    cl.profile(3)
+    F1, U1, W1 = cl.compute_forces(qt)
+    st = cl.stats()
+    cl.profile(False)
+    cl.close()
+    assert torch.equal(F0, F1) and U0 == U1 and np.array_equal(W0, W1)
+    assert 0.5 * st["interactions"] < st["interactions_fp32"] < st["interactions"]
+    assert st["acc_interactions_fp32"] == st["interactions_fp32"]
+    for prec, k in (("f64", 2), ("f32", 1)):
+        w, q = inputs(k, prec, scale=2)
+        cl = CellList("do", prec, rc=w.rc, u_shift=w.ushift, capacity=len(q))
+        cl.set_box(w.L)
+        cl.profile(3)
+        cl.compute_forces(torch.from_numpy(q).cuda())
+        st = cl.stats()
+        cl.profile(False)
+        cl.close()
+        assert st["interactions"] > 0 and st["interactions_fp32"] == 0
