@@ -39,6 +39,7 @@ struct SgSmem {
   uint16_t sent[SG_CAP];                    // entry of each staged element
   uint8_t e_row[SG_MAXE];
   uint8_t e_ci[SG_MAXE];                    // column index inside the row's union range
+  int8_t e_nx[SG_MAXE];                     // x image shift floor(col / l1) of the entry's column
   uint16_t rg[SG_GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
   uint16_t queue[SG_NW][SG_QCAP][32];
   uint32_t wtot[SG_NW][SG_ROWS];            // per-warp row totals (block scan)
@@ -152,6 +153,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
       const int col = sm.r_lo[r] + tid;
       const int nx = floordiv(col, l1);
       const uint32_t cell = (uint32_t)sm.r_base[r] + (uint32_t)(col - nx * l1);
+      sm.e_nx[sm.r_eb[r] + tid] = (int8_t)nx;
       est[r] = cs[cell];
       ecn[r] = cs[cell + 1];
       const int e = sm.r_eb[r] + tid;
@@ -216,7 +218,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
       if (tt[r] < tot) {
         const int row = sm.e_row[ee[r]];
         const int col = sm.r_lo[row] + sm.e_ci[ee[r]];
-        const int nx = floordiv(col, l1);
+        const int nx = sm.e_nx[ee[r]];
         const float bx = (float)(col - A) * wx + (float)nx * ex + sm.r_bf[row][0];
         sm.stage[tt[r]] = make_float4(pp[r].x + bx, pp[r].y + sm.r_bf[row][1], pp[r].z + sm.r_bf[row][2],
                                       __uint_as_float(jj[r]));
@@ -258,7 +260,6 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
                                         uint32_t nh_i, int A, double uix, double uiy, double uiz, double wx64,
                                         double lo64, double hi64, Acc& acc) {
   const int qmax = __reduce_max_sync(0xffffffffu, nq);
-  const int l1 = g.dims[0];
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   for (int q0 = 0; q0 < qmax; q0 += 4) {
     uint32_t jj[4];
@@ -278,7 +279,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
       const uint32_t j = jj[h];
       const int row = sm.e_row[ee[h]];
       const int col = sm.r_lo[row] + sm.e_ci[ee[h]];
-      const int nx = floordiv(col, l1);
+      const int nx = sm.e_nx[ee[h]];
       const double bx = (double)(col - A) * wx64 + (g.variant == 1 ? (double)nx * g.e[0] : 0.0) + sm.r_b[row][0];
       const double dx = (uj[h].x + bx) - uix, dy = (uj[h].y + sm.r_b[row][1]) - uiy,
                    dz = (uj[h].z + sm.r_b[row][2]) - uiz;
