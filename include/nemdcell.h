@@ -48,10 +48,13 @@ typedef enum {
     NC_DO = 1  /* dynamic offset: QR-rotated rectangular cells, l_k = floor(r_kk/d_cut), 27/30/34/36 */
 } nc_variant;
 
-/* Storage and pair-arithmetic precision.  NC_F32 keeps fp32 positions and
- * evaluates pairs in fp32 with an fp64 re-check of every candidate whose
- * fp32 r^2 lies within a relative band of r_c^2, so the pair SET is the
- * canonical fp64 one (R16).  NC_F64 does everything in fp64. */
+/* Storage and pair-arithmetic precision.  NC_F32 keeps fp32 positions,
+ * filters candidates in fp32 (superset bound r^2 < r_c^2 (1 + 1e-4)),
+ * evaluates pairs with r >= 1.2 sigma below the band in fp32 and closer
+ * pairs and every candidate whose r^2 lies in the band around r_c^2 in fp64
+ * from fp64 cell-local coordinates, the band ones by the canonical test, so
+ * the pair SET is the canonical fp64 one (R16).
+ * Forces, U and W are accumulated in fp64.  NC_F64 does everything in fp64. */
 typedef enum { NC_F32 = 0, NC_F64 = 1 } nc_prec;
 
 typedef enum {
