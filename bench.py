@@ -395,11 +395,20 @@ def run_ours(args):
     time.sleep(0.3)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # one event per call boundary as well (median and min per step beside the mean)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev0.record(stream)
-    run_steps(args.steps)
+    if spc == 1:
+        evs[0].record(stream)
+        for k in range(args.steps):
+            cl.step(dt, 1, want_uw=False)
+            evs[k + 1].record(stream)
+    else:
+        run_steps(args.steps)
     ev1.record(stream)
     ev1.synchronize()
     torch.cuda.synchronize()
+    per_step = sorted(evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)) if spc == 1 else []
     barrier()
     clocks = sampler.stop()
     ms_total = ev0.elapsed_time(ev1)
@@ -490,6 +499,8 @@ def run_ours(args):
                                      else "fp64 throughout"),
                        "l2": l2_text(w.n), "parallelism": f"replicas x{ws}", "steps_per_call": spc},
             "particle_steps_per_s": psteps,
+            "ms_per_step_median": per_step[len(per_step) // 2] if per_step else None,
+            "ms_per_step_min": per_step[0] if per_step else None,
             "interactions_per_particle": inter / w.n, "candidates_per_particle": cand / w.n,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "k_pairs",
