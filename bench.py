@@ -471,15 +471,22 @@ def run_ours(args):
         cl.set_box(cl_box(cl))
         cl.compute_forces(qh, Fh)  # warm-up
         torch.cuda.synchronize()
-        reps = max(1, min(3, args.steps))
+        # pipelined host-buffer API: each call copies q in and F out on the library's copy streams,
+        # overlapping the neighbouring calls' evaluations; the last call's U, W at the sync
+        reps = max(3, args.steps)
+        cl.compute_forces_async(qh, Fh)  # warm-up of the async buffers
+        cl.compute_sync()
         t0 = time.perf_counter()
         for _ in range(reps):
-            _, Ue, _ = cl.compute_forces(qh, Fh)
+            cl.compute_forces_async(qh, Fh)
+        Ue, _ = cl.compute_sync()
         t1 = time.perf_counter()
         se = cl.stats()
         e2e = {"value": (se["interactions"] / 2.0) / ((t1 - t0) / reps), "unit": UNIT,
-               "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(Fh.numel() * Fh.element_size() + 8 + 48),
-               "call": "nc_compute_forces(host q -> host F, U, W)"}
+               "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(Fh.numel() * Fh.element_size()),
+               "calls": reps,
+               "call": f"{reps} x nc_compute_forces_async(pinned host q -> pinned host F) + nc_compute_sync (U, W "
+                       f"of the last); wall clock over the calls, copies inside"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

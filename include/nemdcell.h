@@ -158,6 +158,19 @@ nc_status nc_build_cells(nc_ctx *ctx, const void *q, int64_t n);
  * nc_build_cells, plus NC_E_NONFINITE. */
 nc_status nc_compute_forces(nc_ctx *ctx, const void *q, int64_t n, void *F, double *U, double W[6]);
 
+/* Pipelined force evaluations on HOST buffers (pinned memory for the copies
+ * to overlap): the H2D copy of q runs on a library copy stream, the
+ * evaluation on cfg.stream, the D2H copy of F on a second copy stream, with
+ * double-buffered device staging, and the call returns without waiting, so
+ * the copies of consecutive calls overlap the neighbouring evaluations.
+ * q and F (n x 3, host) must stay valid, and F unread, until
+ * nc_compute_sync, which waits for every pending evaluation and returns U and
+ * W (may be NULL) of the LAST one; a non-finite result of any earlier one is
+ * not reported.  Errors: as nc_compute_forces, plus NC_E_ARG for device
+ * pointers and NC_E_STATE for nc_compute_sync without a pending call. */
+nc_status nc_compute_forces_async(nc_ctx *ctx, const void *q, int64_t n, void *F);
+nc_status nc_compute_sync(nc_ctx *ctx, double *U, double W[6]);
+
 /* Load the resident particle state: positions q and PECULIAR momenta p
  * (n x 3, device or host, R19), particle ids gid (int64, may be NULL for
  * 0..n-1).  Computes the initial forces.  Errors: as nc_compute_forces. */

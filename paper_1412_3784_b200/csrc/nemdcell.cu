@@ -69,6 +69,15 @@ struct nc_ctx {
   int last_cpb = 0, last_bpl = 0;
   // SLLOD: the closing half kick of the last step is deferred (leapfrog-style) into the next
   // step's kick-drift kernel, or applied by k_kick when the resident state is read
+  // pipelined host-buffer evaluations (nc_compute_forces_async): copy streams, double-buffered
+  // device staging, events ordering copy-in -> evaluation -> copy-out per buffer
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  void* ain[2] = {nullptr, nullptr};
+  void* aout[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in_ready[2] = {}, ev_in_free[2] = {}, ev_out_ready[2] = {}, ev_out_free[2] = {};
+  bool ab_used[2] = {false, false};
+  int ab = 0;
+  bool async_eval = false;  // an evaluation was enqueued by the async call and not yet synced
   bool kick_pending = false;
   bool count_tiers = false;  // nc_profile mode 2: k_pairs counts its fp32-tier interactions
   K3Kick pend{};
@@ -423,6 +432,52 @@ nc_status compute_user(nc_ctx* ctx, const void* q, int64_t n, void* F, double* U
   st = check_finite(ctx);  // synchronizes the stream
   if (st) return st;
   totals_to_UW(ctx, U, W);
+  return NC_OK;
+}
+
+// Pipelined evaluation on host buffers: H2D on s_h2d, evaluation on the context stream, D2H on
+// s_d2h, buffer b alternating, so the copies of one call overlap the evaluation of its neighbours.
+template <typename T>
+nc_status compute_async_t(nc_ctx* ctx, const void* q, int64_t n, void* F) {
+  const size_t bytes = 3 * sizeof(T) * (size_t)n;
+  if (!ctx->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&ctx->ain[b], 3 * sizeof(T) * (size_t)ctx->cap));
+      CK(cudaMalloc(&ctx->aout[b], 3 * sizeof(T) * (size_t)ctx->cap));
+      CK(cudaEventCreateWithFlags(&ctx->ev_in_ready[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_in_free[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_out_ready[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_out_free[b], cudaEventDisableTiming));
+    }
+  }
+  const int b = ctx->ab;
+  ctx->ab ^= 1;
+  cudaStream_t s = ctx->stream;
+  // copy in (after the evaluation that last read this buffer)
+  if (ctx->ab_used[b]) CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[b], 0));
+  if (n > 0) CK(cudaMemcpyAsync(ctx->ain[b], q, bytes, cudaMemcpyHostToDevice, ctx->s_h2d));
+  CK(cudaEventRecord(ctx->ev_in_ready[b], ctx->s_h2d));
+  // evaluate (device pointers: no staging through io_a / io_b)
+  CK(cudaStreamWaitEvent(s, ctx->ev_in_ready[b], 0));
+  if (ctx->ab_used[b]) CK(cudaStreamWaitEvent(s, ctx->ev_out_free[b], 0));
+  nc_status st = build_user<T>(ctx, ctx->ain[b], n);
+  if (st) return st;
+  CK(cudaEventRecord(ctx->ev_in_free[b], s));
+  st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF);
+  if (st) return st;
+  if (F) {
+    st = unsort_out<T>(ctx, ctx->sF, ctx->sgid, n, ctx->aout[b]);
+    if (st) return st;
+  }
+  CK(cudaEventRecord(ctx->ev_out_ready[b], s));
+  // copy out
+  CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[b], 0));
+  if (F && n > 0) CK(cudaMemcpyAsync(F, ctx->aout[b], bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+  CK(cudaEventRecord(ctx->ev_out_free[b], ctx->s_d2h));
+  ctx->ab_used[b] = true;
+  ctx->async_eval = true;
   return NC_OK;
 }
 
@@ -842,6 +897,20 @@ void nc_destroy(nc_ctx* ctx) {
                 ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot};
   for (void* p : ps)
     if (p) cudaFree(p);
+  if (ctx->s_h2d) {
+    cudaStreamSynchronize(ctx->s_h2d);
+    cudaStreamSynchronize(ctx->s_d2h);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(ctx->ain[b]);
+      cudaFree(ctx->aout[b]);
+      cudaEventDestroy(ctx->ev_in_ready[b]);
+      cudaEventDestroy(ctx->ev_in_free[b]);
+      cudaEventDestroy(ctx->ev_out_ready[b]);
+      cudaEventDestroy(ctx->ev_out_free[b]);
+    }
+    cudaStreamDestroy(ctx->s_h2d);
+    cudaStreamDestroy(ctx->s_d2h);
+  }
   for (auto& p : ctx->prof_ev) {
     cudaEventDestroy(p.second.first);
     cudaEventDestroy(p.second.second);
@@ -921,6 +990,26 @@ nc_status nc_compute_forces(nc_ctx* ctx, const void* q, int64_t n, void* F, doub
   if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box first");
   if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
   return ctx->cfg.prec == NC_F32 ? compute_user<float>(ctx, q, n, F, U, W) : compute_user<double>(ctx, q, n, F, U, W);
+}
+
+nc_status nc_compute_forces_async(nc_ctx* ctx, const void* q, int64_t n, void* F) {
+  if (!ctx || (!q && n > 0)) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box first");
+  if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
+  if ((q && is_device_ptr(q)) || (F && is_device_ptr(F)))
+    return fail(ctx, NC_E_ARG, "nc_compute_forces_async takes host buffers (device ones: nc_compute_forces)");
+  return ctx->cfg.prec == NC_F32 ? compute_async_t<float>(ctx, q, n, F) : compute_async_t<double>(ctx, q, n, F);
+}
+
+nc_status nc_compute_sync(nc_ctx* ctx, double* U, double W[6]) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (ctx->s_d2h) CK(cudaStreamSynchronize(ctx->s_d2h));
+  if (!ctx->async_eval) return fail(ctx, NC_E_STATE, "no pending nc_compute_forces_async");
+  ctx->async_eval = false;
+  nc_status st = check_finite(ctx);  // synchronizes the context stream
+  if (st) return st;
+  totals_to_UW(ctx, U, W);
+  return NC_OK;
 }
 
 nc_status nc_set_state(nc_ctx* ctx, const void* q, const void* p, const int64_t* gid, int64_t n) {

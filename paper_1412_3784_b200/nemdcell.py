@@ -23,6 +23,7 @@ STATUS = {0: "NC_OK", 1: "NC_E_ARG", 2: "NC_E_BOX", 3: "NC_E_DEGENERATE", 4: "NC
           6: "NC_E_CUDA", 7: "NC_E_NCCL", 8: "NC_E_OOM", 9: "NC_E_NONFINITE"}
 
 EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cells", "nc_compute_forces",
+           "nc_compute_forces_async", "nc_compute_sync",
            "nc_set_state", "nc_step_sllod", "nc_get_state", "nc_get_cells", "nc_get_pair_digest", "nc_get_stats",
            "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
            "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_migrate", "nc_slab_unpack",
@@ -88,6 +89,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_set_flow.argtypes = [vp, vp, ctypes.POINTER(nc_remap), d]
         L.nc_build_cells.argtypes = [vp, vp, i64]
         L.nc_compute_forces.argtypes = [vp, vp, i64, vp, vp, vp]
+        L.nc_compute_forces_async.argtypes = [vp, vp, i64, vp]
+        L.nc_compute_sync.argtypes = [vp, vp, vp]
         L.nc_set_state.argtypes = [vp, vp, vp, vp, i64]
         L.nc_step_sllod.argtypes = [vp, d, i32, vp, vp]
         L.nc_get_state.argtypes = [vp, vp, vp, vp, vp, vp, vp]
@@ -173,6 +176,17 @@ def nc_set_flow(ctx, A, pol: nc_remap | None, t: float) -> None:
 
 def nc_build_cells(ctx, q, n: int) -> None:
     _check(ctx, load().nc_build_cells(ctx, _ptr(q), int(n)))
+
+
+def nc_compute_forces_async(ctx, q, n: int, F) -> None:
+    _check(ctx, load().nc_compute_forces_async(ctx, _ptr(q), int(n), _ptr(F)))
+
+
+def nc_compute_sync(ctx):
+    U = ctypes.c_double(0.0)
+    W = np.zeros(6)
+    _check(ctx, load().nc_compute_sync(ctx, ctypes.byref(U), _ptr(W)))
+    return U.value, W
 
 
 def nc_compute_forces(ctx, q, n: int, F):
@@ -397,6 +411,14 @@ class CellList:
             F = torch.empty_like(q) if hasattr(q, "data_ptr") and not isinstance(q, np.ndarray) else np.empty_like(q)
         U, W = nc_compute_forces(self.ctx, q, q.shape[0], F)
         return F, U, W
+
+    def compute_forces_async(self, q, F):
+        """Enqueue one evaluation on host buffers (pinned: copies overlap neighbouring calls)."""
+        nc_compute_forces_async(self.ctx, q, q.shape[0], F)
+
+    def compute_sync(self):
+        """Wait for the pending evaluations; U, W of the last one."""
+        return nc_compute_sync(self.ctx)
 
     def set_state(self, q, p=None, gid=None):
         nc_set_state(self.ctx, q, p, gid, q.shape[0])
