@@ -245,6 +245,14 @@ nc_status nc_slab_layers(nc_ctx *ctx, int rank, int nranks, int32_t *klo, int32_
  * to t + dt with its remap.  Positions are wrapped by nc_slab_migrate. */
 nc_status nc_slab_kick_drift(nc_ctx *ctx, void *q, void *p, const void *F, int64_t n, double dt);
 
+/* As nc_slab_kick_drift, preceded in the same pass by the PREVIOUS step's
+ * closing half kick p <- e^{-A dt_prev/2} p + dt_prev/2 F (what nc_slab_kick
+ * would have done with the same F; bitwise the same arithmetic), so a run of
+ * slab steps needs no separate kick pass.  dt_prev = 0: no pending kick.
+ * Errors: as nc_slab_kick_drift, NC_E_ARG for dt_prev < 0. */
+nc_status nc_slab_kick_kick_drift(nc_ctx *ctx, void *q, void *p, const void *F, int64_t n, double dt_prev,
+                                  double dt);
+
 /* Wrap q in place (R15), then split the n particles by layer: those still
  * in [klo, khi) go to q_out/p_out/gid_out (index order), those in layer
  * klo-1 / khi (mod l3) are packed as migration records into send_lo /

@@ -1506,12 +1506,20 @@ __global__ void k_kick(int64_t n, typename V4<T>::t* __restrict__ p, const typen
 // The gid travels as the bit pattern (fp32) or the exact value (fp64) of .w.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void k_kick_drift3(int64_t n, T* __restrict__ q, T* __restrict__ p, const T* __restrict__ F, SllodParams sp) {
+__global__ void k_kick_drift3(int64_t n, T* __restrict__ q, T* __restrict__ p, const T* __restrict__ F, SllodParams sp,
+                              int pending = 0, const K3Kick pk = K3Kick{}) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double hd = 0.5 * sp.dt;
-  double px = (double)p[3 * i] + hd * (double)F[3 * i], py = (double)p[3 * i + 1] + hd * (double)F[3 * i + 1],
-         pz = (double)p[3 * i + 2] + hd * (double)F[3 * i + 2];
+  double p0 = (double)p[3 * i], p1 = (double)p[3 * i + 1], p2 = (double)p[3 * i + 2];
+  if (pending) {  // the previous step's closing half kick (k_kick3's arithmetic, same F, same rounding)
+    double ax, ay, az;
+    mv3(pk.Em, p0, p1, p2, ax, ay, az);
+    p0 = (double)(T)(ax + pk.hd * (double)F[3 * i]);
+    p1 = (double)(T)(ay + pk.hd * (double)F[3 * i + 1]);
+    p2 = (double)(T)(az + pk.hd * (double)F[3 * i + 2]);
+  }
+  double px = p0 + hd * (double)F[3 * i], py = p1 + hd * (double)F[3 * i + 1], pz = p2 + hd * (double)F[3 * i + 2];
   double ax, ay, az, hx, hy, hz, qx, qy, qz;
   mv3(sp.Em, px, py, pz, ax, ay, az);
   mv3(sp.Eh, ax, ay, az, hx, hy, hz);

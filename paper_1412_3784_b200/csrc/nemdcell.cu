@@ -1159,9 +1159,22 @@ nc_status nc_slab_layers(nc_ctx* ctx, int rank, int nranks, int32_t* klo, int32_
 }
 
 nc_status nc_slab_kick_drift(nc_ctx* ctx, void* q, void* p, const void* F, int64_t n, double dt) {
+  return nc_slab_kick_kick_drift(ctx, q, p, F, n, 0.0, dt);
+}
+
+nc_status nc_slab_kick_kick_drift(nc_ctx* ctx, void* q, void* p, const void* F, int64_t n, double dt_prev,
+                                  double dt) {
   if (!ctx || (n > 0 && (!q || !p || !F))) return fail(ctx, NC_E_ARG, "null argument");
   if (!ctx->have_flow && !ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_flow first");
-  if (!(dt > 0)) return fail(ctx, NC_E_ARG, "dt must be > 0");
+  if (!(dt > 0) || dt_prev < 0) return fail(ctx, NC_E_ARG, "dt must be > 0 and dt_prev >= 0");
+  K3Kick pk{};
+  if (dt_prev > 0) {
+    SllodParams pp;
+    sllod_params(ctx, dt_prev, pp);
+    for (int e = 0; e < 9; ++e) pk.Em[e] = pp.Em[e];
+    pk.hd = 0.5 * dt_prev;
+  }
+  const int pending = dt_prev > 0 ? 1 : 0;
   SllodParams sp;
   sllod_params(ctx, dt, sp);
   double Lnew[9];
@@ -1172,9 +1185,11 @@ nc_status nc_slab_kick_drift(nc_ctx* ctx, void* q, void* p, const void* F, int64
   if (n > 0) {
     prof_begin(ctx);
     if (ctx->cfg.prec == NC_F32)
-      k_kick_drift3<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, (float*)p, (const float*)F, sp);
+      k_kick_drift3<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, (float*)p, (const float*)F, sp,
+                                                                    pending, pk);
     else
-      k_kick_drift3<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, (double*)p, (const double*)F, sp);
+      k_kick_drift3<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, (double*)p, (const double*)F, sp,
+                                                                     pending, pk);
     LAUNCHED();
     prof_end(ctx, NC_K_KICK);
   }

@@ -26,7 +26,8 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_compute_forces_async", "nc_compute_sync",
            "nc_set_state", "nc_step_sllod", "nc_get_state", "nc_get_cells", "nc_get_pair_digest", "nc_get_stats",
            "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
-           "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_migrate", "nc_slab_unpack",
+           "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_kick_kick_drift", "nc_slab_migrate",
+           "nc_slab_unpack",
            "nc_slab_halo", "nc_slab_forces", "nc_slab_kick", "nc_slab_reduce", "nc_set_pair_kernel",
            "nc_pair_kernel_used"]
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
@@ -102,6 +103,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_profile_read.argtypes = [vp, vp, vp]
         L.nc_slab_layers.argtypes = [vp, i32, i32, vp, vp, vp]
         L.nc_slab_kick_drift.argtypes = [vp, vp, vp, vp, i64, d]
+        L.nc_slab_kick_kick_drift.argtypes = [vp, vp, vp, vp, i64, d, d]
         L.nc_slab_migrate.argtypes = [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, i64, vp]
         L.nc_slab_unpack.argtypes = [vp, vp, i64, vp, vp, vp]
         L.nc_slab_halo.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, i64, vp]
@@ -310,6 +312,10 @@ def nc_slab_forces(ctx, q, gid, n_own, h_lo, n_lo, h_hi, n_hi, klo, khi, F, want
     _check(ctx, load().nc_slab_forces(ctx, _ptr(q), _ptr(gid), int(n_own), _ptr(h_lo), int(n_lo), _ptr(h_hi),
                                       int(n_hi), int(klo), int(khi), _ptr(F), _ptr(parts)))
     return parts
+
+
+def nc_slab_kick_kick_drift(ctx, q, p, F, n: int, dt_prev: float, dt: float) -> None:
+    _check(ctx, load().nc_slab_kick_kick_drift(ctx, _ptr(q), _ptr(p), _ptr(F), int(n), float(dt_prev), float(dt)))
 
 
 def nc_slab_kick(ctx, p, F, n, dt) -> None:

@@ -58,6 +58,7 @@ class SlabRank:
         self.hsend = [t(self.bcap, 4), t(self.bcap, 4)]          # halo records to r-1, r+1
         self.hrecv = [t(self.bcap, 4), t(self.bcap, 4)]
         self.n = 0
+        self.pending_dt = 0.0  # a deferred closing half kick (see kick)
 
     def set_flow(self, A, policy, t0, **kw):
         self.cl.set_flow(A, policy, t0, **kw)
@@ -66,6 +67,7 @@ class SlabRank:
         return nc.nc_slab_layers(self.ctx, self.rank, self.nranks)
 
     def load(self, q_own, p_own, gid_own):
+        self.pending_dt = 0.0
         n = len(q_own)
         assert n <= self.cap
         self.q[:n].copy_(self.torch.as_tensor(q_own))
@@ -75,7 +77,9 @@ class SlabRank:
 
     # ---------------------------------------------------------------- phases
     def kick_drift(self, dt):
-        nc.nc_slab_kick_drift(self.ctx, self.q, self.p, self.F, self.n, dt)
+        # the previous step's closing half kick, if deferred, runs in the same pass
+        nc.nc_slab_kick_kick_drift(self.ctx, self.q, self.p, self.F, self.n, self.pending_dt, dt)
+        self.pending_dt = 0.0
 
     def migrate(self):
         klo, khi, _ = self.layers()
@@ -108,7 +112,14 @@ class SlabRank:
                                  want_parts)
 
     def kick(self, dt):
-        nc.nc_slab_kick(self.ctx, self.p, self.F, self.n, dt)
+        # closing half kick: deferred into the next kick_drift (p and F in this rank's order stay
+        # untouched until then); flush() applies it when the momenta are read
+        self.pending_dt = dt
+
+    def flush(self):
+        if self.pending_dt > 0:
+            nc.nc_slab_kick(self.ctx, self.p, self.F, self.n, self.pending_dt)
+            self.pending_dt = 0.0
 
     def reduce(self, all_parts):
         return nc.nc_slab_reduce(self.ctx, all_parts)
@@ -220,6 +231,12 @@ class SlabSystem:
             return None
         allp = self.tr.gather(parts)
         return self.ranks[0].reduce(allp)
+
+    def flush(self):
+        """Apply deferred closing kicks (before the momenta are read)."""
+        for r in self.ranks:
+            if hasattr(r, "flush"):
+                r.flush()
 
     def step(self, dt, want_uw=True):
         for r in self.ranks:

@@ -38,6 +38,7 @@ def make_system(w, q, p, P, variant, prec):
 
 
 def gather_state(system, n, dtype):
+    system.flush()  # deferred closing kicks
     q = np.zeros((n, 3), dtype=dtype)
     p = np.zeros((n, 3), dtype=dtype)
     F = np.zeros((n, 3), dtype=dtype)
