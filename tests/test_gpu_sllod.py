@@ -214,3 +214,24 @@ def test_one_call_equals_stepwise(prec, variant):
     b = run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=1)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.array_equal(a[2], b[2]) and a[3] == b[3] and a[4] == b[4]
+
+
+def test_deferred_kick_dropped_by_set_state():
+    """The closing half kick of a step is held back until the state is read; loading a new state
+    in between must discard it (the new momenta are returned untouched)."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(2, scale=2)
+    q = W.positions(w, dtype=np.float64, k=2)
+    p = W.momenta(w, dtype=np.float64, k=2)
+    cl = CellList("do", "f64", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    cl.set_flow(w.A, w.policy, w.t0, L0=w.L0, tstar=w.extra["tstar"])
+    qd, pd = torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda()
+    cl.set_state(qd, pd)
+    cl.step(0.002, 1, want_uw=False)  # leaves a closing kick pending
+    cl.set_state(qd, pd)
+    po = torch.empty_like(pd)
+    cl.get_state(None, po)
+    cl.close()
+    assert torch.equal(po, pd)
