@@ -9,12 +9,16 @@
 //   K3  k_pairs           : warp-per-cell pair kernel: builds the 27 (DS) or
 //                           27/30/34/36 (DO) neighborhood on the fly, stages
 //                           the neighbor particles (image shift applied) in
-//                           shared memory, filters r^2 < r_c^2 into per-lane
-//                           queues, evaluates LJ/WCA for the queued pairs,
-//                           full i-side accumulation, no atomics
+//                           shared memory, filters r^2 < r_c^2 (1 + tau) two
+//                           candidates at a time (LDS.64 + FADD2/FFMA2) into
+//                           per-lane hit words, evaluates the hits in a packed
+//                           fp32 far tier and an fp64 close tier, full i-side
+//                           accumulation, no atomics
+//       k_pairs_seg       : the same pair set for sparse cells (k3_seg.cuh)
 //   K3r k_reduce          : deterministic fixed-order reduction of partials (one launch)
-//   K4  k_kick_drift_key  : SLLOD half kick + flow factor + drift, fused with K1
-//       k_kick            : SLLOD flow factor + half kick
+//   K4  k_kick_drift_key  : SLLOD half kick + flow factor + drift, fused with K1 (and with
+//                           the previous step's deferred closing half kick)
+//       k_kick            : SLLOD flow factor + half kick (when the state is read)
 //
 // Canonical fp64 arithmetic (reading R16): every operation that decides an
 // integer (wrap, cell key, stencil rows/columns, pair membership in the
