@@ -207,9 +207,10 @@ def run_slab(args):
     from paper_1412_3784_b200.nemdcell import CellList
     from paper_1412_3784_b200.slab import DistTransport, SlabRank, SlabSystem, own_particles
 
-    w = workload(args.config)
-    q = W.positions(w, dtype=np.float32, k=args.config, r=0)
-    p = W.momenta(w, dtype=np.float32, k=args.config, r=0)
+    # --weak: 8,388,608 particles per GPU in a box elongated along v3; else C<k> split
+    w = W.make_weak(ws) if args.weak else workload(args.config)
+    q = W.positions(w, dtype=np.float32, k=args.config if not args.weak else 4, r=0)
+    p = W.momenta(w, dtype=np.float32, k=args.config if not args.weak else 4, r=0)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
@@ -319,9 +320,11 @@ def run_slab(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
-            "config": {"workload": f"C{args.config}", "n_total": w.n, "variant": args.variant,
+            "config": {"workload": w.name if args.weak else f"C{args.config}", "n_total": w.n,
+                       "n_per_gpu": w.n // ws, "variant": args.variant,
                        "box": box_text(w), "potential": pot_text(w),
                        "precision": "fp32 storage + fp32 filter, fp64 interactions",
                        "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
@@ -542,10 +545,12 @@ def main():
     ap.add_argument("--steps-per-call", type=int, default=1,
                     help="SLLOD steps per nc_step_sllod call (0 = all timed steps in one call; measured the same)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even on one GPU")
+    ap.add_argument("--weak", action="store_true",
+                    help="slab path, weak scaling: 8,388,608 particles per GPU (box elongated along v3)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.slab:
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.slab or args.weak:
         return run_slab(args)
     return run_ours(args)
 

@@ -120,8 +120,10 @@ def box_at(L0, A, policy, t, extra) -> np.ndarray:
 FCC_BASIS = np.array([[0.0, 0.0, 0.0], [0.5, 0.5, 0.0], [0.5, 0.0, 0.5], [0.0, 0.5, 0.5]])
 
 
-def fractional_sites(lattice: str, K: int, lo: int, hi: int) -> np.ndarray:
-    """Fractional site coordinates for site ids [lo, hi): id = b + nb*(x + K*(y + K*z))."""
+def fractional_sites(lattice: str, K: int, lo: int, hi: int, Kz: int = 0) -> np.ndarray:
+    """Fractional site coordinates for site ids [lo, hi): id = b + nb*(x + K*(y + K*z)); K x K x Kz
+    lattice cells (Kz = K unless given: the weak-scaling boxes are elongated along v3)."""
+    Kz = Kz or K
     nb = 4 if lattice == "fcc" else 1
     ids = np.arange(lo, hi, dtype=np.int64)
     b = ids % nb
@@ -131,7 +133,7 @@ def fractional_sites(lattice: str, K: int, lo: int, hi: int) -> np.ndarray:
     z = cell // (K * K)
     basis = FCC_BASIS if lattice == "fcc" else np.zeros((1, 3))
     lam = np.stack([x, y, z], axis=1).astype(np.float64) + basis[b]
-    return lam / K
+    return lam / np.array([K, K, Kz], dtype=np.float64)
 
 
 def positions(w: Workload, dtype=np.float64, k: int = 0, r: int = 0) -> np.ndarray:
@@ -140,9 +142,10 @@ def positions(w: Workload, dtype=np.float64, k: int = 0, r: int = 0) -> np.ndarr
     out = np.empty((w.n, 3), dtype=dtype)
     for c, lo in enumerate(range(0, w.n, CHUNK)):
         hi = min(w.n, lo + CHUNK)
-        lam = fractional_sites(w.lattice, w.K, lo, hi)
+        Kz = w.extra.get("Kz", w.K)
+        lam = fractional_sites(w.lattice, w.K, lo, hi, Kz)
         g = rng_for(k, r, 1000 + c)
-        lam += g.uniform(-w.jitter, w.jitter, size=lam.shape) / w.K
+        lam += g.uniform(-w.jitter, w.jitter, size=lam.shape) / np.array([w.K, w.K, Kz], dtype=np.float64)
         lam -= np.floor(lam)  # sites stay in [0,1)^3 fractional
         q = lam[:, 0:1] * w.L[:, 0] + lam[:, 1:2] * w.L[:, 1] + lam[:, 2:3] * w.L[:, 2]
         out[lo:hi] = q.astype(dtype)
@@ -231,6 +234,24 @@ def make(k: int, r: int = 0, *, flow: str = "uniaxial", scale: int = 1) -> Workl
                         potential="wca", prec=("f32",), lattice="sc", K=K, jitter=0.05, seed=(k, r), steps=steps,
                         extra=extra)
     raise ValueError(k)
+
+
+def make_weak(P: int, r: int = 0) -> Workload:
+    """Weak-scaling workload: C4's construction with 8,388,608 particles per GPU --
+    an FCC lattice of 128 x 128 x 128P cells in the KR box Rot diag(a, a, P a), a = 214.99 sigma
+    (85.5 cell layers per GPU along v3, which the planar flow leaves untouched)."""
+    w = make(4, r)
+    K = 128
+    a = _side(4 * K ** 3)
+    L0, lam = kr_basis(a)
+    L0[2, 2] = P * a
+    w.L0 = L0
+    w.K = K
+    w.n = 4 * K * K * (K * P)
+    w.extra = dict(w.extra, Kz=K * P)
+    w.L = box_at(L0, w.A, "kr", w.t0, w.extra)
+    w.name = f"C4w{P}"
+    return w
 
 
 def perfect_fcc(K: int = 10):
