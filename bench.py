@@ -287,10 +287,13 @@ def run_slab(args):
     p64 = p32 / 2.0
     flops0 = 9.0 * cand0 + 30.0 * inter0
     t_bound = (9.0 * cand0 + 30.0 * inter0 * split) / p32 + 30.0 * inter0 * (1.0 - split) / p64
-    achieved = flops0 / (pairs_ms / max(pairs_n, 1) * 1e-3) / 1e12
+    # a slab evaluation launches k_pairs three times (interior layers, then the two boundary layers
+    # after the halo arrives): time per EVALUATION
+    pairs_eval_ms = pairs_ms / evals
+    achieved = flops0 / (pairs_eval_ms * 1e-3) / 1e12
     roof = {"bound": "alu", "achieved": achieved, "peak": flops0 / t_bound / 1e12, "unit": "TFLOP/s",
             "frac": achieved / (flops0 / t_bound / 1e12), "traffic": None, "kernel": "k_pairs (rank 0)",
-            "kernel_ms": pairs_ms / max(pairs_n, 1),
+            "kernel_ms": pairs_eval_ms, "launches_per_eval": pairs_n / evals,
             "peak_note": f"FP32/FP64 blend as the 1-GPU line; {split:.1%} of rank 0's interactions in the fp32 tier"}
 
     # end to end through the slab API: every step each rank copies its own positions from pinned

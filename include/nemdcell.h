@@ -280,6 +280,19 @@ nc_status nc_slab_forces(nc_ctx *ctx, const void *q, const uint32_t *gid, int64_
                          int64_t n_lo, const void *halo_from_hi, int64_t n_hi, int klo, int khi, void *F,
                          double *layer_parts);
 
+/* nc_slab_forces in two calls, so the halo exchange can overlap work: begin
+ * (with the halo COUNTS n_lo, n_hi already known) sorts the own particles
+ * into their cells and runs K3 on the interior own layers klo+1 .. khi-2,
+ * whose neighborhoods contain own cells only; end (with the halo records)
+ * sorts the halo particles in, runs K3 on the two boundary layers, reduces
+ * and writes F and layer_parts exactly as nc_slab_forces (bitwise).  Both are
+ * enqueued on cfg.stream; end synchronizes it.  Errors: as nc_slab_forces;
+ * NC_E_STATE for end without begin. */
+nc_status nc_slab_forces_begin(nc_ctx *ctx, const void *q, const uint32_t *gid, int64_t n_own, int64_t n_lo,
+                               int64_t n_hi, int klo, int khi);
+nc_status nc_slab_forces_end(nc_ctx *ctx, const void *halo_from_lo, const void *halo_from_hi, void *F,
+                             double *layer_parts);
+
 /* SLLOD second half: p <- E(-dt/2) p + dt/2 F on n own particles. */
 nc_status nc_slab_kick(nc_ctx *ctx, void *p, const void *F, int64_t n, double dt);
 

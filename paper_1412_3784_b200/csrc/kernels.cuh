@@ -332,14 +332,22 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __r
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
 __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ cs, const uint32_t* __restrict__ gid_in,
-                          uint32_t* __restrict__ tmp, uint32_t* __restrict__ tmpgid, uint32_t* __restrict__ tmpkey) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                          uint32_t* __restrict__ tmp, uint32_t* __restrict__ tmpgid, uint32_t* __restrict__ tmpkey,
+                          int64_t i0 = 0) {
+  // particles [i0, i0 + n) (a slab evaluation scatters its own and its halo particles separately)
+  int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= i0 + n) return;
   const uint32_t c = key[i];
   uint32_t pos = cs[c] + slot[i];
   tmp[pos] = (uint32_t)i;
   tmpgid[pos] = gid_in ? gid_in[i] : (uint32_t)i;
   tmpkey[pos] = c;  // k_rank_gather reads the cell in bucket order (coalesced) instead of gathering key[i]
+}
+
+// cs[c] += b for c in [c0, c1): the own cells' starts after the halo particles that precede them
+__global__ void k_add_range(uint32_t* __restrict__ cs, int64_t c0, int64_t c1, uint32_t b) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < c1) cs[c] += b;
 }
 
 #ifndef RG_MINB
@@ -357,9 +365,11 @@ k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __res
                               typename V4<T>::t* __restrict__ q_out, typename V4<T>::t* __restrict__ p_out,
                               uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
                               float4* __restrict__ u32_out, uint32_t* __restrict__ nh_out,
-                              const __grid_constant__ Geom g, uint32_t* __restrict__ idx_out = nullptr) {
-  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
+                              const __grid_constant__ Geom g, uint32_t* __restrict__ idx_out = nullptr,
+                              int64_t s0 = 0) {
+  // bucket positions [s0, s0 + n) (a slab evaluation places own and halo particles in two phases)
+  int64_t s = s0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= s0 + n) return;
   const uint32_t i = tmp[s], c = tmpkey[s], gg = tmpgid[s];
   const typename V4<T>::t q = qw[i];  // gathers issued before the rank loop
   const uint32_t c0 = cs[c], c1 = cs[c + 1];

@@ -78,6 +78,10 @@ struct nc_ctx {
   bool ab_used[2] = {false, false};
   int ab = 0;
   bool async_eval = false;  // an evaluation was enqueued by the async call and not yet synced
+  // a slab evaluation between nc_slab_forces_begin and nc_slab_forces_end
+  int64_t slab_n_own = 0, slab_n1 = 0, slab_n2 = 0, slab_b_own = 0;
+  int slab_klo = 0, slab_khi = 0;
+  bool slab_open = false;
   bool kick_pending = false;
   bool count_tiers = false;  // nc_profile mode 2: k_pairs counts its fp32-tier interactions
   K3Kick pend{};
@@ -298,9 +302,12 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
 
 template <typename T, bool DIGEST>
 nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t* gid, typename V4<T>::t* F,
-                       int layer0 = 0, int nlay = -1) {
+                       int layer0 = 0, int nlay = -1, int part_layer0 = -1, bool reduce = true) {
+  // part_layer0: the layer whose block partials start bpart (default layer0); a slab evaluation
+  // launches its layers in two parts and reduces once (reduce = false for the parts)
   cudaStream_t s = ctx->stream;
   const Geom& g = ctx->g;
+  if (part_layer0 < 0) part_layer0 = layer0;
   if (nlay < 0) nlay = g.dims[2];
   int cpb = cells_per_block(g);
   int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
@@ -308,6 +315,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
   prof_begin(ctx);
+  double* bp = nullptr;  // set once bpl is final (below)
   if constexpr (sizeof(T) == 4) {
     const int Gseg = seg_cells(ctx, g);
     if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
@@ -316,32 +324,38 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       const size_t smem_s = sizeof(SgSmem);
       bpl = bpl_s;
       nblocks = bpl * nlay;
+      bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SEGMENT;
       k_pairs_seg<DIGEST><<<nblocks, SG_NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
-                                                      (float4*)F, ctx->bpart, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
+                                                      (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
                                                       nseg, bpl, layer0);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
+      bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       if (!DIGEST && ctx->count_tiers)
-        k_pairs<T, DIGEST, true><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
+        k_pairs<T, DIGEST, true><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
                                                            ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
       else
-        k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart,
+        k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
                                                      ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
     }
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
-    k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, ctx->bpart, ctx->dcnt,
+    bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
+    k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp, ctx->dcnt,
                                                  ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
   }
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
-  int nl = nlay;
-  prof_begin(ctx);
-  k_reduce<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart, ctx->part_tot, ctx->part_acc, ctx->rcount);
-  LAUNCHED();
-  prof_end(ctx, NC_K_REDUCE);
   ctx->last_cpb = cpb;
+  ctx->last_bpl = bpl;
+  if (reduce) {
+    const int nl = layer0 + nlay - part_layer0;  // every layer whose partials start at bpart
+    prof_begin(ctx);
+    k_reduce<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart, ctx->part_tot, ctx->part_acc, ctx->rcount);
+    LAUNCHED();
+    prof_end(ctx, NC_K_REDUCE);
+  }
   ctx->last_bpl = bpl;
   ctx->tot_valid = false;
   ctx->have_eval = true;
@@ -691,20 +705,82 @@ nc_status partition(nc_ctx* ctx, int64_t n, const T* q, const T* p, const uint32
   return NC_OK;
 }
 
+// Slab force evaluation in two phases so the halo exchange can overlap the interior work:
+//  begin: own particles -> cells (their bucket positions after the halo particles that precede them
+//         in cell order, whose COUNT is known from the count exchange), K3 on the interior own layers
+//         (klo+1 .. khi-2), whose stencils touch own layers only;
+//  end:   halo particles -> cells (a full rescan reproduces the own cells' starts), K3 on the two
+//         boundary layers, one fixed-order reduction over all own layers, forces unsorted.
+// Results are bitwise those of the one-phase evaluation (the same cells, orders and partials).
 template <typename T>
-nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_own, const void* h1, int64_t n1,
-                        const void* h2, int64_t n2, int klo, int khi, T* F, double* parts) {
+nc_status slab_begin_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_own, int64_t n1, int64_t n2, int klo,
+                       int khi) {
   cudaStream_t s = ctx->stream;
   const Geom& g = ctx->g;
   const int64_t n = n_own + n1 + n2;
   if (n > ctx->cap) return fail(ctx, NC_E_OOM, "own + halo particles exceed capacity");
-  int64_t C = g.ncells;
+  const int64_t C = g.ncells, per_layer = (int64_t)g.dims[0] * g.dims[1];
+  const int l3 = g.dims[2];
   CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
   typename V4<T>::t* wq = (typename V4<T>::t*)ctx->wq;
   prof_begin(ctx);
   if (n_own > 0)
     k_wrap_key_src<T><<<nblk(n_own, 256), 256, 0, s>>>(n_own, q, 3, gid, 0, wq, ctx->gin, ctx->key, ctx->slot,
                                                       ctx->counts, g);
+  LAUNCHED();
+  prof_end(ctx, NC_K_WRAPKEY);
+  {
+    nc_status sst = launch_scan(ctx, ctx->counts, C, ctx->cs);
+    if (sst) return sst;
+  }
+  // halo particles in cells before the own cells: the lower halo layer when it precedes klo (not
+  // on the periodic seam), the upper one when it wraps to layer 0
+  const int L_lo = (klo - 1 + l3) % l3, L_hi = khi % l3;
+  const int64_t b_own = (L_lo < klo ? n1 : 0) + (L_hi < klo ? n2 : 0);
+  if (b_own > 0) {
+    const int64_t c0 = (int64_t)klo * per_layer;
+    k_add_range<<<nblk(C + 1 - c0, 256), 256, 0, s>>>(ctx->cs, c0, C + 1, (uint32_t)b_own);
+    LAUNCHED();
+  }
+  if (n_own > 0) {
+    prof_begin(ctx);
+    k_scatter<<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp, ctx->tmpgid,
+                                               ctx->tmpkey);
+    LAUNCHED();
+    prof_end(ctx, NC_K_SCATTER);
+    prof_begin(ctx);
+    k_rank_gather<T><<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+                                                      (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
+                                                      ctx->u32, ctx->nh, g, ctx->sidx, b_own);
+    LAUNCHED();
+    prof_end(ctx, NC_K_RANKGATHER);
+  }
+  ctx->slab_n_own = n_own;
+  ctx->slab_n1 = n1;
+  ctx->slab_n2 = n2;
+  ctx->slab_b_own = b_own;
+  ctx->slab_klo = klo;
+  ctx->slab_khi = khi;
+  ctx->slab_open = true;
+  ctx->occ_hint = (double)n_own / ((double)per_layer * (double)(khi - klo));
+  if (khi - klo > 2) {  // interior layers: their stencils see own cells only
+    nc_status st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid,
+                                          (typename V4<T>::t*)ctx->sF, klo + 1, khi - klo - 2, klo, false);
+    if (st) return st;
+  }
+  return NC_OK;
+}
+
+template <typename T>
+nc_status slab_end_t(nc_ctx* ctx, const void* h1, const void* h2, T* F, double* parts) {
+  cudaStream_t s = ctx->stream;
+  const Geom& g = ctx->g;
+  const int64_t n_own = ctx->slab_n_own, n1 = ctx->slab_n1, n2 = ctx->slab_n2, b_own = ctx->slab_b_own;
+  const int klo = ctx->slab_klo, khi = ctx->slab_khi;
+  const int64_t n = n_own + n1 + n2, C = g.ncells;
+  ctx->slab_open = false;
+  typename V4<T>::t* wq = (typename V4<T>::t*)ctx->wq;
+  prof_begin(ctx);
   if (n1 > 0)
     k_wrap_key_src<T><<<nblk(n1, 256), 256, 0, s>>>(n1, (const T*)h1, 4, nullptr, n_own, wq, ctx->gin, ctx->key,
                                                     ctx->slot, ctx->counts, g);
@@ -713,19 +789,27 @@ nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_
                                                     ctx->key, ctx->slot, ctx->counts, g);
   LAUNCHED();
   prof_end(ctx, NC_K_WRAPKEY);
-  {
+  {  // all counts now: the own cells' starts come out as in begin (b_own halo particles before them)
     nc_status sst = launch_scan(ctx, ctx->counts, C, ctx->cs);
     if (sst) return sst;
   }
-  if (n > 0) {
+  if (n1 + n2 > 0) {
     prof_begin(ctx);
-    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp, ctx->tmpgid, ctx->tmpkey);
+    k_scatter<<<nblk(n1 + n2, 256), 256, 0, s>>>(n1 + n2, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp,
+                                                 ctx->tmpgid, ctx->tmpkey, n_own);
     LAUNCHED();
     prof_end(ctx, NC_K_SCATTER);
+    // the halo buckets: [0, b_own) and [b_own + n_own, n)
     prof_begin(ctx);
-    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
-                                                  (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u, ctx->u32,
-                                                  ctx->nh, g, ctx->sidx);
+    if (b_own > 0)
+      k_rank_gather<T><<<nblk(b_own, 256), 256, 0, s>>>(b_own, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+                                                        (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
+                                                        ctx->u32, ctx->nh, g, ctx->sidx, 0);
+    const int64_t rest = n - (b_own + n_own);
+    if (rest > 0)
+      k_rank_gather<T><<<nblk(rest, 256), 256, 0, s>>>(rest, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+                                                       (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
+                                                       ctx->u32, ctx->nh, g, ctx->sidx, b_own + n_own);
     LAUNCHED();
     prof_end(ctx, NC_K_RANKGATHER);
   }
@@ -733,9 +817,15 @@ nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_
   ctx->last_in_gid = ctx->gin;
   ctx->last_resident = false;
   ctx->have_cells = true;
-  nc_status st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid,
-                                        (typename V4<T>::t*)ctx->sF, klo, khi - klo);
+  // boundary layers, then one reduction over all own layers
+  nc_status st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF,
+                                        klo, 1, klo, khi - klo == 1);
   if (st) return st;
+  if (khi - klo > 1) {
+    st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF,
+                                khi - 1, 1, klo, true);
+    if (st) return st;
+  }
   if (n > 0 && F) {
     prof_begin(ctx);
     k_unsort_idx<T><<<nblk(n, 256), 256, 0, s>>>(n, (const typename V4<T>::t*)ctx->sF, ctx->sidx, n_own, F);
@@ -747,6 +837,14 @@ nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_
   }
   CK(cudaStreamSynchronize(s));
   return NC_OK;
+}
+
+template <typename T>
+nc_status slab_forces_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_own, const void* h1, int64_t n1,
+                        const void* h2, int64_t n2, int klo, int khi, T* F, double* parts) {
+  nc_status st = slab_begin_t<T>(ctx, q, gid, n_own, n1, n2, klo, khi);
+  if (st) return st;
+  return slab_end_t<T>(ctx, h1, h2, F, parts);
 }
 }  // namespace
 
@@ -1280,6 +1378,25 @@ nc_status nc_slab_forces(nc_ctx* ctx, const void* q, const uint32_t* gid, int64_
                                     (float*)F, layer_parts)
              : slab_forces_t<double>(ctx, (const double*)q, gid, n_own, halo_from_lo, n_lo, halo_from_hi, n_hi, klo,
                                      khi, (double*)F, layer_parts);
+}
+
+nc_status nc_slab_forces_begin(nc_ctx* ctx, const void* q, const uint32_t* gid, int64_t n_own, int64_t n_lo,
+                               int64_t n_hi, int klo, int khi) {
+  if (!ctx || (n_own > 0 && (!q || !gid)) || n_lo < 0 || n_hi < 0) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
+  if (klo < 0 || khi > ctx->g.dims[2] || khi - klo < 1) return fail(ctx, NC_E_ARG, "bad layer range");
+  return ctx->cfg.prec == NC_F32 ? slab_begin_t<float>(ctx, (const float*)q, gid, n_own, n_lo, n_hi, klo, khi)
+                                 : slab_begin_t<double>(ctx, (const double*)q, gid, n_own, n_lo, n_hi, klo, khi);
+}
+
+nc_status nc_slab_forces_end(nc_ctx* ctx, const void* halo_from_lo, const void* halo_from_hi, void* F,
+                             double* layer_parts) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (!ctx->slab_open) return fail(ctx, NC_E_STATE, "nc_slab_forces_begin first");
+  if ((ctx->slab_n1 > 0 && !halo_from_lo) || (ctx->slab_n2 > 0 && !halo_from_hi))
+    return fail(ctx, NC_E_ARG, "null argument");
+  return ctx->cfg.prec == NC_F32 ? slab_end_t<float>(ctx, halo_from_lo, halo_from_hi, (float*)F, layer_parts)
+                                 : slab_end_t<double>(ctx, halo_from_lo, halo_from_hi, (double*)F, layer_parts);
 }
 
 nc_status nc_slab_kick(nc_ctx* ctx, void* p, const void* F, int64_t n, double dt) {

@@ -28,7 +28,8 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_get_stencil_histogram", "nc_launch_count", "nc_last_error", "nc_version", "nc_profile",
            "nc_profile_read", "nc_slab_layers", "nc_slab_kick_drift", "nc_slab_kick_kick_drift", "nc_slab_migrate",
            "nc_slab_unpack",
-           "nc_slab_halo", "nc_slab_forces", "nc_slab_kick", "nc_slab_reduce", "nc_set_pair_kernel",
+           "nc_slab_halo", "nc_slab_forces", "nc_slab_forces_begin", "nc_slab_forces_end", "nc_slab_kick",
+           "nc_slab_reduce", "nc_set_pair_kernel",
            "nc_pair_kernel_used"]
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
@@ -108,6 +109,8 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_slab_unpack.argtypes = [vp, vp, i64, vp, vp, vp]
         L.nc_slab_halo.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, i64, vp]
         L.nc_slab_forces.argtypes = [vp, vp, vp, i64, vp, i64, vp, i64, i32, i32, vp, vp]
+        L.nc_slab_forces_begin.argtypes = [vp, vp, vp, i64, i64, i64, i32, i32]
+        L.nc_slab_forces_end.argtypes = [vp, vp, vp, vp, vp]
         L.nc_slab_kick.argtypes = [vp, vp, vp, i64, d]
         L.nc_slab_reduce.argtypes = [vp, vp, i32, vp, vp, vp]
         L.nc_launch_count.argtypes = [vp]
@@ -311,6 +314,17 @@ def nc_slab_forces(ctx, q, gid, n_own, h_lo, n_lo, h_hi, n_hi, klo, khi, F, want
     parts = np.zeros((khi - klo, NPART)) if want_parts else None
     _check(ctx, load().nc_slab_forces(ctx, _ptr(q), _ptr(gid), int(n_own), _ptr(h_lo), int(n_lo), _ptr(h_hi),
                                       int(n_hi), int(klo), int(khi), _ptr(F), _ptr(parts)))
+    return parts
+
+
+def nc_slab_forces_begin(ctx, q, gid, n_own, n_lo, n_hi, klo, khi) -> None:
+    _check(ctx, load().nc_slab_forces_begin(ctx, _ptr(q), _ptr(gid), int(n_own), int(n_lo), int(n_hi), int(klo),
+                                            int(khi)))
+
+
+def nc_slab_forces_end(ctx, h_lo, h_hi, F, klo, khi, want_parts=True):
+    parts = np.zeros((khi - klo, NPART)) if want_parts else None
+    _check(ctx, load().nc_slab_forces_end(ctx, _ptr(h_lo), _ptr(h_hi), _ptr(F), _ptr(parts)))
     return parts
 
 

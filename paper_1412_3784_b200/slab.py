@@ -111,6 +111,16 @@ class SlabRank:
         return nc.nc_slab_forces(self.ctx, self.q, self.gid, self.n, h_lo, n_lo, h_hi, n_hi, klo, khi, self.F,
                                  want_parts)
 
+    def forces_begin(self, n_lo, n_hi):
+        """Own particles into cells and K3 on the interior layers (the halo counts are known)."""
+        klo, khi, _ = self.layers()
+        nc.nc_slab_forces_begin(self.ctx, self.q, self.gid, self.n, n_lo, n_hi, klo, khi)
+
+    def forces_end(self, h_lo, n_lo, h_hi, n_hi, want_parts=True):
+        """Halo particles in, K3 on the boundary layers, reduction, forces (bitwise = forces())."""
+        klo, khi, _ = self.layers()
+        return nc.nc_slab_forces_end(self.ctx, h_lo, h_hi, self.F, klo, khi, want_parts)
+
     def kick(self, dt):
         # closing half kick: deferred into the next kick_drift (p and F in this rank's order stay
         # untouched until then); flush() applies it when the momenta are read
@@ -133,6 +143,17 @@ class SlabRank:
 class LoopbackTransport:
     """All ranks in one process (tests on one GPU): rank r's send_lo is rank r-1's
     from_hi, its send_hi is rank r+1's from_lo (periodic in the rank index)."""
+
+    # split exchange (counts first, then the payload) for the overlapped force evaluation
+    def counts(self, sends):
+        P = len(sends)
+        return [(sends[(r - 1) % P][3], sends[(r + 1) % P][1]) for r in range(P)]
+
+    def start(self, sends, recv_bufs, counts):
+        return self.exchange(sends, recv_bufs)
+
+    def finish(self, pending):
+        return pending
 
     def exchange(self, sends, recv_bufs):
         P = len(sends)
@@ -171,6 +192,33 @@ class DistTransport:
                dist.P2POp(dist.irecv, tensors_in[1], hi), dist.P2POp(dist.irecv, tensors_in[0], lo)]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+
+    def counts(self, sends):
+        torch = self.torch
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        cnt_out = [torch.tensor([n_lo], dtype=torch.int64, device=self.device),
+                   torch.tensor([n_hi], dtype=torch.int64, device=self.device)]
+        cnt_in = [torch.zeros(1, dtype=torch.int64, device=self.device) for _ in range(2)]
+        self._p2p(cnt_out, cnt_in)
+        return [(int(cnt_in[0].item()), int(cnt_in[1].item()))]
+
+    def start(self, sends, recv_bufs, counts):
+        """Issue the payload exchange and return without waiting (NCCL runs on its own stream)."""
+        dist = self.dist
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        b_lo, b_hi = recv_bufs[0]
+        (m_lo, m_hi), = counts
+        assert m_lo <= len(b_lo) and m_hi <= len(b_hi), "receive buffer too small"
+        lo, hi = (self.rank - 1) % self.P, (self.rank + 1) % self.P
+        ops = [dist.P2POp(dist.isend, s_lo[:max(n_lo, 1)], lo), dist.P2POp(dist.isend, s_hi[:max(n_hi, 1)], hi),
+               dist.P2POp(dist.irecv, b_hi[:max(m_hi, 1)], hi), dist.P2POp(dist.irecv, b_lo[:max(m_lo, 1)], lo)]
+        return dist.batch_isend_irecv(ops), [(b_lo, m_lo, b_hi, m_hi)]
+
+    def finish(self, pending):
+        works, out = pending
+        for w in works:
+            w.wait()  # the current stream waits for the exchange
+        return out
 
     def exchange(self, sends, recv_bufs):
         torch = self.torch
@@ -225,8 +273,17 @@ class SlabSystem:
 
     def forces(self, want_uw=True):
         hs = [r.halo() for r in self.ranks]
-        hr = self.tr.exchange(hs, [r.hrecv for r in self.ranks])
-        parts = [r.forces(*h, want_parts=want_uw) for r, h in zip(self.ranks, hr)]
+        if hasattr(self.tr, "start") and all(hasattr(r, "forces_begin") for r in self.ranks):
+            # overlapped: counts, then the payload in flight while the interior layers are evaluated
+            cnt = self.tr.counts(hs)
+            pend = self.tr.start(hs, [r.hrecv for r in self.ranks], cnt)
+            for r, (m_lo, m_hi) in zip(self.ranks, cnt):
+                r.forces_begin(m_lo, m_hi)
+            hr = self.tr.finish(pend)
+            parts = [r.forces_end(*h, want_parts=want_uw) for r, h in zip(self.ranks, hr)]
+        else:
+            hr = self.tr.exchange(hs, [r.hrecv for r in self.ranks])
+            parts = [r.forces(*h, want_parts=want_uw) for r, h in zip(self.ranks, hr)]
         if not want_uw:
             return None
         allp = self.tr.gather(parts)

@@ -101,6 +101,14 @@ class NumpyRank:
         np.add.at(parts[:, 7], lay, r.cnt.astype(np.float64))
         return parts
 
+    # the split evaluation (SlabSystem overlaps the halo payload with forces_begin)
+    def forces_begin(self, n_lo, n_hi):
+        self.pending_counts = (n_lo, n_hi)
+
+    def forces_end(self, h_lo, n_lo, h_hi, n_hi, want_parts=True):
+        assert (n_lo, n_hi) == self.pending_counts, "counts of begin and end agree"
+        return self.forces(h_lo, n_lo, h_hi, n_hi, want_parts)
+
     def reduce(self, allp):
         tot = allp.sum(axis=0)
         return tot[0], tot[1:7], {"interactions": tot[7]}
