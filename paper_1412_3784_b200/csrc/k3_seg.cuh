@@ -21,32 +21,33 @@
 
 namespace nc {
 
-#ifndef SG_NW_OVR
-#define SG_NW_OVR 2
-#endif
-constexpr int SG_NW = SG_NW_OVR;            // warps per block (share one staged union)
-constexpr int SG_NT = 32 * SG_NW;
-constexpr int SG_CAP = 384 * SG_NW;         // staged union elements
 constexpr int SG_ROWS = 12;                 // stencil rows (DS 9, DO <= 12)
-constexpr int SG_GMAX = 24 * SG_NW;         // cells per segment
-constexpr int SG_MAXE = SG_ROWS * (SG_GMAX + 4);  // union entries (row x column)
 constexpr int SG_QCAP = 32;                 // per-lane hit queue
+// NW warps per block share one staged union: 2 (segments of 48 cells) or 4 (96 cells, large grids)
+template <int NW>
+struct SgCfg {
+  static constexpr int NT = 32 * NW;
+  static constexpr int CAP = 384 * NW;          // staged union elements
+  static constexpr int GMAX = 24 * NW;          // cells per segment
+  static constexpr int MAXE = SG_ROWS * (GMAX + 4);  // union entries (row x column)
+};
 
+template <int NW>
 struct SgSmem {
-  float4 stage[SG_CAP];                     // segment-frame x, y, z; w = sorted index bits
-  uint32_t e_start[SG_MAXE];                // first sorted particle of the entry's cell
-  uint16_t e_off[SG_MAXE + 1];              // staging offset of the entry
-  uint16_t sent[SG_CAP];                    // entry of each staged element
-  uint8_t e_row[SG_MAXE];
-  uint8_t e_ci[SG_MAXE];                    // column index inside the row's union range
-  int8_t e_nx[SG_MAXE];                     // x image shift floor(col / l1) of the entry's column
-  uint16_t rg[SG_GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
-  uint16_t queue[SG_NW][SG_QCAP][32];
-  uint32_t wtot[SG_NW][SG_ROWS];            // per-warp row totals (block scan)
-  double part[SG_NW][NPART];                // per-warp partials (fixed-order combine)
-  uint32_t cst[SG_GMAX];                    // first sorted particle of each segment cell
-  uint16_t ct0[SG_GMAX];                    // staged offset of each segment cell
-  uint16_t nsz[SG_GMAX];                    // neighborhood size (cells) of each segment cell
+  float4 stage[SgCfg<NW>::CAP];                     // segment-frame x, y, z; w = sorted index bits
+  uint32_t e_start[SgCfg<NW>::MAXE];                // first sorted particle of the entry's cell
+  uint16_t e_off[SgCfg<NW>::MAXE + 1];              // staging offset of the entry
+  uint16_t sent[SgCfg<NW>::CAP];                    // entry of each staged element
+  uint8_t e_row[SgCfg<NW>::MAXE];
+  uint8_t e_ci[SgCfg<NW>::MAXE];                    // column index inside the row's union range
+  int8_t e_nx[SgCfg<NW>::MAXE];                     // x image shift floor(col / l1) of the entry's column
+  uint16_t rg[SgCfg<NW>::GMAX][SG_ROWS][2];         // per cell and row: staged sub-range [st, en)
+  uint16_t queue[NW][SG_QCAP][32];
+  uint32_t wtot[NW][SG_ROWS];            // per-warp row totals (block scan)
+  double part[NW][NPART];                // per-warp partials (fixed-order combine)
+  uint32_t cst[SgCfg<NW>::GMAX];                    // first sorted particle of each segment cell
+  uint16_t ct0[SgCfg<NW>::GMAX];                    // staged offset of each segment cell
+  uint16_t nsz[SgCfg<NW>::GMAX];                    // neighborhood size (cells) of each segment cell
   // rows
   int r_lo[SG_ROWS], r_n[SG_ROWS], r_eb[SG_ROWS + 1], r_base[SG_ROWS];
   int r_ny[SG_ROWS], r_nz[SG_ROWS];         // image shifts of the row (DO n2, n3; DS n1, n2)
@@ -59,8 +60,11 @@ struct SgSmem {
 // Stencil rows of the segment [A, A+G) in row (a1, a2): union column ranges, brackets,
 // staged union, per-cell sub-ranges.  All SG_NT threads of the block call it.  Returns
 // false (uniformly) if the union holds more than SG_CAP elements (caller shrinks G).
+template <int NW>
 __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const float4* __restrict__ u32, int A, int G,
-                         int a1, int a2, SgSmem& sm, int tid) {
+                         int a1, int a2, SgSmem<NW>& sm, int tid) {
+  constexpr int SG_NT = SgCfg<NW>::NT, SG_CAP = SgCfg<NW>::CAP, SG_GMAX = SgCfg<NW>::GMAX,
+                SG_MAXE = SgCfg<NW>::MAXE, SG_NW = NW;
   const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
   const int lane = tid & 31, wid = tid >> 5;
   // ---- rows (warp 0)
@@ -253,8 +257,8 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
 }
 
 // fp64 evaluation of one lane's queued staged indices (four per iteration, global loads first).
-template <bool DIGEST>
-__device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const double4* __restrict__ u,
+template <bool DIGEST, int NW>
+__device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem<NW>& sm, const double4* __restrict__ u,
                                         const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                                         const uint32_t* __restrict__ gid, uint32_t qb, int nq, uint32_t me,
                                         uint32_t nh_i, int A, double uix, double uiy, double uiz, double wx64,
@@ -325,15 +329,17 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem& sm, const d
   __syncwarp();
 }
 
-template <bool DIGEST>
-__global__ void __launch_bounds__(SG_NT, 16 / SG_NW)
+template <bool DIGEST, int NW>
+__global__ void __launch_bounds__(32 * NW, 16 / NW)
 k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
             const float4* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
             float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
             uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int G, int nseg,
             int bpl, int layer0) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  SgSmem& sm = *reinterpret_cast<SgSmem*>(smraw);
+  constexpr int SG_NT = SgCfg<NW>::NT, SG_CAP = SgCfg<NW>::CAP, SG_NW = NW;
+  (void)SG_NT;
+  SgSmem<NW>& sm = *reinterpret_cast<SgSmem<NW>*>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int l1 = g.dims[0];
   const int layer = layer0 + (int)(blockIdx.x / bpl);
@@ -352,7 +358,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
   int A = Abeg;
   while (A < Aend) {
     int Gs = Aend - A;
-    while (!sg_setup(g, cs, u32, A, Gs, a1, a2, sm, tid)) {
+    while (!sg_setup<NW>(g, cs, u32, A, Gs, a1, a2, sm, tid)) {
       if (Gs == 1) { Gs = 0; break; }  // a single cell's neighborhood above SG_CAP: flagged below
       Gs = (Gs + 1) / 2;
     }
@@ -407,7 +413,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
         const int lmax = __reduce_max_sync(0xffffffffu, len);
         for (int k0 = 0; k0 < lmax; k0 += 8) {
           if (__any_sync(0xffffffffu, nq > SG_QCAP - 8)) {  // room for 8 more hits in every queue
-            sg_eval<DIGEST>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+            sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
             nq = 0;
           }
           const int kend = min(lmax, k0 + 8);
@@ -422,7 +428,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
           }
         }
       }
-      sg_eval<DIGEST>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+      sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
       const double fx = acc.fx, fy = acc.fy, fz = acc.fz, uu = acc.u;
       const double w0 = acc.w0, w1 = acc.w1, w2 = acc.w2, w3 = acc.w3, w4 = acc.w4, w5 = acc.w5;
       const uint32_t cnt = acc.cnt, nrc = acc.nrc;

@@ -82,6 +82,7 @@ struct nc_ctx {
   int64_t slab_n_own = 0, slab_n1 = 0, slab_n2 = 0, slab_b_own = 0;
   int slab_klo = 0, slab_khi = 0;
   bool slab_open = false;
+  int seg_nw = 2;  // warps per block of the sparse-cell kernel (seg_cells)
   bool kick_pending = false;
   bool count_tiers = false;  // nc_profile mode 2: k_pairs counts its fp32-tier interactions
   K3Kick pend{};
@@ -186,7 +187,7 @@ int cells_per_block(const Geom& g) {
 // Cells per segment of the sparse-cell kernel, 0 = use the warp-per-cell kernel.  Mean occupancy
 // below 4 particles per cell (WCA at rho = 0.8442: ~1.3) selects segments of ~48 particles (two
 // warps); nc_set_pair_kernel forces either kernel, NC_SEG=0 / NC_SEG=1 likewise (A/B runs).
-int seg_cells(const nc_ctx* ctx, const Geom& g) {
+int seg_cells(nc_ctx* ctx, const Geom& g) {
   static int env_mode = [] {
     const char* e = getenv("NC_SEG");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
@@ -197,10 +198,16 @@ int seg_cells(const nc_ctx* ctx, const Geom& g) {
                                           : (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (mode < 0 && occ >= 4.0) return 0;
   // a fixed segment length (not occupancy-derived): block partials group the same cells on every
-  // rank of a slab decomposition, so U and W stay bitwise independent of the rank count (P7)
-  int G = std::min(SG_GMAX, g.dims[0]);
-  int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * g.dims[1] * g.dims[2];
+  // rank of a slab decomposition, so U and W stay bitwise independent of the rank count (P7).
+  // 4 warps per block (96-cell segments) when that still leaves >= ~8 waves of blocks (large grids:
+  // C3 0.728 vs 0.771 ms), else 2 (48 cells; C1 0.028 vs 0.037 ms) -- from the global grid only.
+  const int64_t rows = (int64_t)g.dims[1] * g.dims[2];
+  int NW = 2;
+  if ((int64_t)((g.dims[0] + SgCfg<4>::GMAX - 1) / SgCfg<4>::GMAX) * rows >= 4736) NW = 4;
+  int G = std::min(NW == 4 ? SgCfg<4>::GMAX : SgCfg<2>::GMAX, g.dims[0]);
+  int64_t blocks = (int64_t)((g.dims[0] + G - 1) / G) * rows;
   if (blocks > ctx->max_blocks) return 0;
+  ctx->seg_nw = NW;
   return G;
 }
 
@@ -321,14 +328,19 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
     if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
       const int nseg = (g.dims[0] + Gseg - 1) / Gseg;
       const int bpl_s = nseg * g.dims[1];
-      const size_t smem_s = sizeof(SgSmem);
+      const size_t smem_s = ctx->seg_nw == 4 ? sizeof(SgSmem<4>) : sizeof(SgSmem<2>);
       bpl = bpl_s;
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SEGMENT;
-      k_pairs_seg<DIGEST><<<nblocks, SG_NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs, ctx->nh, gid,
-                                                      (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg,
-                                                      nseg, bpl, layer0);
+      if (ctx->seg_nw == 4)
+        k_pairs_seg<DIGEST, 4><<<nblocks, SgCfg<4>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
+                                                                   ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
+                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0);
+      else
+        k_pairs_seg<DIGEST, 2><<<nblocks, SgCfg<2>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
+                                                                   ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
+                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
@@ -971,8 +983,10 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs<float, true>, sizeof(K3Smem<float>)},
         {(const void*)k_pairs<double, false>, sizeof(K3Smem<double>)},
         {(const void*)k_pairs<double, true>, sizeof(K3Smem<double>)},
-        {(const void*)k_pairs_seg<false>, sizeof(SgSmem)},
-        {(const void*)k_pairs_seg<true>, sizeof(SgSmem)}};
+        {(const void*)k_pairs_seg<false, 2>, sizeof(SgSmem<2>)},
+        {(const void*)k_pairs_seg<true, 2>, sizeof(SgSmem<2>)},
+        {(const void*)k_pairs_seg<false, 4>, sizeof(SgSmem<4>)},
+        {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)}};
     for (const KA& a : ka) {
       cudaError_t e = cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
       if (e != cudaSuccess) {
