@@ -145,9 +145,9 @@ def workload(k: int):
     return W.make(k)
 
 
-def oracle_sample(w, q32, sample: int, seed: int = 0, prec: str = "f32"):
+def oracle_sample(w, q32, sample: int, seed: int = 0, prec: str = "f32", variant: str = "do"):
     """The CPU oracle as it stands on a bounded sample of the workload: full O(N)
-    DO cell-list build, pair loop for `sample` random particles; extrapolated to
+    cell-list build (the bench's variant), pair loop for `sample` random particles; extrapolated to
     one full force evaluation.  Returns (interactions/s unordered, seconds per
     full evaluation, sample description, threads)."""
     import oracle
@@ -155,7 +155,7 @@ def oracle_sample(w, q32, sample: int, seed: int = 0, prec: str = "f32"):
     qo = oracle.wrap(q32.astype(np.float64), w.L, prec)
     rng = np.random.default_rng(seed)
     idx = np.sort(rng.choice(len(qo), size=sample, replace=False))
-    r = oracle.evaluate(oracle.DO, qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx, want=())
+    r = oracle.evaluate(oracle.DS if variant == "ds" else oracle.DO, qo, w.L, w.rc, w.eps, w.sigma, w.ushift, idx=idx, want=())
     n = len(qo)
     t_full = r.t_build + r.t_eval * (n / sample)
     inter_full = r.interactions * (n / sample) / 2.0
@@ -175,7 +175,7 @@ def run_reference(args):
     sample = min(args.ref_sample, w.n)
     vals, times = [], []
     for s in range(args.warmup + args.steps):
-        v, tf, r, thr = oracle_sample(w, q, sample, seed=s, prec=prec)
+        v, tf, r, thr = oracle_sample(w, q, sample, seed=s, prec=prec, variant=args.variant)
         if s >= args.warmup:
             vals.append(v)
             times.append(tf)
@@ -185,9 +185,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
-        "config": {"workload": f"C{args.config}", "n": w.n, "variant": "do", "box": box_text(w)},
+        "config": {"workload": f"C{args.config}", "n": w.n, "variant": args.variant, "box": box_text(w)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
-                         "sample": f"per step: full O(N) DO cell build + pair loop of {sample} random particles, "
+                         "sample": f"per step: full O(N) {args.variant.upper()} cell build + pair loop of {sample} random particles, "
                                    f"extrapolated to one force evaluation of all {w.n}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -522,9 +522,9 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, tf, r, thr = oracle_sample(w, q, min(args.ref_sample, w.n), prec=prec)
+        v, tf, r, thr = oracle_sample(w, q, min(args.ref_sample, w.n), prec=prec, variant=args.variant)
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
-               "sample": f"full O(N) DO cell build + pair loop of {args.ref_sample} random particles of C{args.config}, "
+               "sample": f"full O(N) {args.variant.upper()} cell build + pair loop of {args.ref_sample} random particles of C{args.config}, "
                          f"extrapolated to one force evaluation ({tf:.1f} s)"}
 
     if rank == 0:
