@@ -952,10 +952,11 @@ __device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<fl
     float r2a, r2b;
     upk2(fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX))), r2a, r2b);
     const bool fa = !DIGEST && r2a >= split2 && r2a < lo32, fb = !DIGEST && r2b >= split2 && r2b < lo32;
-    stsq(qc, aa);
-    qc += (va && !fa) ? K3_QSTRIDE : 0u;
-    stsq(qc, ab);
-    qc += (vb && !fb) ? K3_QSTRIDE : 0u;
+    const bool qa = va && !fa, qb = vb && !fb;  // close / band hits (predicated stores: no wavefront otherwise)
+    if (qa) stsq(qc, aa);
+    qc += qa ? K3_QSTRIDE : 0u;
+    if (qb) stsq(qc, ab);
+    qc += qb ? K3_QSTRIDE : 0u;
     float ia, ib;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(r2a));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(r2b));
