@@ -446,6 +446,140 @@ def test_sllod_equilibrium_is_velocity_verlet_energy_conserving():
     assert max(abs(e - E0) for e in Es) < 2e-3 * abs(E0)
 
 
+def _lattice_residual(q, q_ref, L):
+    """max over particles of the distance (in fractional units of L) from q - q_ref to the
+    nearest lattice vector L n: zero iff q is an image of q_ref."""
+    d = np.linalg.solve(L, (q - q_ref).T).T
+    return np.abs(d - np.round(d)).max()
+
+
+def test_sllod_shear_free_flight_is_a_straight_line():
+    """F = 0, p0 != 0, shear A (A^2 = 0): SLLOD's lab velocity v = p/m + A q
+    is a constant of the free motion (dq/dt = p/m + A q, dp/dt = -A p, so
+    dv/dt = A^2 q = 0), hence the lab trajectory is the straight line
+    q_n = q0 + n dt (p0/m + A q0) -- exactly, for any dt, since the discrete
+    map's E(dt/2) E(-dt/2) = I - A^2 dt^2/4 = I.  Wrapping and the Lees-Edwards
+    resets only replace q by a lattice image q + L_t n, whose velocity is
+    v + A L_t n, so q_n must equal the straight line modulo
+    the lattice L_t at every step.  Fails for E(+dt/2) on p, for a
+    drift without the E(dt/2) factor, or for a lab/peculiar mix-up."""
+    rng = np.random.default_rng(11)
+    a, rate, m = 10.0, 0.7, 1.3
+    for gamma0 in (0.0, 0.31, -0.45):
+        L0 = np.array([[a, gamma0 * a, 0.0], [0.0, a, 0.0], [0.0, 0.0, a]])
+        A = np.zeros((3, 3)); A[0, 1] = rate
+        b = obox.Box(L0, A, "le", 0.0)
+        q0 = oracle.wrap(rng.uniform(0, 1, size=(64, 3)) @ L0.T, L0)
+        p0 = rng.normal(size=(64, 3))
+        v0 = p0 / m + q0 @ A.T
+        q, p, F = q0.copy(), p0.copy(), np.zeros_like(q0)
+        dt = 0.05
+        nres = 0
+        for n in range(1, 121):  # t = 6: the tilt passes the half-spacing reset ~4 times
+            g_before = b.L[0, 1]
+            q, p, F, _, _ = obox.sllod_step(q, p, F, b, dt, _zero_forces, mass=m)
+            nres += int(b.L[0, 1] < g_before)
+            assert _lattice_residual(q, q0 + n * dt * v0, b.L) < 1e-12
+            # peculiar momenta themselves follow p(t) = e^{-At} p0 = (I - A t) p0 exactly
+            assert np.abs(p - p0 @ (np.eye(3) - A * n * dt).T).max() < 1e-12 * np.abs(p0).max() * (1 + rate * n * dt)
+        assert nres >= 3
+
+
+def _exact_free_flight_diag(q0, p0, a_diag, t, m):
+    """Closed form of dq/dt = p/m + A q, dp/dt = -A p for diagonal A = diag(a):
+    p(t) = e^{-at} p0, q(t) = e^{at} q0 + (e^{at} - e^{-at}) / (2a) p0/m  (t p0/m for a = 0)."""
+    a = np.asarray(a_diag, dtype=np.float64)
+    g = np.where(a != 0.0, np.sinh(a * t) / np.where(a != 0.0, a, 1.0), t)
+    return np.exp(a * t) * q0 + g * p0 / m, np.exp(-a * t) * p0
+
+
+def _free_flight_run(box_factory, q0, p0, T, nsteps, m):
+    b = box_factory()
+    q, p, F = q0.copy(), p0.copy(), np.zeros_like(q0)
+    dt = T / nsteps
+    nremap = 0
+    for _ in range(nsteps):
+        Lb = b.L.copy()
+        q, p, F, _, _ = obox.sllod_step(q, p, F, b, dt, _zero_forces, mass=m)
+        nremap += int(np.abs(np.linalg.solve(obox.expm(b.A, dt) @ Lb, b.L) - np.eye(3)).max() > 0.5)
+    return q, p, b, nremap
+
+
+def test_sllod_elongational_free_flight_converges_to_exact_solution():
+    """F = 0, diagonal A (KR planar, and the generalized-KR uniaxial /
+    biaxial flows, P:431-439 with R23): the momentum factor gives
+    p_n = e^{-A n dt} p0 exactly (to rounding) and the positions converge at
+    SECOND order to the exact ODE solution e^{At} q0 + (e^{At} - e^{-At}) (2A)^{-1} p0/m,
+    modulo the lattice of the remapped box (the remaps happen inside the runs):
+    halving dt quarters the error.  A wrong sign in E(-dt/2), a missing E(dt/2) drift
+    factor or a first-order splitting fails this."""
+    rng = np.random.default_rng(12)
+    m = 0.8
+    a = 12.0
+    cases = []
+    L0kr, _ = obox.kr_initial_basis(a)
+    eps = 0.5
+    Akr = np.diag([eps, -eps, 0.0])
+    tstar = math.log((3.0 + math.sqrt(5.0)) / 2.0) / eps
+    cases.append((Akr, lambda: obox.Box(L0kr, Akr, "kr", tstar - 0.6), tstar - 0.6))
+    L0g, om1, om2 = obox.gkr_construction(a)
+    for ad in ((-1.0, -1.0, 2.0), (1.0, 1.0, -2.0)):
+        Ag = np.diag(eps * np.array(ad))
+        bb = obox.Box(L0g, Ag, "gkr", 0.0, om1=om1, om2=om2)
+        # start 0.6 before alpha_2 crosses a half-integer: a reset inside the run
+        t_cross = (0.5 / abs(bb.beta[1] * bb.eps))
+        t0 = t_cross - 0.6
+        cases.append((Ag, (lambda Ag=Ag, t0=t0: obox.Box(L0g, Ag, "gkr", t0, om1=om1, om2=om2)), t0))
+    T = 1.5
+    for A, factory, t0 in cases:
+        Lstart = factory().L
+        q0 = oracle.wrap(rng.uniform(0, 1, size=(48, 3)) @ Lstart.T, Lstart)
+        p0 = rng.normal(size=(48, 3)) * 2.0
+        errs = []
+        for nsteps in (60, 120, 240):
+            q, p, b, nremap = _free_flight_run(factory, q0, p0, T, nsteps, m)
+            assert nremap >= 1, "the run must cross a remap"
+            q_ex, p_ex = _exact_free_flight_diag(q0, p0, np.diag(A), T, m)
+            assert np.abs(p - p_ex).max() < 1e-13 * np.abs(p0).max() * 4
+            errs.append(_lattice_residual(q, q_ex, b.L))
+        assert errs[0] > 1e-9  # the splitting error is visible at all (not trivially exact)
+        r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+        assert 3.6 < r1 < 4.4 and 3.6 < r2 < 4.4, (errs, r1, r2)
+
+
+def test_expm_matches_closed_forms():
+    """e^{As} for non-diagonal, non-nilpotent A (the scaling-and-squaring branch) against
+    closed forms (to 1e-14 per unit of |As|): (a) a rotation generator gives the rotation
+    matrix by angle theta s;
+    (b) a random diagonalizable traceless A = V D V^{-1} gives V e^{Ds} V^{-1} (eigen-
+    decomposition written out, not through expm); (c) diagonal and shear (nilpotent)
+    branches: elementwise exp and exactly I + As."""
+    for theta, s in ((0.3, 1.0), (1.7, 2.5), (-4.0, 3.0), (1e-3, 0.5)):
+        G = np.array([[0.0, -theta, 0.0], [theta, 0.0, 0.0], [0.0, 0.0, 0.0]])
+        c, sn = math.cos(theta * s), math.sin(theta * s)
+        R = np.array([[c, -sn, 0.0], [sn, c, 0.0], [0.0, 0.0, 1.0]])
+        # scaling and squaring amplifies rounding ~ linearly in |As| (each squaring doubles it)
+        assert np.abs(obox.expm(G, s) - R).max() < 1e-14 * max(1.0, abs(theta * s))
+    rng = np.random.default_rng(13)
+    for _ in range(20):
+        Q, _ = np.linalg.qr(rng.normal(size=(3, 3)))
+        V = Q + 0.2 * rng.normal(size=(3, 3))  # non-orthogonal, well conditioned
+        if np.linalg.cond(V) > 5:
+            continue
+        dvals = rng.uniform(-1.0, 1.0, size=3)
+        dvals -= dvals.mean()  # traceless (P:138)
+        Vi = np.linalg.inv(V)
+        A = V @ np.diag(dvals) @ Vi
+        for s in (0.1, 1.0, 3.0):
+            E = V @ np.diag(np.exp(dvals * s)) @ Vi
+            nrm = max(1.0, np.abs(A * s).sum(axis=1).max())
+            assert np.abs(obox.expm(A, s) - E).max() < 1e-14 * nrm * max(1.0, np.abs(E).max()) * np.linalg.cond(V)
+    D = np.diag([0.2, -0.5, 0.3])
+    assert np.array_equal(obox.expm(D, 2.0), np.diag(np.exp(np.array([0.4, -1.0, 0.6]))))
+    S = np.zeros((3, 3)); S[0, 1] = 0.75
+    assert np.array_equal(obox.expm(S, 3.0), np.array([[1.0, 2.25, 0.0], [0.0, 1.0, 0.0], [0.0, 0.0, 1.0]]))
+
+
 def test_fig9_long_run_efficiency_matches_paper():
     """Paper's efficiency study: uniaxial A = diag(0.05, -0.025, -0.025),
     a = 10 d_cut, d_cut = (3/4pi)^(1/3) (interaction volume 1); long-run mean
