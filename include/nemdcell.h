@@ -65,8 +65,9 @@ typedef enum {
     NC_E_FLOW = 4,       /* |tr A| > 1e-12 max(1, max|A_ij|): flow not incompressible */
     NC_E_STATE = 5,      /* call order: no box / flow / state set yet */
     NC_E_CUDA = 6,       /* a CUDA runtime error (text in nc_last_error) */
-    NC_E_NCCL = 7,       /* reserved for the multi-GPU slab path */
-    NC_E_OOM = 8,        /* n or the cell count exceeds what was allocated */
+    NC_E_NCCL = 7,       /* an NCCL call of the slab path failed (text in nc_last_error) */
+    NC_E_OOM = 8,        /* n or the cell count exceeds what was allocated; a cell above the pair kernel's
+                            staging capacity (448 particles); a pair list above its cap */
     NC_E_NONFINITE = 9   /* a non-finite force, energy or virial was produced */
 } nc_status;
 
@@ -173,7 +174,8 @@ nc_status nc_compute_sync(nc_ctx *ctx, double *U, double W[6]);
 
 /* Load the resident particle state: positions q and PECULIAR momenta p
  * (n x 3, device or host, R19), particle ids gid (int64, may be NULL for
- * 0..n-1).  Computes the initial forces.  Errors: as nc_compute_forces. */
+ * 0..n-1; otherwise a permutation of 0..n-1, NC_E_ARG if not: outputs are indexed
+ * by gid).  Computes the initial forces.  Errors: as nc_compute_forces. */
 nc_status nc_set_state(nc_ctx *ctx, const void *q, const void *p, const int64_t *gid, int64_t n);
 
 /* Advance the resident state by nsteps SLLOD velocity-Verlet steps of size
@@ -203,6 +205,32 @@ nc_status nc_get_cells(nc_ctx *ctx, int64_t *cell_of, int64_t *cell_start, int32
  * of the canonical displacement d = (q_j + L n) - q_i.  Runs a separate
  * digest evaluation of the last built cells (not on the timed path). */
 nc_status nc_get_pair_digest(nc_ctx *ctx, uint32_t *cnt, uint64_t *hsum, uint64_t *hxor);
+
+/* Full pair set of the last built cells (small N only): a separate digest evaluation (the same
+ * kernel, membership decisions and tier split as the timed one) that also lists every ordered
+ * pair (i, j, n) of the pair set P as 5 int32 per pair --
+ * gid_i, gid_j, n1, n2, n3, with n the lattice image of the canonical displacement
+ * d = (q_j + L n) - q_i -- sorted ascending by (gid_i, gid_j, n1, n2, n3) into i_j_n (host,
+ * 5 x cap int32).  *npairs receives the count.  Errors: NC_E_STATE (no cells), NC_E_ARG,
+ * NC_E_OOM if the list is longer than cap (*npairs still holds the count), NC_E_CUDA. */
+nc_status nc_get_pairs(nc_ctx *ctx, int64_t cap, int32_t *i_j_n, int64_t *npairs);
+
+/* Cell contents of the last build (parity of the counting sort, R27): gid of every slot of the
+ * cell-sorted order (host int64, n); cell c holds slots [cell_start[c], cell_start[c+1]) of
+ * nc_get_cells, in ascending gid.  Errors: NC_E_STATE, NC_E_ARG. */
+nc_status nc_get_cell_gids(nc_ctx *ctx, int64_t *gid_sorted);
+
+/* Per-particle interaction counts written by the TIMED pair kernel of the last force evaluation
+ * (nc_compute_forces / nc_set_state / nc_step_sllod; not a digest run): cnt[gid] (host uint32, n).
+ * A digest or pair-list call is itself an evaluation: read the counts before it.  Errors:
+ * NC_E_STATE (no evaluation), NC_E_ARG. */
+nc_status nc_get_pair_counts(nc_ctx *ctx, uint32_t *cnt);
+
+/* Test hooks.  NC_DBG_DROP_ENTRIES = 1 drops the LAST entry of every neighborhood (a truncated
+ * stencil: the negative control that parity tests must catch); 0 restores the method.  Takes
+ * effect at the next nc_set_box / step.  Errors: NC_E_ARG. */
+enum { NC_DBG_DROP_ENTRIES = 1 };
+nc_status nc_debug(nc_ctx *ctx, int what, int value);
 
 /* Instrumentation of the last evaluation. */
 nc_status nc_get_stats(nc_ctx *ctx, nc_stats *out);

@@ -78,6 +78,12 @@ struct Geom {
   double rsplit2;           // fp32-mode pairs with r^2 >= rsplit2 (and below band_lo) use fp32 force math
   // fp32 copies for the fp32 kernels (constant-bank operands; set by the host with the above)
   float f_split2, f_lo, f_hi, f_sig2, f_c48, f_m24;
+  // cell centre in the cell-local rotated frame (fp32 staging is centred on it), and the tensor-core
+  // filter's superset bound on r^2 (kernels.cuh, mma_filter)
+  double cc[3];
+  float f_cc[3];
+  float f_hmma;
+  int dbg_drop;     // negative control (nc_debug): drop this many entries from every neighborhood
 };
 
 enum { GEOM_OK = 0, GEOM_BAD_BOX = 1, GEOM_DEGENERATE = 2 };

@@ -242,6 +242,7 @@ __device__ bool sg_setup(const Geom& g, const uint32_t* __restrict__ cs, const f
         c0 = (int)floor(__dsub_rn((double)(a0 - 1), sm.r_ox[r]));
         c1 = (int)ceil(__dsub_rn((double)(a0 + 2), sm.r_ox[r]));
       }
+      if (r == nrows - 1) c1 -= g.dbg_drop;  // negative control (nc_debug): the last entry of build_entries
       ns += c1 - c0;
       const int eb = sm.r_eb[r] - sm.r_lo[r];
       sm.rg[tid][r][0] = sm.e_off[eb + c0];
@@ -262,7 +263,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem<NW>& sm, con
                                         const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                                         const uint32_t* __restrict__ gid, uint32_t qb, int nq, uint32_t me,
                                         uint32_t nh_i, int A, double uix, double uiy, double uiz, double wx64,
-                                        double lo64, double hi64, Acc& acc) {
+                                        double lo64, double hi64, Acc& acc, const PairOut& po, uint32_t gi) {
   const int qmax = __reduce_max_sync(0xffffffffu, nq);
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   for (int q0 = 0; q0 < qmax; q0 += 4) {
@@ -317,13 +318,7 @@ __device__ __forceinline__ void sg_eval(const Geom& g, const SgSmem<NW>& sm, con
       acc.w0 += tx * dx; acc.w1 += ty * dy; acc.w2 += tz * dz;
       acc.w3 += tx * dy; acc.w4 += tx * dz; acc.w5 += ty * dz;
       acc.cnt += ok ? 1u : 0u;
-      if (DIGEST && ok) {
-        const uint64_t key = (uint64_t)gid[j] | ((uint64_t)(n0 + 8) << 32) | ((uint64_t)(n1 + 8) << 36) |
-                             ((uint64_t)(n2 + 8) << 40);
-        const uint64_t hh = mix64(key);
-        acc.hs += hh;
-        acc.hx ^= hh;
-      }
+      if (DIGEST && ok) digest_add<DIGEST>(acc, gid, j, n0, n1, n2, po, gi);
     }
   }
   __syncwarp();
@@ -335,7 +330,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
             const float4* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
             float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
             uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int G, int nseg,
-            int bpl, int layer0) {
+            int bpl, int layer0, const PairOut po) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int SG_NT = SgCfg<NW>::NT, SG_CAP = SgCfg<NW>::CAP, SG_NW = NW;
   (void)SG_NT;
@@ -362,8 +357,8 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
       if (Gs == 1) { Gs = 0; break; }  // a single cell's neighborhood above SG_CAP: flagged below
       Gs = (Gs + 1) / 2;
     }
-    if (Gs == 0) {  // cannot stage (cells of > ~20 particles): report as non-finite so the host fails loudly
-      tNF += 1.0;
+    if (Gs == 0) {  // cannot stage (cells of > ~20 particles): the host fails loudly (NC_E_OOM)
+      tNF += (tid == 0) ? K3_OVERFLOW : 0.0;
       A += 1;
       continue;
     }
@@ -398,6 +393,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
       const double4 ui = u[me];
       const double uix = ui.x + (double)(A + gc - A) * wx64, uiy = ui.y, uiz = ui.z;
       const uint32_t nh_i = (g.variant == 1 && act) ? nh[me] : 0u;
+      const uint32_t gi = DIGEST ? gid[me] : 0u;
       // candidates of i: its cell's stencil minus itself
       int T = 0;
       if (act)
@@ -413,7 +409,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
         const int lmax = __reduce_max_sync(0xffffffffu, len);
         for (int k0 = 0; k0 < lmax; k0 += 8) {
           if (__any_sync(0xffffffffu, nq > SG_QCAP - 8)) {  // room for 8 more hits in every queue
-            sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+            sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc, po, gi);
             nq = 0;
           }
           const int kend = min(lmax, k0 + 8);
@@ -428,7 +424,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
           }
         }
       }
-      sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc);
+      sg_eval<DIGEST, NW>(g, sm, u, qs, nh, gid, qb, nq, me, nh_i, A, uix, uiy, uiz, wx64, lo64, hi64, acc, po, gi);
       const double fx = acc.fx, fy = acc.fy, fz = acc.fz, uu = acc.u;
       const double w0 = acc.w0, w1 = acc.w1, w2 = acc.w2, w3 = acc.w3, w4 = acc.w4, w5 = acc.w5;
       const uint32_t cnt = acc.cnt, nrc = acc.nrc;
@@ -437,7 +433,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
         const double Ui = 2.0 * g.eps * uu - 0.5 * g.ushift * (double)cnt;
         Fout[me] = make_float4((float)(g.Q[0] * fx + g.Q[1] * fy + g.Q[2] * fz),
                                (float)(g.Q[3] * fx + g.Q[4] * fy + g.Q[5] * fz),
-                               (float)(g.Q[6] * fx + g.Q[7] * fy + g.Q[8] * fz), 0.0f);
+                               (float)(g.Q[6] * fx + g.Q[7] * fy + g.Q[8] * fz), __uint_as_float(cnt));
         if (DIGEST) { dcnt[me] = cnt; dhs[me] = hs; dhx[me] = hx; }
         tU += Ui;
         tW[0] += 0.5 * w0; tW[1] += 0.5 * w1; tW[2] += 0.5 * w2;

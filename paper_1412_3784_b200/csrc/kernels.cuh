@@ -403,7 +403,7 @@ k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __res
 // ---------------------------------------------------------------------------
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 64;  // permanent far element (padding slot of the evaluation)
-constexpr int K3_STAGE = K3_CAP + 66;  // + up to 2S far sentinels so the filter needs no bounds checks (even: 8-byte pairs)
+constexpr int K3_STAGE = K3_CAP + 66;  // fp64 mode: + up to S far sentinels so the filter needs no bounds checks
 #ifndef K3_QCAP_OVR
 #define K3_QCAP_OVR 48
 #endif
@@ -442,10 +442,15 @@ constexpr int K3_CELLS = K3_CELLS_OVR;  // fewest cells per warp (= per block: o
 constexpr int NPART = 13;       // U, W0..W5, interactions, candidates, stencil cells, rechecks, fp32-tier interactions, nonfinite
 constexpr double K3_BAND64 = 1e-12;
 
+// fp32 mode: staged x, y, z (image bracket applied, centred on the center cell) and |v|^2 as four
+// arrays of stride K3_SSTR floats.  K3_SSTR = 8 (mod 32): the four words one mma B fragment takes
+// (lane (g, t) reads component t of element 8k + g) fall in four disjoint bank octets.
+constexpr int K3_SSTR = 520;
+constexpr int K3_HW = (K3_CAP + 127) / 128;  // hit words per (row, MMA stream): 16 column blocks each
+static_assert(K3_SSTR % 32 == 8 && K3_SSTR > K3_DUMMY && 128 * K3_HW <= K3_DUMMY, "staging stride / padding");
 template <typename T>
-struct K3Stage64 {  // fp32 mode: staged x, y, z (image bracket applied) as separate arrays, entry brackets
-  float sx[K3_STAGE], sy[K3_STAGE], sz[K3_STAGE];
-  float Bf[K3_MAXE][3];
+struct K3Stage64 {
+  float sc[4][K3_SSTR];
 };
 template <>
 struct K3Stage64<double> {  // fp64 mode: stage holds LAB positions; packed DO home shift of each j
@@ -457,11 +462,23 @@ struct K3Smem {
   typename V4<T>::t stage[sizeof(T) == 8 ? K3_STAGE : 1];  // fp64 mode: staged lab positions, .w = sorted index
   K3Stage64<T> s64;
   K3QT queue[sizeof(T) == 4 ? K3_CQ : K3_QCAP][32];  // fp32: close-tier queue; fp64: survivor queue
-  uint32_t mq[sizeof(T) == 4 ? K3_MW : 1][32];         // fp32: hit words mq[w][lane]
+  union {  // fp32: the entries' fp32 brackets while staging, then the hit words [row][MMA stream t][word w]
+    float Bf[K3_MAXE][3];
+    uint32_t hw[sizeof(T) == 4 ? 16 * 4 * K3_HW : 1];
+  };
   uint8_t sent[K3_STAGE];
   uint32_t e_start[K3_MAXE], e_cnt[K3_MAXE], e_off[K3_MAXE];
-  int32_t e_n[K3_MAXE][3];
+  int8_t e_n[K3_MAXE][3];  // lattice image shift of the entry (|n_k| <= 2)
+  int e_center;            // the entry of the center cell itself (build_entries)
   double e_B[K3_MAXE][3];
+};
+
+// Full (i, j, n) pair lists for nc_get_pairs (digest instantiations only; small N): one global
+// atomic slot per ordered pair, the host sorts.
+struct PairOut {
+  int32_t* ijn;            // 5 x int32 per pair: gid_i, gid_j, n1, n2, n3
+  unsigned long long* n;   // pairs found (may exceed cap: the host reports the count)
+  long long cap;
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -492,8 +509,9 @@ __device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int 
       sm.e_B[lane][1] = g.R[4] * u1 + g.R[5] * u2;
       sm.e_B[lane][2] = g.R[8] * u2;
     }
+    if (lane == 0) sm.e_center = 13;  // delta = (0, 0, 0)
     __syncwarp();
-    return 27;
+    return 27 - g.dbg_drop;  // dbg_drop > 0 only for the negative-control test (nc_debug)
   }
   // DO: lanes 0..11 = (layer dz, row index ri)
   int ncols = 0, c0 = 0, m = 0, n2 = 0, n3 = 0, kd = 0, jd = 0, dz = 0;
@@ -524,6 +542,8 @@ __device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int 
   }
   int total = __shfl_sync(0xffffffffu, x, 15);
   int off = x - ncols;
+  // the center cell: layer dz = 0 (n3 = 0), its middle row m = a1 (n2 = 0, ri = 1, lane 5), middle column
+  if (lane == 5) sm.e_center = off + 1;
   for (int t = 0; t < ncols; ++t) {
     int col = c0 + t;
     int n1 = floordiv(col, l1);
@@ -536,7 +556,7 @@ __device__ __forceinline__ int build_entries(const Geom& g, int a0, int a1, int 
     sm.e_B[e][2] = (double)dz * g.w[2] + (double)n3 * g.e[2];
   }
   __syncwarp();
-  return total;
+  return total - g.dbg_drop;
 }
 
 // Per-lane accumulators: F (lab frame in fp64 mode, rotated in fp32 mode),
@@ -575,6 +595,8 @@ struct PairCtx {
   const uint32_t* nh;
   const uint32_t* gid;
   uint32_t nh_i;
+  PairOut po;          // digest instantiations: optional full pair list
+  uint32_t gi;         // gid of i (pair lists)
 };
 
 __device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
@@ -643,13 +665,21 @@ __device__ __forceinline__ void lj_accumulate(double sig2, double eps24, Acc& ac
 }
 
 template <bool DIGEST>
-__device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32_t j, int n0, int n1, int n2) {
+__device__ __forceinline__ void digest_add(Acc& acc, const uint32_t* gid, uint32_t j, int n0, int n1, int n2,
+                                           const PairOut& po, uint32_t gi) {
   if (DIGEST) {
     uint64_t key = (uint64_t)gid[j] | ((uint64_t)(n0 + 8) << 32) | ((uint64_t)(n1 + 8) << 36) |
                    ((uint64_t)(n2 + 8) << 40);
     uint64_t h = mix64(key);
     acc.hs += h;
     acc.hx ^= h;
+    if (po.ijn) {
+      const unsigned long long k = atomicAdd(po.n, 1ull);
+      if ((long long)k < po.cap) {
+        int32_t* o = po.ijn + 5 * k;
+        o[0] = (int32_t)gi; o[1] = (int32_t)gid[j]; o[2] = n0; o[3] = n1; o[4] = n2;
+      }
+    }
   }
 }
 
@@ -669,7 +699,7 @@ __device__ __forceinline__ void eval_one(const Geom& g, const PairCtx<T>& pc, co
   double dz = exact_d(g, 2, v.z, pc.uz, n0, n1, n2);
   double r2 = dx * dx + dy * dy + dz * dz;
   lj_accumulate(sig2, eps24, acc, dx, dy, dz, r2);
-  digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2);
+  digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2, pc.po, pc.gi);
 }
 
 // Evaluate the queued filter survivors of every lane (warp-uniform loop, two
@@ -784,7 +814,7 @@ __device__ __forceinline__ uint32_t qaddr(K3QT e, uint32_t stage0) { return addr
 
 // fp32 staging is three float arrays (sx, sy, sz): a broadcast LDS.32 is one shared-memory
 // wavefront, a 16-byte LDS.128 four (the filter is bound by the shared-memory pipe)
-constexpr uint32_t K3_YOFF = 4u * K3_STAGE, K3_ZOFF = 8u * K3_STAGE;  // bytes from sx to sy, sz
+constexpr uint32_t K3_YOFF = 4u * K3_SSTR, K3_ZOFF = 8u * K3_SSTR;  // bytes from the x array to y, z
 __device__ __forceinline__ float ldsf(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -878,8 +908,8 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
     acc.w3 += txa * dya + txb * dyb; acc.w4 += txa * dza + txb * dzb; acc.w5 += tya * dza + tyb * dzb;
     acc.cnt += (oka ? 1u : 0u) + (okb ? 1u : 0u);
     if (DIGEST) {
-      if (oka) digest_add<DIGEST>(acc, pc.gid, ja, na0, na1, na2);
-      if (okb) digest_add<DIGEST>(acc, pc.gid, jb, nb0, nb1, nb2);
+      if (oka) digest_add<DIGEST>(acc, pc.gid, ja, na0, na1, na2, pc.po, pc.gi);
+      if (okb) digest_add<DIGEST>(acc, pc.gid, jb, nb0, nb1, nb2, pc.po, pc.gi);
     }
   };
   // queue entry k of this lane -> staged index t, sorted index j (pc.my + dummy for none), entry e
@@ -898,182 +928,247 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
   }
 }
 
-// Mask mode.  Lane (i, s) of an i-batch with S streams filters the staged element PAIRS
-// {2k, 2k+1}, k = s, s+S, ... (one "pair step" = one LDS.64 per coordinate: the S lanes of a step
-// read S distinct 8-byte words, one shared-memory wavefront for S <= 2).  Hits are bits of per-lane
-// 32-bit words, bit 31 - (2q + h) for element 2(s + S(16w + q)) + h of word w; one STS.32 per word.
-
-// pop this lane's next hit (highest bit of the current word; returns its staged address) and
-// refill the word when it empties
-__device__ __forceinline__ uint32_t pop_hit(uint32_t& cur, uint32_t& wa, uint32_t& wq, uint32_t wend, uint32_t step2m8,
-                                            uint32_t wstep, bool& valid) {
-  valid = cur != 0;
-  const uint32_t c = (uint32_t)__clz(cur);  // candidate 2q + h of the highest hit (32 if none)
-  cur ^= 0x80000000u >> c;                  // shift by 32 gives 0: nothing to clear
-  const uint32_t cc = valid ? c : 0u;       // idle lanes read element 0 of their word: finite, masked
-  // element 2(s + S(16w + q)) + h lies at wa + 8 S q + 4 h = wa + 4 cc + (8 S - 8) q
-  const uint32_t a = wa + 4u * cc + step2m8 * (cc >> 1);
-  if (cur == 0 && wq < wend) {
-    cur = ldsu(wq);
-    wq += 128u;
-    wa += wstep;
-  }
-  return a;
-}
-
-// Far tier straight from the hit words, two hits per iteration on packed fp32x2 (FADD2/FMUL2/FFMA2)
-// with packed partial sums folded into the fp64 Acc once per chunk.  Everything else (r < r_split,
-// the cutoff band, every hit in digest mode) is compacted into the close queue, which is handed
-// to the fp64 tier whenever some lane's queue is nearly full, and at the end.
-template <bool DIGEST>
-__device__ __forceinline__ void eval_masks_f32x2(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 uint32_t& nfar, int qits, int nhit, int nw, uint32_t sa0,
-                                                 uint32_t step2, int lane, uint32_t stage0,
-                                                 const double4* __restrict__ u64) {
-  // qits = this lane's hits + empty words (an empty word costs one idle pop)
-  const int qmax = __reduce_max_sync(0xffffffffu, qits);
-  const float split2 = g.f_split2, lo32 = g.f_lo;
-  const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
-  const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), C48 = pk2(g.f_c48, g.f_c48), M24 = pk2(g.f_m24, g.f_m24),
-                 NEG1 = pk2(-1.0f, -1.0f);
-  const uint32_t wstep = 16u * step2;  // bytes of staged elements covered by one hit word
-  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
-  const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
-  uint32_t cur = nw > 0 ? ldsu(mq0) : 0u, wa = sa0, wq = mq0 + 128u, wend = mq0 + 128u * (uint32_t)nw;
-  uint32_t qc = qc0;
-  int nclose_all = 0;
-  uint64_t Fx = 0, Fy = 0, Fz = 0, Uq = 0, W0 = 0, W1 = 0, W2 = 0, W3 = 0, W4 = 0, W5 = 0;  // packed partial sums
-  for (int k = 0; k < qmax; k += 2) {
-    bool va, vb;
-    const uint32_t aa = pop_hit(cur, wa, wq, wend, step2 - 8u, wstep, va);
-    const uint32_t ab = pop_hit(cur, wa, wq, wend, step2 - 8u, wstep, vb);
-    const uint64_t DX = add2(pk2(ldsf(aa), ldsf(ab)), nfx), DY = add2(pk2(ldsf(aa + K3_YOFF), ldsf(ab + K3_YOFF)), nfy),
-                   DZ = add2(pk2(ldsf(aa + K3_ZOFF), ldsf(ab + K3_ZOFF)), nfz);
-    float r2a, r2b;
-    upk2(fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX))), r2a, r2b);
-    const bool fa = !DIGEST && r2a >= split2 && r2a < lo32, fb = !DIGEST && r2b >= split2 && r2b < lo32;
-    const bool qa = va && !fa, qb = vb && !fb;  // close / band hits (predicated stores: no wavefront otherwise)
-    if (qa) stsq(qc, aa);
-    qc += qa ? K3_QSTRIDE : 0u;
-    if (qb) stsq(qc, ab);
-    qc += qb ? K3_QSTRIDE : 0u;
-    float ia, ib;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(r2a));
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(r2b));
-    const uint64_t IR = pk2((va && fa) ? ia : 0.0f, (vb && fb) ? ib : 0.0f);  // one mask per pair
-    const uint64_t S2 = mul2(SIG2, IR);
-    const uint64_t S6 = mul2(mul2(S2, S2), S2);
-    const uint64_t FR = mul2(mul2(fma2(C48, S6, M24), S6), IR);  // (48 eps s6 - 24 eps) s6 / r^2
-    const uint64_t TX = mul2(FR, DX), TY = mul2(FR, DY), TZ = mul2(FR, DZ);
-    Fx = add2(Fx, TX); Fy = add2(Fy, TY); Fz = add2(Fz, TZ);
-    Uq = fma2(S6, add2(S6, NEG1), Uq);
-    W0 = fma2(TX, DX, W0); W1 = fma2(TY, DY, W1); W2 = fma2(TZ, DZ, W2);
-    W3 = fma2(TX, DY, W3); W4 = fma2(TX, DZ, W4); W5 = fma2(TY, DZ, W5);
-    if ((k & 6) == 6 && __any_sync(0xffffffffu, qc > qclim)) {  // every 8 hits
-      __syncwarp();
-      const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
-      eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
-      __syncwarp();
-      nclose_all += nclose;
-      qc = qc0;
-    }
-  }
-  auto fold = [](uint64_t v) { float a, b; upk2(v, a, b); return (double)a + (double)b; };
-  acc.fx -= fold(Fx); acc.fy -= fold(Fy); acc.fz -= fold(Fz); acc.u += fold(Uq);
-  acc.w0 += fold(W0); acc.w1 += fold(W1); acc.w2 += fold(W2);
-  acc.w3 += fold(W3); acc.w4 += fold(W4); acc.w5 += fold(W5);
-  __syncwarp();
-  const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
-  acc.cnt += (uint32_t)(nhit - nclose_all - nclose);  // every hit is either far or went to the fp64 tier
-  nfar += (uint32_t)(nhit - nclose_all - nclose);      // this lane's fp32-tier count (roofline accounting)
-  eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
-}
-
 // (m << 1) | (v >> 31): one funnel shift
 __device__ __forceinline__ uint32_t shl_in(uint32_t m, uint32_t v) {
   uint32_t r;
   asm("shf.l.clamp.b32 %0, %1, %2, 1;" : "=r"(r) : "r"(v), "r"(m));
   return r;
 }
+
+// ---------------------------------------------------------------------------
+// NC_F32 candidate filter on the tensor cores (mma.sync m16n8k4, tf32 operands, fp32 accumulate).
+//
+// The distance check of a cell's particles i against its staged neighborhood j is a dense
+// rank-3 contraction: r^2 = |u_i|^2 + |v_j|^2 - 2 u_i . v_j.  One mma.m16n8k4 takes 16 rows i x 8
+// columns j with A row i = (-2u_i, 1), B column j = (v_j, |v_j|^2) and the fp32 accumulator input
+// C = |u_i|^2 - h per row, so the SIGN of D is the superset test r~^2 < h.  tf32 keeps 10 mantissa bits (x, y, z truncated, |v|^2 rounded):
+// |r~^2 - r^2| <= 2^-10 4.01 |u_i| |v_j| + 2^-11 |v_j|^2 + accumulation rounding, and with cell-centred
+// coordinates |u_i| <= R_i (half the cell diagonal) and |v_j| <= R_i + r_c for any pair inside the
+// cutoff, so h = r_c^2 + that bound (Geom::f_hmma, host) makes the hit set a SUPERSET of the pair
+// set; every hit is re-decided exactly by the fp32 far tier / fp64 close tier (canonical inside the
+// 1e-12 band), so the pair set is unchanged.  Lane (g = lane/4, t = lane%4) holds rows g, g+8
+// (+16, +24) and columns 8k + 2t + {0, 1}: its hit bits for row r, "MMA stream" t, are packed
+// into 32-bit words, bit 31 - (2k' + h) of word w <-> staged element 8 (16 w + k') + 2 t + h.
+// ---------------------------------------------------------------------------
+// C is a persistent register quad per row group (c[0] = c[1] = row g, c[2] = c[3] = row g + 8):
+// distinct registers, so no accumulator copies are needed per mma
+__device__ __forceinline__ void mma1684(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t b0, const float (&c)[4]) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%7,%8,%9,%10};"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a0), "r"(a1), "r"(b0), "f"(c[0]), "f"(c[1]), "f"(c[2]), "f"(c[3]));
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {  // round to the nearest tf32 (10 mantissa bits)
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// one column block: rows g, g+8 of lane (g, t), columns 8k + 2t + {0, 1}
+__device__ __forceinline__ void mma_step(uint32_t b, uint32_t a0, uint32_t a1, const float (&c)[4], uint32_t& m0,
+                                         uint32_t& m1) {
+  float d[4];
+  mma1684(d, a0, a1, b, c);
+  m0 = shl_in(m0, __float_as_uint(d[0]));
+  m0 = shl_in(m0, __float_as_uint(d[1]));
+  m1 = shl_in(m1, __float_as_uint(d[2]));
+  m1 = shl_in(m1, __float_as_uint(d[3]));
+}
+
+// 2-bit groups of a 16-bit value (group k = bits 15-2k, 14-2k) spread to bits 29-4k, 28-4k
+__device__ __forceinline__ uint32_t spread2(uint32_t x) {
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  return x;
+}
+
+// Filter W words (16 column blocks each; the staged chunk is padded to 128 W elements) into the hit
+// words of the far-tier lanes (row, s), two per row: lane (row, s) takes MMA streams s and s + 2 of
+// its row, interleaved in 2-bit groups (one shuffle with the partner lane t ^ 2, which holds the other
+// stream of the same rows): word w2 at hw[(row 2 + s) 2W + w2], bit c = 2q + h <-> staged element
+// 64 w2 + 4 q + 2 s + h -- a lane's words cover its elements in order with a uniform stride (pop_hit).
+__device__ __forceinline__ void mma_filter(uint32_t stage0, uint32_t hw0, int W, uint32_t a0, uint32_t a1,
+                                           const float (&c)[4], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t bb = stage0 + 4u * ((uint32_t)t * K3_SSTR + (uint32_t)g);  // component t of element 8k + g
+  const bool lo = t < 2;  // lane t < 2 builds row g's words (streams t, t + 2), lane t >= 2 row g + 8's
+  const uint32_t o0 = hw0 + 4u * (uint32_t)(((lo ? g : g + 8) * 2 + (t & 1)) * 2 * W);
+#pragma unroll 1
+  for (int w = 0; w < W; ++w) {
+    uint32_t m0 = 0u, m1 = 0u;
+    const uint32_t bw = bb + 512u * (uint32_t)w;
+    uint32_t b[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) b[k] = ldsu(bw + 32u * k);  // all loads of the word first
+#pragma unroll
+    for (int k = 0; k < 16; ++k) mma_step(b[k], a0, a1, c, m0, m1);
+    const uint32_t x = __shfl_xor_sync(0xffffffffu, lo ? m1 : m0, 2);
+    const uint32_t ma = lo ? m0 : x, mb = lo ? x : m1;  // streams s = t & 1 and s + 2
+    stsu(o0 + 8u * (uint32_t)w, (spread2(ma >> 16) << 2) | spread2(mb >> 16));               // blocks 0-7
+    stsu(o0 + 8u * (uint32_t)w + 4u, (spread2(ma & 0xffffu) << 2) | spread2(mb & 0xffffu));  // blocks 8-15
+  }
+}
+
+// Hit cursor over one far lane's words (mma_filter's layout): bit c = 2q + h of the current word is the
+// staged element at address wa + 16 q + 4 h = wa + 4 c + 8 (c >> 1); pop the highest hit and refill the
+// word when it empties (predicated: next word +4 bytes, element base +64 elements).
+struct HitCur {
+  uint32_t cur, wa, wq, wend;
+};
+__device__ __forceinline__ uint32_t pop_hit(HitCur& h, bool& valid) {
+  valid = h.cur != 0;
+  const uint32_t c = (uint32_t)__clz(h.cur);  // highest hit (32 if none)
+  h.cur ^= 0x80000000u >> c;                  // shift by 32 gives 0: nothing to clear
+  const uint32_t cc = valid ? c : 0u;         // idle lanes read their word's first element: finite, masked
+  const uint32_t a = h.wa + 4u * cc + 8u * (cc >> 1);
+  if (h.cur == 0 && h.wq < h.wend) {
+    h.cur = ldsu(h.wq);
+    h.wq += 4u;
+    h.wa += 256u;
+  }
+  return a;
+}
+
+// Far tier straight from the hit words, two hits per iteration on packed fp32x2 (FADD2/FMUL2/FFMA2)
+// with packed partial sums folded into the fp64 Acc once per chunk.  Each hit is re-decided from the
+// staged fp32 coordinates: r_split^2 <= r^2 < r_c^2 (1 - 1e-4) is a far pair (fp32 force math);
+// everything else (r < r_split, the cutoff band, the MMA filter's margin beyond it) is compacted into
+// the close queue, which is handed to the fp64 tier (canonical membership inside the 1e-12 band, no
+// pair beyond r_c) whenever some lane's queue is nearly full, and at the end.  Digest mode keeps
+// exactly this split (the timed kernel's membership decisions) and adds every far pair's key.
+template <bool DIGEST>
+__device__ __forceinline__ void eval_hits(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
+                                          uint32_t& nfar, uint32_t wl0, int nwords, uint32_t wa0, int lane,
+                                          uint32_t stage0, const double4* __restrict__ u64) {
+  int nhit = 0, qits = 0;  // this lane's hits and empty words (an empty word costs one idle pop)
+  for (int k = 0; k < nwords; ++k) {
+    const int c = __popc(ldsu(wl0 + 4u * k));
+    nhit += c;
+    qits += c ? c : 1;
+  }
+  HitCur h;
+  h.cur = ldsu(wl0);
+  h.wa = wa0;
+  h.wq = wl0 + 4u;
+  h.wend = wl0 + 4u * (uint32_t)nwords;
+  const int qmax = (__reduce_max_sync(0xffffffffu, qits) + 1) >> 1;  // two hits per iteration
+  const float split2 = g.f_split2, lo32 = g.f_lo;
+  const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
+  const uint64_t SIG2 = pk2(g.f_sig2, g.f_sig2), C48 = pk2(g.f_c48, g.f_c48), M24 = pk2(g.f_m24, g.f_m24),
+                 NEG1 = pk2(-1.0f, -1.0f);
+  const uint32_t qc0 = smem_u32(&sm.queue[0][lane]), qclim = qc0 + K3_QSTRIDE * (K3_CQ - 8);
+  uint32_t qc = qc0;
+  int nclose_all = 0;
+  uint64_t Fx = 0, Fy = 0, Fz = 0, Uq = 0, W0 = 0, W1 = 0, W2 = 0, W3 = 0, W4 = 0, W5 = 0;  // packed partial sums
+  // far iterations until some lane's close queue nears capacity (checked every 4 iterations = 8 hits)
+  // or the hits run out, then the fp64 tier on the queued items: one inlined copy of each tier
+  int k = 0;
+  while (true) {
+    bool flush = false;
+    for (; k < qmax; ++k) {
+      bool va, vb;
+      const uint32_t aa = pop_hit(h, va);
+      const uint32_t ab = pop_hit(h, vb);
+      const uint64_t DX = add2(pk2(ldsf(aa), ldsf(ab)), nfx), DY = add2(pk2(ldsf(aa + K3_YOFF), ldsf(ab + K3_YOFF)), nfy),
+                     DZ = add2(pk2(ldsf(aa + K3_ZOFF), ldsf(ab + K3_ZOFF)), nfz);
+      float r2a, r2b;
+      upk2(fma2(DZ, DZ, fma2(DY, DY, mul2(DX, DX))), r2a, r2b);
+      // far: r_split <= r and r^2 < r_c^2 (1 - 1e-4); everything else -- close pairs, the cutoff band and
+      // the MMA margin beyond it (the fp64 tier rejects those) -- goes to the close queue
+      const bool fa = r2a >= split2 && r2a < lo32, fb = r2b >= split2 && r2b < lo32;
+      const bool qa = va && !fa, qb = vb && !fb;  // predicated stores: no wavefront otherwise
+      if (qa) stsq(qc, aa);
+      qc += qa ? K3_QSTRIDE : 0u;
+      if (qb) stsq(qc, ab);
+      qc += qb ? K3_QSTRIDE : 0u;
+      float ia, ib;
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ia) : "f"(r2a));
+      asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ib) : "f"(r2b));
+      const uint64_t IR = pk2((va && fa) ? ia : 0.0f, (vb && fb) ? ib : 0.0f);  // one mask per pair
+      const uint64_t S2 = mul2(SIG2, IR);
+      const uint64_t S6 = mul2(mul2(S2, S2), S2);
+      const uint64_t FR = mul2(mul2(fma2(C48, S6, M24), S6), IR);  // (48 eps s6 - 24 eps) s6 / r^2
+      const uint64_t TX = mul2(FR, DX), TY = mul2(FR, DY), TZ = mul2(FR, DZ);
+      Fx = add2(Fx, TX); Fy = add2(Fy, TY); Fz = add2(Fz, TZ);
+      Uq = fma2(S6, add2(S6, NEG1), Uq);
+      W0 = fma2(TX, DX, W0); W1 = fma2(TY, DY, W1); W2 = fma2(TZ, DZ, W2);
+      W3 = fma2(TX, DY, W3); W4 = fma2(TX, DZ, W4); W5 = fma2(TY, DZ, W5);
+      if (DIGEST) {  // far pairs' keys (the close tier adds its own)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh == 0 ? (va && fa) : (vb && fb)) {
+            const uint32_t t = ((hh == 0 ? aa : ab) - stage0) >> 2;
+            const uint32_t j = sidx_of(sm, t, pc.base_off);
+            int n0, n1, n2;
+            image_of<float>(g, sm, t, g.variant == 1 ? pc.nh[j] : 0u, pc.nh_i, n0, n1, n2);
+            digest_add<DIGEST>(acc, pc.gid, j, n0, n1, n2, pc.po, pc.gi);
+          }
+        }
+      }
+      if ((k & 3) == 3 && __any_sync(0xffffffffu, qc > qclim)) {
+        flush = true;
+        ++k;
+        break;
+      }
+    }
+    __syncwarp();
+    const int nclose = (int)((qc - qc0) / K3_QSTRIDE);
+    nclose_all += nclose;
+    eval_close_f64<DIGEST>(g, pc, sm, acc, nclose, lane, stage0, u64, sm.queue);
+    __syncwarp();
+    qc = qc0;
+    if (!flush) break;
+  }
+  auto fold = [](uint64_t v) { float a, b; upk2(v, a, b); return (double)a + (double)b; };
+  acc.fx -= fold(Fx); acc.fy -= fold(Fy); acc.fz -= fold(Fz); acc.u += fold(Uq);
+  acc.w0 += fold(W0); acc.w1 += fold(W1); acc.w2 += fold(W2);
+  acc.w3 += fold(W3); acc.w4 += fold(W4); acc.w5 += fold(W5);
+  const int nf = nhit - nclose_all;  // every hit is far or went to the fp64 tier
+  acc.cnt += (uint32_t)nf;
+  nfar += (uint32_t)nf;  // this lane's fp32-tier count (roofline accounting)
+}
+
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
   uint64_t v;
   asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
   return v;
 }
 
-// Mask filter over pair steps (see above): per pair step three LDS.64 (x, y, z of elements 2k, 2k+1,
-// already packed for FADD2) and three packed ops give both r^2; hit bits are set with immediates.
-template <bool DIGEST>
-__device__ __forceinline__ void filter_chunk_f32(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
-                                                 uint32_t& nfar, int s, int S, int iters, int lane,
-                                                 const double4* __restrict__ u64) {
-  static_assert(16 * K3_MW >= (K3_CAP + 1) / 2, "hit words must cover one chunk (S = 1: ceil(K3_CAP / 2) pair steps)");
-  static_assert(K3_UNROLL % 2 == 0 && 32 % K3_UNROLL == 0, "groups of whole pair steps");
-  constexpr int G2 = K3_UNROLL / 2;  // pair steps per group
-  const uint32_t stage0 = smem_u32(&sm.s64.sx[0]);
-  const uint32_t step2 = 8u * (uint32_t)S;  // bytes between a lane's consecutive pair steps
-  const float hi = pc.hi;
-  const uint64_t nfx = pk2(-pc.fx, -pc.fx), nfy = pk2(-pc.fy, -pc.fy), nfz = pk2(-pc.fz, -pc.fz);
-  const uint32_t sa0 = stage0 + 8u * (uint32_t)s;
-  const uint32_t mq0 = smem_u32(&sm.mq[0][lane]);
-  const int iters2 = (iters + 1) >> 1;  // pair steps: ceil(ctot / 2S)
-  uint32_t sa = sa0;
-  int qlen = 0, nhit = 0, w = 0;  // qlen: hits + empty words (evaluation pops this lane needs)
-  // hit bits are shifted in from the right: (r^2 - hi) is formed inside the packed FMA chain
-  // (dx^2 - hi first) and its sign bit enters the word with one funnel shift per candidate,
-  // so candidate c of a word (c = 2q + h, 0..31) ends at bit 31 - c
-  const uint64_t NHI = pk2(-hi, -hi);
-  auto pair_step = [&](uint64_t X, uint64_t Y, uint64_t Z, uint32_t& m) {
-    const uint64_t dx = add2(X, nfx), dy = add2(Y, nfy), dz = add2(Z, nfz);
-    float ea, eb;  // r^2 - hi (sign bit set: hit)
-    upk2(fma2(dz, dz, fma2(dy, dy, fma2(dx, dx, NHI))), ea, eb);
-    m = shl_in(m, __float_as_uint(ea));
-    m = shl_in(m, __float_as_uint(eb));
-  };
-  auto group = [&](uint32_t sa, uint32_t& m) {
-    uint64_t X[G2], Y[G2], Z[G2];
-#pragma unroll
-    for (int q = 0; q < G2; ++q) {  // all loads of the group first (asm keeps program order)
-      X[q] = lds64(sa + step2 * q);
-      Y[q] = lds64(sa + step2 * q + K3_YOFF);
-      Z[q] = lds64(sa + step2 * q + K3_ZOFF);
-    }
-#pragma unroll
-    for (int q = 0; q < G2; ++q) pair_step(X[q], Y[q], Z[q], m);
-  };
-  auto put = [&](uint32_t m) {
-    stsu(mq0 + 128u * (uint32_t)w, m);
-    const int c = __popc(m);
-    nhit += c;
-    qlen += c ? c : 1;
-    ++w;
-  };
-  const int nfull = iters2 >> 4;
-  while (w < nfull) {
-    uint32_t m = 0;
-#pragma unroll
-    for (int g8 = 0; g8 < 32; g8 += 2 * G2) {
-      group(sa, m);
-      sa += step2 * G2;
-    }
-    put(m);
+// Staging offsets of the entries of one chunk [e0, e1) of the neighborhood (<= K3_CAP elements);
+// returns e1 (warp-uniform).  A single entry above K3_CAP (a cell of more than K3_CAP particles)
+// returns e0: the caller flags it (NC_E_OOM on the host) and skips the entry.
+template <typename SM>
+__device__ __forceinline__ int chunk_end(const SM& sm, int e0, int nst, int lane) {
+  const uint32_t base_off = sm.e_off[e0];
+  int e1 = e0;
+  for (int eb = e0; eb < nst; eb += 32) {
+    const int e = eb + lane;
+    const bool fits = e < nst && (sm.e_off[e] + sm.e_cnt[e] - base_off) <= (uint32_t)K3_CAP;
+    const int nfit = __popc(__ballot_sync(0xffffffffu, fits));  // the fitting entries are a prefix
+    e1 = eb + nfit;
+    if (nfit < 32) break;
   }
-  const int rem = iters2 & 15;
-  if (rem) {  // last word: whole groups, then single pair steps, then aligned to bit 31
-    uint32_t m = 0;
-    int q = 0;
-    for (; q + G2 <= rem; q += G2) {
-      group(sa, m);
-      sa += step2 * G2;
-    }
-    for (; q < rem; ++q) {
-      pair_step(lds64(sa), lds64(sa + K3_YOFF), lds64(sa + K3_ZOFF), m);
-      sa += step2;
-    }
-    put(m << (32 - 2 * rem));
+  return e1;
+}
+constexpr double K3_OVERFLOW = 1048576.0;  // tNF marker of a cell above K3_CAP particles (host: NC_E_OOM)
+
+// Stream combine of a lane group: rows are S consecutive lanes, fixed binary tree over s.
+__device__ __forceinline__ void combine_streams(Acc& acc, int S, int s, bool act, int lane) {
+  for (int o = 1; o < S; o <<= 1) {
+    const bool take = act && ((s & (2 * o - 1)) == 0);
+    const int src = lane ^ o;
+    acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
+    acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
+    acc.w0 = shfl_comb(acc.w0, src, take); acc.w1 = shfl_comb(acc.w1, src, take);
+    acc.w2 = shfl_comb(acc.w2, src, take); acc.w3 = shfl_comb(acc.w3, src, take);
+    acc.w4 = shfl_comb(acc.w4, src, take); acc.w5 = shfl_comb(acc.w5, src, take);
+    const uint32_t c2 = __shfl_sync(0xffffffffu, acc.cnt, src);
+    const uint32_t r2c = __shfl_sync(0xffffffffu, acc.nrc, src);
+    const uint64_t h1 = __shfl_sync(0xffffffffu, acc.hs, src);
+    const uint64_t h2 = __shfl_sync(0xffffffffu, acc.hx, src);
+    if (take) { acc.cnt += c2; acc.nrc += r2c; acc.hs += h1; acc.hx ^= h2; }
   }
-  __syncwarp();
-  eval_masks_f32x2<DIGEST>(g, pc, sm, acc, nfar, qlen, nhit, w, sa0, step2, lane, stage0, u64);
 }
 
 // One warp per block; each warp handles K3_CELLS consecutive cells of one
@@ -1089,7 +1184,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         const typename V4<T>::t* __restrict__ qs, const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid,
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
         uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl,
-        int layer0) {
+        int layer0, const PairOut po) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lane = threadIdx.x & 31;
   K3Smem<T>& sm = *reinterpret_cast<K3Smem<T>*>(smraw);
@@ -1108,14 +1203,16 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   pc.qs = qs;
   pc.nh = nh;
   pc.gid = gid;
+  pc.po = po;
+  pc.gi = 0u;
 
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
   uint32_t tFu = 0;  // this lane's fp32-tier interactions (< 2^32 per lane)
   if constexpr (sizeof(T) == 4) {
     // 16-bit queue entries decode without a carry only if the block's shared memory sits in one 64 KB page
     if ((smem_u32(smraw) & 0xffffu) + (uint32_t)sizeof(K3Smem<T>) > 0x10000u) tNF += 1.0;
-    if (lane == 0) {  // permanent far element used to pad the two-wide evaluation (reads particle 0 + far bracket)
-      sm.s64.sx[K3_DUMMY] = sm.s64.sy[K3_DUMMY] = sm.s64.sz[K3_DUMMY] = 1e30f;
+    if (lane == 0) {  // permanent far element used to pad the two-wide close evaluation (far bracket)
+      sm.s64.sc[0][K3_DUMMY] = sm.s64.sc[1][K3_DUMMY] = sm.s64.sc[2][K3_DUMMY] = 1e30f;
       sm.sent[K3_DUMMY] = K3_MAXE - 1;
       sm.e_B[K3_MAXE - 1][0] = 1e150; sm.e_B[K3_MAXE - 1][1] = 1e150; sm.e_B[K3_MAXE - 1][2] = 1e150;
     }
@@ -1157,82 +1254,176 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     if (ni == 0) continue;
     tC += (double)ni * (double)tot - (double)ni;
 
-    for (int ib = 0; ib < ni; ib += 32) {
-      const int nb = min(32, ni - ib);
-      const int S = 32 / nb;               // streams over the j list
-      const int il = lane % nb;
-      const bool act = lane < S * nb;
-      const int s = act ? lane / nb : 0;   // ghost lanes shadow stream 0 (no extra smem addresses)
-      pc.my = ibase + ib + il;
-      if constexpr (sizeof(T) == 4) {
-        double4 ui = u[pc.my];
-        float4 uf = u32[pc.my];
+    if constexpr (sizeof(T) == 4) {
+      // ---------------- NC_F32: tensor-core filter, packed fp32 far tier, fp64 close tier
+      const uint32_t stage0 = smem_u32(&sm.s64.sc[0][0]);
+      const uint32_t hw0 = smem_u32(&sm.hw[0]);
+      const int g8 = lane >> 2, t4 = lane & 3;
+      int staged0 = -1, staged1 = -1;  // entries currently staged (reused by the next i-batch)
+      for (int ib = 0; ib < ni; ib += 16) {
+        const int nb = min(16, ni - ib);
+        constexpr int S = 2;  // far-tier lanes per row (mma_filter's interleaved word layout)
+        const int row = lane / S, s = lane % S;
+        const bool act = row < nb;
+        pc.my = ibase + ib + (act ? row : 0);
+        const double4 ui = u[pc.my];  // fp64 i (close tier); consumed after staging: its latency overlaps
         pc.ux = ui.x; pc.uy = ui.y; pc.uz = ui.z;
-        pc.fx = act ? uf.x : -1e30f;  // ghost lanes never pass the filter
-        pc.fy = uf.y; pc.fz = uf.z;
-        pc.m2x = -2.0f * pc.fx; pc.m2y = -2.0f * pc.fy; pc.m2z = -2.0f * pc.fz;
-        pc.uu = act ? fmaf(pc.fz, pc.fz, fmaf(pc.fy, pc.fy, pc.fx * pc.fx)) : __int_as_float(0x7f800000);
-      } else {
-        typename V4<T>::t qi = qs[pc.my];
-        pc.ux = act ? qi.x : -1e300; pc.uy = qi.y; pc.uz = qi.z;
-      }
-      pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
-      Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+        pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
+        if (DIGEST) pc.gi = gid[pc.my];
+        // MMA A fragments (rows g8, g8 + 8: component t4 of (-2 u, 1)), C = |u|^2 - h per row, and the
+        // far lanes' fp32 i: from the staged center cell (set with the first chunk that holds it)
+        uint32_t a0 = 0u, a1 = 0u;
+        float c[4];
+        bool have_a = false;
+        Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
 
-      int e0 = 0;
-      while (e0 < nst) {
-        const uint32_t base_off = sm.e_off[e0];
-        int e1 = e0;
-        for (int eb = e0; eb < nst; eb += 32) {
-          int e = eb + lane;
-          bool fits = e < nst && (sm.e_off[e] + sm.e_cnt[e] - base_off) <= (uint32_t)K3_CAP;
-          int nfit = __popc(__ballot_sync(0xffffffffu, fits));  // the fitting entries are a prefix
-          e1 = eb + nfit;
-          if (nfit < 32) break;
-        }
-        if (e1 == e0) e1 = e0 + 1;  // unreachable: a cell holds fewer than K3_CAP particles
-        const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
-        // stage the chunk: staged element t <- particle e_start[e] + (t - e_off[e]) of entry e, shifted
-        // by the entry's image bracket B_e in fp64.  Flattened over t (lanes read consecutive particles of
-        // each neighbor cell: coalesced), two elements per lane in flight.
-        if constexpr (sizeof(T) == 4) {
-          // (1) entry id of every staged element, fp32 brackets; (2) flattened coalesced copy
-          for (int eb = e0; eb < e1; eb += 32) {
-            const int e = eb + lane;
-            if (e < e1) {
-              const uint32_t dst = sm.e_off[e] - base_off, cnt = sm.e_cnt[e];
-              for (uint32_t k = 0; k < cnt; ++k) sm.sent[dst + k] = (uint8_t)e;
-              sm.s64.Bf[e][0] = (float)sm.e_B[e][0];
-              sm.s64.Bf[e][1] = (float)sm.e_B[e][1];
-              sm.s64.Bf[e][2] = (float)sm.e_B[e][2];
-            }
+        int e0 = 0;
+        while (e0 < nst) {
+          const uint32_t base_off = sm.e_off[e0];
+          const int e1 = chunk_end(sm, e0, nst, lane);
+          if (e1 == e0) {  // one cell above K3_CAP particles: cannot stage it (host reports NC_E_OOM)
+            tNF += (lane == 0 && ib == 0) ? K3_OVERFLOW : 0.0;
+            e0 += 1;
+            continue;
           }
-          __syncwarp();
-          // K3_STGR elements per lane in flight: all index lookups and loads first, then the stores
-          for (uint32_t t0 = 0; t0 < ctot; t0 += 32 * K3_STGR) {
-            uint32_t tt[K3_STGR], jj[K3_STGR];
-            int ee[K3_STGR];
-            float4 pp[K3_STGR];
-#pragma unroll
-            for (int r = 0; r < K3_STGR; ++r) {
-              tt[r] = t0 + 32u * r + lane;
-              const bool v = tt[r] < ctot;
-              ee[r] = v ? sm.sent[tt[r]] : e0;
-              jj[r] = sm.e_start[ee[r]] + tt[r] - (sm.e_off[ee[r]] - base_off);
-              pp[r] = v ? u32[jj[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int r = 0; r < K3_STGR; ++r) {
-              if (tt[r] < ctot) {
-                const float x = pp[r].x + sm.s64.Bf[ee[r]][0], y = pp[r].y + sm.s64.Bf[ee[r]][1],
-                            z = pp[r].z + sm.s64.Bf[ee[r]][2];
-                sm.s64.sx[tt[r]] = x;
-                sm.s64.sy[tt[r]] = y;
-                sm.s64.sz[tt[r]] = z;
+          const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
+          const int W = (int)((ctot + 127) / 128);  // hit words: 16 column blocks of 8 elements each
+          // (a vote: the compiler then knows the branch is warp-uniform and keeps the shuffles of the
+          // rest of the kernel free of divergence handling)
+          if (__any_sync(0xffffffffu, e0 != staged0 || e1 != staged1)) {
+            // stage: element t <- particle e_start[e] + (t - e_off[e]) of entry e, plus the entry's image
+            // bracket relative to the center cell's centre (coalesced over t); |v|^2 for the MMA filter
+            for (int eb = e0; eb < e1; eb += 32) {
+              const int e = eb + lane;
+              if (e < e1) {
+                const uint32_t dst = sm.e_off[e] - base_off, cnt = sm.e_cnt[e];
+                for (uint32_t k = 0; k < cnt; ++k) sm.sent[dst + k] = (uint8_t)e;
+                sm.Bf[e][0] = (float)(sm.e_B[e][0] - g.cc[0]);
+                sm.Bf[e][1] = (float)(sm.e_B[e][1] - g.cc[1]);
+                sm.Bf[e][2] = (float)(sm.e_B[e][2] - g.cc[2]);
               }
             }
+            __syncwarp();
+            for (uint32_t t0 = 0; t0 < ctot; t0 += 32 * K3_STGR) {
+              uint32_t tt[K3_STGR], jj[K3_STGR];
+              int ee[K3_STGR];
+              float4 pp[K3_STGR];
+#pragma unroll
+              for (int r = 0; r < K3_STGR; ++r) {
+                tt[r] = t0 + 32u * r + lane;
+                const bool v = tt[r] < ctot;
+                ee[r] = v ? sm.sent[tt[r]] : e0;
+                jj[r] = sm.e_start[ee[r]] + tt[r] - (sm.e_off[ee[r]] - base_off);
+                pp[r] = v ? u32[jj[r]] : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int r = 0; r < K3_STGR; ++r) {
+                if (tt[r] < ctot) {
+                  const float x = pp[r].x + sm.Bf[ee[r]][0], y = pp[r].y + sm.Bf[ee[r]][1],
+                              z = pp[r].z + sm.Bf[ee[r]][2];
+                  sm.s64.sc[0][tt[r]] = x;
+                  sm.s64.sc[1][tt[r]] = y;
+                  sm.s64.sc[2][tt[r]] = z;
+                  sm.s64.sc[3][tt[r]] = tf32_rna(fmaf(z, z, fmaf(y, y, x * x)));
+                }
+              }
+            }
+            for (int t = (int)ctot + lane; t < 128 * W; t += 32) {  // pad to whole words: never a hit
+              sm.s64.sc[0][t] = sm.s64.sc[1][t] = sm.s64.sc[2][t] = 0.0f;
+              sm.s64.sc[3][t] = 1e30f;
+            }
+            staged0 = e0;
+            staged1 = e1;
           }
-        } else {
+          __syncwarp();
+          if (!have_a) {
+            const int ec = sm.e_center;
+            // a vote: warp-uniform for the compiler (the shuffles after it need no divergence handling)
+            const bool in_chunk = __any_sync(0xffffffffu, ec >= e0 && ec < e1);
+            const uint32_t ci0 = in_chunk ? sm.e_off[ec] - base_off + (uint32_t)ib : 0u;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int r = g8 + 8 * q;
+              uint32_t av = 0u;
+              float cr = 1e30f;  // ghost rows: never a hit
+              if (r < nb) {
+                float x, y, z;
+                if (in_chunk) {  // staged = u32 + (0 - cc) rounded: the same value as below
+                  x = sm.s64.sc[0][ci0 + r]; y = sm.s64.sc[1][ci0 + r]; z = sm.s64.sc[2][ci0 + r];
+                } else {
+                  const float4 v = u32[ibase + ib + r];
+                  x = v.x - g.f_cc[0]; y = v.y - g.f_cc[1]; z = v.z - g.f_cc[2];
+                }
+                const float comp = t4 == 0 ? x : (t4 == 1 ? y : z);
+                av = __float_as_uint(t4 < 3 ? -2.0f * comp : 1.0f);
+                cr = fmaf(z, z, fmaf(y, y, x * x)) - g.f_hmma;
+              }
+              if (q == 0) a0 = av; else a1 = av;
+              c[2 * q] = cr;
+              c[2 * q + 1] = cr;
+            }
+            if (in_chunk) {
+              const uint32_t ti = ci0 + (uint32_t)(act ? row : 0);
+              pc.fx = sm.s64.sc[0][ti]; pc.fy = sm.s64.sc[1][ti]; pc.fz = sm.s64.sc[2][ti];
+            } else {
+              pc.fx = (float)(ui.x - g.cc[0]); pc.fy = (float)(ui.y - g.cc[1]); pc.fz = (float)(ui.z - g.cc[2]);
+            }
+            have_a = true;
+          }
+          mma_filter(stage0, hw0, W, a0, a1, c, lane);
+          __syncwarp();
+          pc.base_off = base_off;
+          const int nw = 2 * W;  // words per far lane
+          eval_hits<DIGEST>(g, pc, sm, acc, tFu, hw0 + 4u * (uint32_t)((row * S + s) * nw), nw,
+                            stage0 + 8u * (uint32_t)s, lane, stage0, u);
+          __syncwarp();
+          e0 = e1;
+        }
+        combine_streams(acc, S, s, act, lane);
+        const bool owner = act && s == 0;
+        // fold the factors of R11/R12: U_i = 2 eps sum s6(s6-1) - cnt u_shift / 2; W_i = sum fr d d / 2
+        const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
+        if (owner) {  // lab-frame force F = Q F_rot; .w = the particle's interaction count (parity)
+          const double Fx = g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz;
+          const double Fy = g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz;
+          const double Fz = g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz;
+          Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, idx_to_w(acc.cnt, T()));
+          if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
+          tU += Ui;
+          tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
+          tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
+          tI += (double)acc.cnt;
+          tR += (double)acc.nrc;
+        }
+        const double fchk = owner ? acc.fx + acc.fy + acc.fz + Ui : 0.0;
+        tNF += isfinite(fchk) ? 0.0 : 1.0;
+      }
+    } else {
+      // ---------------- NC_F64: canonical fp64 filter on every candidate, error-free d
+      for (int ib = 0; ib < ni; ib += 32) {
+        const int nb = min(32, ni - ib);
+        const int S = 32 / nb;               // streams over the j list
+        const int il = lane % nb;
+        const bool act = lane < S * nb;
+        const int s = act ? lane / nb : 0;   // ghost lanes shadow stream 0 (no extra smem addresses)
+        pc.my = ibase + ib + il;
+        {
+          typename V4<T>::t qi = qs[pc.my];
+          pc.ux = act ? qi.x : -1e300; pc.uy = qi.y; pc.uz = qi.z;
+        }
+        pc.nh_i = (g.variant == 1) ? nh[pc.my] : 0u;
+        if (DIGEST) pc.gi = gid[pc.my];
+        Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+        int e0 = 0;
+        while (e0 < nst) {
+          const uint32_t base_off = sm.e_off[e0];
+          const int e1 = chunk_end(sm, e0, nst, lane);
+          if (e1 == e0) {
+            tNF += (lane == 0) ? K3_OVERFLOW : 0.0;
+            e0 += 1;
+            continue;
+          }
+          const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
           for (int eb = e0; eb < e1; eb += 32) {
             int e = eb + lane;
             uint32_t cnt = 0, st = 0, dst = 0;
@@ -1247,71 +1438,51 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
               }
             }
           }
-        }
-        // far sentinels after the chunk: S (fp64 streams), 2S (fp32 pair steps)
-        for (int t = lane; t < (sizeof(T) == 8 ? S : 2 * S); t += 32) {
-          if constexpr (sizeof(T) == 8) {
+          for (int t = lane; t < S; t += 32) {  // far sentinels after the chunk (one per stream)
             sm.stage[ctot + t] = far4<T>();
             sm.s64.nh[ctot + t] = 0u;
-          } else {
-            sm.s64.sx[ctot + t] = sm.s64.sy[ctot + t] = sm.s64.sz[ctot + t] = 1e30f;
+            sm.sent[ctot + t] = 0;
           }
-          sm.sent[ctot + t] = 0;
-        }
-        __syncwarp();
-        const int iters = (int)((ctot + S - 1) / S);
-        pc.base_off = base_off;
-        if constexpr (sizeof(T) == 4) {
-          filter_chunk_f32<DIGEST>(g, pc, sm, acc, tFu, s, S, iters, lane, u);
-        } else {
+          __syncwarp();
+          const int iters = (int)((ctot + S - 1) / S);
+          pc.base_off = base_off;
           filter_chunk<T, DIGEST>(g, pc, sm, acc, s, S, iters, lane);
+          __syncwarp();
+          e0 = e1;
         }
-        __syncwarp();
-        e0 = e1;
-      }
-
-      // combine the S streams of each i: fixed binary tree over s (log2 S shuffle steps)
-      for (int o = 1; o < S; o <<= 1) {
-        const int src_s = s + o;
-        bool take = act && ((s & (2 * o - 1)) == 0) && (src_s < S);
-        const int src = (lane + o * nb) & 31;
-        acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
-        acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
-        acc.w0 = shfl_comb(acc.w0, src, take); acc.w1 = shfl_comb(acc.w1, src, take);
-        acc.w2 = shfl_comb(acc.w2, src, take); acc.w3 = shfl_comb(acc.w3, src, take);
-        acc.w4 = shfl_comb(acc.w4, src, take); acc.w5 = shfl_comb(acc.w5, src, take);
-        uint32_t c2 = __shfl_sync(0xffffffffu, acc.cnt, src);
-        uint32_t r2c = __shfl_sync(0xffffffffu, acc.nrc, src);
-        if (take) { acc.cnt += c2; acc.nrc += r2c; }
-        if (DIGEST) {
-          uint64_t h1 = __shfl_sync(0xffffffffu, acc.hs, src);
-          uint64_t h2 = __shfl_sync(0xffffffffu, acc.hx, src);
-          if (take) { acc.hs += h1; acc.hx ^= h2; }
+        // combine the S streams of each i: fixed binary tree over s (log2 S shuffle steps)
+        for (int o = 1; o < S; o <<= 1) {
+          const int src_s = s + o;
+          bool take = act && ((s & (2 * o - 1)) == 0) && (src_s < S);
+          const int src = (lane + o * nb) & 31;
+          acc.fx = shfl_comb(acc.fx, src, take); acc.fy = shfl_comb(acc.fy, src, take);
+          acc.fz = shfl_comb(acc.fz, src, take); acc.u = shfl_comb(acc.u, src, take);
+          acc.w0 = shfl_comb(acc.w0, src, take); acc.w1 = shfl_comb(acc.w1, src, take);
+          acc.w2 = shfl_comb(acc.w2, src, take); acc.w3 = shfl_comb(acc.w3, src, take);
+          acc.w4 = shfl_comb(acc.w4, src, take); acc.w5 = shfl_comb(acc.w5, src, take);
+          uint32_t c2 = __shfl_sync(0xffffffffu, acc.cnt, src);
+          uint32_t r2c = __shfl_sync(0xffffffffu, acc.nrc, src);
+          if (take) { acc.cnt += c2; acc.nrc += r2c; }
+          if (DIGEST) {
+            uint64_t h1 = __shfl_sync(0xffffffffu, acc.hs, src);
+            uint64_t h2 = __shfl_sync(0xffffffffu, acc.hx, src);
+            if (take) { acc.hs += h1; acc.hx ^= h2; }
+          }
         }
-      }
-      const bool owner = (lane < nb);
-      // fold the factors of R11/R12: U_i = 2 eps sum s6(s6-1) - cnt u_shift / 2; W_i = sum fr d d / 2
-      const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
-      if (owner) {
-        double Fx = acc.fx, Fy = acc.fy, Fz = acc.fz;
-        if constexpr (sizeof(T) == 4) {  // lab-frame force F = Q F_rot
-          Fx = g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz;
-          Fy = g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz;
-          Fz = g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz;
+        const bool owner = (lane < nb);
+        const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
+        if (owner) {
+          Fout[pc.my] = mk4((T)acc.fx, (T)acc.fy, (T)acc.fz, idx_to_w(acc.cnt, T()));
+          if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
+          tU += Ui;
+          tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
+          tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
+          tI += (double)acc.cnt;
+          tR += (double)acc.nrc;
         }
-        Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, (T)0);
-        if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
+        const double fchk = owner ? acc.fx + acc.fy + acc.fz + Ui : 0.0;
+        tNF += isfinite(fchk) ? 0.0 : 1.0;
       }
-      // per-lane partials across the warp's cells; one fixed-order warp reduction at the end
-      double fchk = owner ? acc.fx + acc.fy + acc.fz + Ui : 0.0;
-      if (owner) {
-        tU += Ui;
-        tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
-        tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
-        tI += (double)acc.cnt;
-        tR += (double)acc.nrc;
-      }
-      tNF += isfinite(fchk) ? 0.0 : 1.0;
     }
   }
   tU = warp_sum_d(tU);
@@ -1319,7 +1490,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
   tI = warp_sum_d(tI);
   tR = warp_sum_d(tR);
-  // fp32-tier interactions only in the counting instantiation (nc_profile mode 2): the counter's
+  // fp32-tier interactions only in the counting instantiation (nc_profile mode 3): the counter's
   // register costs the hot kernel ~1%
   const double tF = COUNT ? warp_sum_d((double)tFu) : 0.0;
   tNF = warp_sum_d(tNF);

@@ -91,6 +91,8 @@ struct nc_ctx {
   double occ_hint = -1.0;         // slab path: particles per cell of the own layers (auto kernel choice)
   double host_tot[NPART];
   bool tot_valid = false;
+  int dbg_drop = 0;               // nc_debug negative control
+  PairOut po{nullptr, nullptr, 0};  // nc_get_pairs: pair-list output of the next digest evaluation
 
   // live kernel timing (nc_profile)
   bool prof = false;
@@ -242,6 +244,33 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   g.f_sig2 = (float)g.sig2;
   g.f_c48 = (float)(48.0 * g.eps);
   g.f_m24 = (float)(-24.0 * g.eps);
+  // fp32 staging frame: centred on the cell (DS: u = R (lambda - a/c) spans R [0, 1/c); DO: [0, w)),
+  // R_i = the largest |u - cc| over the cell (half its longest diagonal)
+  double Ri = 0.0;
+  if (g.variant == 0) {
+    const double h0 = 0.5 * g.cinv[0], h1 = 0.5 * g.cinv[1], h2 = 0.5 * g.cinv[2];
+    g.cc[0] = g.R[0] * h0 + g.R[1] * h1 + g.R[2] * h2;
+    g.cc[1] = g.R[4] * h1 + g.R[5] * h2;
+    g.cc[2] = g.R[8] * h2;
+    for (int sx = -1; sx <= 1; sx += 2)
+      for (int sy = -1; sy <= 1; sy += 2) {
+        const double x = g.R[0] * sx * h0 + g.R[1] * sy * h1 + g.R[2] * h2, y = g.R[4] * sy * h1 + g.R[5] * h2,
+                     z = g.R[8] * h2;
+        Ri = std::max(Ri, std::sqrt(x * x + y * y + z * z));
+      }
+  } else {
+    for (int k = 0; k < 3; ++k) g.cc[k] = 0.5 * g.w[k];
+    Ri = std::sqrt(g.cc[0] * g.cc[0] + g.cc[1] * g.cc[1] + g.cc[2] * g.cc[2]);
+  }
+  for (int k = 0; k < 3; ++k) g.f_cc[k] = (float)g.cc[k];
+  Ri *= 1.0 + 1e-6;  // clamped keys (R14) may leave a particle ~1 ulp outside its cell
+  // tensor-core filter bound (kernels.cuh, mma_filter): tf32 operands (x, y, z truncated to 10
+  // mantissa bits, |v|^2 rounded) give |r~^2 - r^2| <= 2^-10 4.01 |u_i| |v_j| + 2^-11 |v_j|^2, with
+  // |u_i| <= R_i and |v_j| <= R_i + r_c inside the cutoff; plus 1e-4 r_c^2 for the fp32 accumulation
+  // and the two-part row constant
+  const double vmax = Ri + ctx->cfg.rc;
+  g.f_hmma = (float)(g.rc2 + std::ldexp(4.01 * Ri * vmax, -10) + std::ldexp(vmax * vmax, -11) + 1e-4 * g.rc2);
+  g.dbg_drop = ctx->dbg_drop;
   ctx->g = g;
   ctx->have_box = true;
   return NC_OK;
@@ -321,6 +350,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
+  const PairOut po = DIGEST ? ctx->po : PairOut{nullptr, nullptr, 0};
   prof_begin(ctx);
   double* bp = nullptr;  // set once bpl is final (below)
   if constexpr (sizeof(T) == 4) {
@@ -336,26 +366,26 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       if (ctx->seg_nw == 4)
         k_pairs_seg<DIGEST, 4><<<nblocks, SgCfg<4>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
                                                                    ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
-                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0);
+                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
       else
         k_pairs_seg<DIGEST, 2><<<nblocks, SgCfg<2>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
                                                                    ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
-                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0);
+                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       if (!DIGEST && ctx->count_tiers)
         k_pairs<T, DIGEST, true><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
-                                                           ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+                                                           ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
       else
         k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
-                                                     ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+                                                     ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
     }
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
     bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
     k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp, ctx->dcnt,
-                                                 ctx->dhs, ctx->dhx, g, cpb, bpl, layer0);
+                                                 ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
   }
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
@@ -403,6 +433,10 @@ void totals_to_UW(const nc_ctx* ctx, double* U, double* W) {
 nc_status check_finite(nc_ctx* ctx) {
   nc_status st = fetch_totals(ctx);
   if (st) return st;
+  if (ctx->host_tot[NPART - 1] >= K3_OVERFLOW)
+    return fail(ctx, NC_E_OOM, "a neighborhood holds more particles than the pair kernel can stage (cell kernel: " +
+                                   std::to_string(K3_CAP) + " per cell; sparse-cell kernel: one neighborhood per "
+                                   "segment union): too dense for this cutoff / kernel");
   bool ok = ctx->host_tot[NPART - 1] == 0.0;
   for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
   if (!ok) return fail(ctx, NC_E_NONFINITE, "non-finite force, energy or virial");
@@ -661,8 +695,7 @@ template <typename T>
 nc_status digest_t(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_t* hxor) {
   const void* qs = ctx->last_resident ? ctx->st_q[ctx->cur] : ctx->sq;
   const uint32_t* gid = ctx->last_resident ? ctx->st_gid[ctx->cur] : ctx->sgid;
-  void* F = ctx->last_resident ? ctx->sF : ctx->sF;
-  nc_status st = launch_pairs<T, true>(ctx, (const typename V4<T>::t*)qs, gid, (typename V4<T>::t*)F);
+  nc_status st = launch_pairs<T, true>(ctx, (const typename V4<T>::t*)qs, gid, (typename V4<T>::t*)ctx->sF);
   if (st) return st;
   int64_t n = ctx->n_last;
   std::vector<uint32_t> c(n), gg(n);
@@ -680,6 +713,44 @@ nc_status digest_t(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_t* hxor) {
   return NC_OK;
 }
 
+// Full pair list of the last built cells: one digest evaluation with the pair output enabled, then
+// a host sort by (gid_i, gid_j, n1, n2, n3).
+template <typename T>
+nc_status pairs_t(nc_ctx* ctx, int64_t cap, int32_t* ijn, int64_t* npairs) {
+  int32_t* dev = nullptr;
+  unsigned long long* dn = nullptr;
+  const int64_t dcap = std::max<int64_t>(cap, 1);
+  CK(cudaMalloc(&dev, sizeof(int32_t) * 5 * (size_t)dcap));
+  CK(cudaMalloc(&dn, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(dn, 0, sizeof(unsigned long long), ctx->stream));
+  ctx->po = PairOut{dev, dn, (long long)cap};
+  nc_status st = digest_t<T>(ctx, nullptr, nullptr, nullptr);
+  ctx->po = PairOut{nullptr, nullptr, 0};
+  unsigned long long total = 0;
+  std::vector<int32_t> h;
+  if (st == NC_OK) {
+    cudaMemcpy(&total, dn, sizeof total, cudaMemcpyDeviceToHost);
+    const int64_t m = std::min<int64_t>((int64_t)total, cap);
+    h.resize(5 * (size_t)m);
+    if (m > 0) cudaMemcpy(h.data(), dev, sizeof(int32_t) * 5 * (size_t)m, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(dev);
+  cudaFree(dn);
+  if (st) return st;
+  CK(cudaGetLastError());
+  *npairs = (int64_t)total;
+  if ((int64_t)total > cap) return fail(ctx, NC_E_OOM, "pair list longer than cap (npairs holds the count)");
+  std::vector<int64_t> order(total);
+  for (int64_t k = 0; k < (int64_t)total; ++k) order[k] = k;
+  std::sort(order.begin(), order.end(), [&](int64_t x, int64_t y) {
+    for (int f = 0; f < 5; ++f)
+      if (h[5 * x + f] != h[5 * y + f]) return h[5 * x + f] < h[5 * y + f];
+    return false;
+  });
+  for (int64_t k = 0; k < (int64_t)total; ++k)
+    for (int f = 0; f < 5; ++f) ijn[5 * k + f] = h[5 * order[k] + f];
+  return NC_OK;
+}
 
 // ---------------------------------------------------------------- slab helpers
 nc_status sllod_params(nc_ctx* ctx, double dt, SllodParams& sp) {
@@ -1005,7 +1076,7 @@ void nc_destroy(nc_ctx* ctx) {
   void* ps[] = {ctx->st_q[0], ctx->st_q[1], ctx->st_p[0], ctx->st_p[1], ctx->st_gid[0], ctx->st_gid[1], ctx->st_F,
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
-                ctx->part_tot, ctx->part_acc, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
+                ctx->part_tot, ctx->part_acc, ctx->rcount, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
                 ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot};
   for (void* p : ps)
     if (p) cudaFree(p);
@@ -1128,9 +1199,13 @@ nc_status nc_set_state(nc_ctx* ctx, const void* q, const void* p, const int64_t*
   if (!ctx || (!q && n > 0)) return fail(ctx, NC_E_ARG, "null argument");
   if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
   if (n < 0 || n > ctx->cap) return fail(ctx, NC_E_OOM, "n exceeds capacity");
-  if (gid)
-    for (int64_t i = 0; i < n; ++i)
-      if (gid[i] < 0 || gid[i] > 0xFFFFFFFFLL) return fail(ctx, NC_E_ARG, "gid out of range");
+  if (gid) {  // must be a permutation of 0..n-1: outputs are indexed by gid (nc_get_state, digests)
+    std::vector<uint8_t> seen((size_t)n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (gid[i] < 0 || gid[i] >= n) return fail(ctx, NC_E_ARG, "gid must be a permutation of 0..n-1 (out of range)");
+      if (seen[(size_t)gid[i]]++) return fail(ctx, NC_E_ARG, "gid must be a permutation of 0..n-1 (duplicate)");
+    }
+  }
   ctx->kick_pending = false;  // the new state replaces the momenta the deferred kick belonged to
   return ctx->cfg.prec == NC_F32 ? set_state_t<float>(ctx, q, p, gid, n) : set_state_t<double>(ctx, q, p, gid, n);
 }
@@ -1214,6 +1289,53 @@ nc_status nc_get_pair_digest(nc_ctx* ctx, uint32_t* cnt, uint64_t* hsum, uint64_
   if (!ctx->have_cells) return fail(ctx, NC_E_STATE, "no cells built");
   nc_status st = ctx->cfg.prec == NC_F32 ? digest_t<float>(ctx, cnt, hsum, hxor) : digest_t<double>(ctx, cnt, hsum, hxor);
   return st;
+}
+
+nc_status nc_get_pairs(nc_ctx* ctx, int64_t cap, int32_t* i_j_n, int64_t* npairs) {
+  if (!ctx || !npairs || (cap > 0 && !i_j_n) || cap < 0) return fail(ctx, NC_E_ARG, "null argument or cap < 0");
+  if (!ctx->have_cells) return fail(ctx, NC_E_STATE, "no cells built");
+  return ctx->cfg.prec == NC_F32 ? pairs_t<float>(ctx, cap, i_j_n, npairs) : pairs_t<double>(ctx, cap, i_j_n, npairs);
+}
+
+nc_status nc_get_cell_gids(nc_ctx* ctx, int64_t* gid_sorted) {
+  if (!ctx || !gid_sorted) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_cells) return fail(ctx, NC_E_STATE, "no cells built");
+  const int64_t n = ctx->n_last;
+  const uint32_t* gid = ctx->last_resident ? ctx->st_gid[ctx->cur] : ctx->sgid;
+  std::vector<uint32_t> g(n);
+  CK(cudaMemcpyAsync(g.data(), gid, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t k = 0; k < n; ++k) gid_sorted[k] = g[k];
+  return NC_OK;
+}
+
+nc_status nc_get_pair_counts(nc_ctx* ctx, uint32_t* cnt) {
+  if (!ctx || !cnt) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_eval) return fail(ctx, NC_E_STATE, "no evaluation yet");
+  const int64_t n = ctx->n_last;
+  const bool f32 = ctx->cfg.prec == NC_F32;
+  const void* F = ctx->last_resident ? ctx->st_F : ctx->sF;
+  const uint32_t* gid = ctx->last_resident ? ctx->st_gid[ctx->cur] : ctx->sgid;
+  std::vector<unsigned char> f(v4size(ctx) * n);
+  std::vector<uint32_t> g(n);
+  CK(cudaMemcpyAsync(f.data(), F, f.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(g.data(), gid, 4 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int64_t k = 0; k < n; ++k) {
+    uint32_t c;
+    if (f32) std::memcpy(&c, f.data() + 16 * k + 12, 4);
+    else { double w; std::memcpy(&w, f.data() + 32 * k + 24, 8); c = (uint32_t)w; }
+    cnt[g[k]] = c;
+  }
+  return NC_OK;
+}
+
+nc_status nc_debug(nc_ctx* ctx, int what, int value) {
+  if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
+  if (what != NC_DBG_DROP_ENTRIES || value < 0 || value > 1) return fail(ctx, NC_E_ARG, "bad debug option");
+  ctx->dbg_drop = value;
+  ctx->g.dbg_drop = value;
+  return NC_OK;
 }
 
 nc_status nc_get_stats(nc_ctx* ctx, nc_stats* out) {
@@ -1438,6 +1560,10 @@ nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* 
   }
   ctx->tot_valid = true;
   ctx->have_eval = true;
+  if (ctx->host_tot[NPART - 1] >= K3_OVERFLOW)
+    return fail(ctx, NC_E_OOM, "a neighborhood holds more particles than the pair kernel can stage (cell kernel: " +
+                                   std::to_string(K3_CAP) + " per cell; sparse-cell kernel: one neighborhood per "
+                                   "segment union): too dense for this cutoff / kernel");
   bool ok = ctx->host_tot[NPART - 1] == 0.0;
   for (int k = 0; k < 7; ++k) ok = ok && std::isfinite(ctx->host_tot[k]);
   totals_to_UW(ctx, U, W);

@@ -30,7 +30,8 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_slab_unpack",
            "nc_slab_halo", "nc_slab_forces", "nc_slab_forces_begin", "nc_slab_forces_end", "nc_slab_kick",
            "nc_slab_reduce", "nc_set_pair_kernel",
-           "nc_pair_kernel_used"]
+           "nc_pair_kernel_used", "nc_get_pairs", "nc_get_cell_gids", "nc_get_pair_counts", "nc_debug"]
+NC_DBG_DROP_ENTRIES = 1
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
 KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
@@ -99,6 +100,10 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_get_cells.argtypes = [vp, vp, vp, vp, vp]
         L.nc_get_pair_digest.argtypes = [vp, vp, vp, vp]
         L.nc_get_stats.argtypes = [vp, ctypes.POINTER(nc_stats)]
+        L.nc_get_pairs.argtypes = [vp, i64, vp, vp]
+        L.nc_get_cell_gids.argtypes = [vp, vp]
+        L.nc_get_pair_counts.argtypes = [vp, vp]
+        L.nc_debug.argtypes = [vp, i32, i32]
         L.nc_get_stencil_histogram.argtypes = [vp, vp]
         L.nc_profile.argtypes = [vp, i32]
         L.nc_profile_read.argtypes = [vp, vp, vp]
@@ -239,6 +244,30 @@ def nc_get_pair_digest(ctx, n: int):
     hx = np.zeros(n, dtype=np.uint64)
     _check(ctx, load().nc_get_pair_digest(ctx, _ptr(cnt), _ptr(hs), _ptr(hx)))
     return cnt, hs, hx
+
+
+def nc_get_pairs(ctx, cap: int = 1 << 20) -> np.ndarray:
+    """Sorted (npairs, 5) int32 array: gid_i, gid_j, n1, n2, n3 of every ordered pair."""
+    n = ctypes.c_int64()
+    out = np.zeros((max(int(cap), 1), 5), dtype=np.int32)
+    _check(ctx, load().nc_get_pairs(ctx, int(cap), _ptr(out), ctypes.byref(n)))
+    return out[: n.value].copy()
+
+
+def nc_get_cell_gids(ctx, n: int) -> np.ndarray:
+    g = np.zeros(n, dtype=np.int64)
+    _check(ctx, load().nc_get_cell_gids(ctx, _ptr(g)))
+    return g
+
+
+def nc_get_pair_counts(ctx, n: int) -> np.ndarray:
+    c = np.zeros(n, dtype=np.uint32)
+    _check(ctx, load().nc_get_pair_counts(ctx, _ptr(c)))
+    return c
+
+
+def nc_debug(ctx, what: int, value: int) -> None:
+    _check(ctx, load().nc_debug(ctx, int(what), int(value)))
 
 
 def nc_get_stats(ctx) -> dict:
@@ -414,6 +443,19 @@ class CellList:
         except Exception:
             pass
 
+    def _arr3(self, x, name):
+        """Refuse arrays whose dtype or shape does not match the context (the C-ABI reads
+        n x 3 elements of the context precision through a raw pointer)."""
+        if x is None:
+            return x
+        dt = getattr(x, "dtype", None)
+        ok = dt in (self.dtype, self.np_dtype) or (isinstance(x, np.ndarray) and x.dtype == self.np_dtype)
+        if not ok:
+            raise TypeError(f"{name}: dtype {dt} does not match the context precision {self.prec}")
+        if len(x.shape) != 2 or x.shape[1] != 3:
+            raise ValueError(f"{name}: shape {tuple(x.shape)} is not (n, 3)")
+        return x
+
     def set_box(self, L):
         nc_set_box(self.ctx, L)
 
@@ -422,18 +464,25 @@ class CellList:
         nc_set_flow(self.ctx, A, r, t)
 
     def build_cells(self, q):
+        self._arr3(q, "q")
         nc_build_cells(self.ctx, q, q.shape[0])
 
     def compute_forces(self, q, F=None):
         import torch
 
+        self._arr3(q, "q")
         if F is None:
             F = torch.empty_like(q) if hasattr(q, "data_ptr") and not isinstance(q, np.ndarray) else np.empty_like(q)
+        self._arr3(F, "F")
+        if F.shape[0] != q.shape[0]:
+            raise ValueError("F must have the shape of q")
         U, W = nc_compute_forces(self.ctx, q, q.shape[0], F)
         return F, U, W
 
     def compute_forces_async(self, q, F):
         """Enqueue one evaluation on host buffers (pinned: copies overlap neighbouring calls)."""
+        self._arr3(q, "q")
+        self._arr3(F, "F")
         nc_compute_forces_async(self.ctx, q, q.shape[0], F)
 
     def compute_sync(self):
@@ -441,6 +490,10 @@ class CellList:
         return nc_compute_sync(self.ctx)
 
     def set_state(self, q, p=None, gid=None):
+        self._arr3(q, "q")
+        self._arr3(p, "p")
+        if p is not None and p.shape[0] != q.shape[0]:
+            raise ValueError("p must have the shape of q")
         nc_set_state(self.ctx, q, p, gid, q.shape[0])
 
     def step(self, dt, nsteps=1, want_uw=True):
@@ -454,6 +507,18 @@ class CellList:
 
     def digest(self, n):
         return nc_get_pair_digest(self.ctx, n)
+
+    def pairs(self, cap=1 << 20):
+        return nc_get_pairs(self.ctx, cap)
+
+    def cell_gids(self, n):
+        return nc_get_cell_gids(self.ctx, n)
+
+    def pair_counts(self, n):
+        return nc_get_pair_counts(self.ctx, n)
+
+    def debug_drop_entries(self, on=True):
+        nc_debug(self.ctx, NC_DBG_DROP_ENTRIES, 1 if on else 0)
 
     def stats(self):
         return nc_get_stats(self.ctx)

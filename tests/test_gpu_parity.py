@@ -28,14 +28,16 @@ def gpu_eval(w, q, variant, prec, digest=True, kernel="auto"):
     qt = torch.from_numpy(np.ascontiguousarray(q)).cuda()
     F, U, W = cl.compute_forces(qt)
     torch.cuda.synchronize()
+    counts = cl.pair_counts(len(q))  # per-particle counts from the TIMED kernel (before any digest run)
     used = cl.pair_kernel_used()
     if kernel != "auto":
         assert used == kernel, (used, kernel)
     st = cl.stats()
     cell_of, cs, dims, wq = cl.cells(len(q), st["ncells"])
+    gids = cl.cell_gids(len(q))
     dig = cl.digest(len(q)) if digest else None
     out = dict(F=F.double().cpu().numpy(), U=U, W=W, stats=st, cell_of=cell_of, cs=cs, dims=dims, wq=wq, dig=dig,
-               hist=cl.stencil_histogram(), launches=cl.launches(), kernel=used)
+               hist=cl.stencil_histogram(), launches=cl.launches(), kernel=used, counts=counts, gids=gids)
     cl.close()
     return out
 
@@ -49,8 +51,10 @@ def check_against_oracle(w, q, variant, prec, idx=None, kernel="auto"):
     cell, nh, dims = oracle.cell_keys(VAR[variant], qo, w.L, w.rc)
     assert list(g["dims"]) == list(dims)
     assert np.array_equal(g["cell_of"], cell)
-    cs, _ = oracle.cell_sort(cell, int(np.prod(dims.astype(np.int64))))
+    cs, order = oracle.cell_sort(cell, int(np.prod(dims.astype(np.int64))))
     assert np.array_equal(g["cs"], cs)
+    # cell contents: the gid sequence of the counting sort, (cell, gid) order (R27), bit-exact
+    assert np.array_equal(g["gids"], order)
     # stencil histogram: exact
     hist, _ = oracle.stencil_histogram(VAR[variant], w.L, w.rc)
     assert np.array_equal(g["hist"], hist)
@@ -59,6 +63,8 @@ def check_against_oracle(w, q, variant, prec, idx=None, kernel="auto"):
     cnt, hs, hx = g["dig"]
     sel = slice(None) if idx is None else idx
     assert np.array_equal(cnt[sel], r.cnt)
+    # the timed kernel's own membership decisions (all tiers), not only the digest instantiation's
+    assert np.array_equal(g["counts"][sel], r.cnt)
     assert np.array_equal(hs[sel], r.hsum)
     assert np.array_equal(hx[sel], r.hxor)
     tF, tU, tW = TOL[prec]
