@@ -113,6 +113,43 @@ def dist_setup(backend):
     return rank, lrank, ws
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def relaxed_fluid(w, variant, k, device, iters=200, eta=1e-3, dmax=0.05):
+    """BASELINE's fluid input (configs 1-4): positions uniform in fractional
+    coordinates, then `iters` capped steepest-descent overlap-removal steps
+    q <- q + F min(eta, dmax / |F|), the forces from the library itself (an NC_F64 context, so the
+    1e30-scale forces of the first, overlapping configurations stay finite).  Untimed input
+    preparation.  Returns fp64 host positions."""
+    import torch
+    from paper_1412_3784_b200 import workloads as W
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    q = torch.from_numpy(W.uniform_positions(w, dtype=np.float64, k=k)).to(device)
+    cl = CellList(variant, "f64", rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, capacity=w.n, max_cells=0,
+                  device=torch.device(device).index or 0)
+    cl.set_box(w.L)
+    F = torch.empty_like(q)
+    for _ in range(iters):
+        cl.compute_forces(q, F)
+        fn = torch.linalg.vector_norm(F, dim=1, keepdim=True).clamp_min(1e-300)
+        q.add_(F * torch.clamp(dmax / fn, max=eta))
+    fmax = float(torch.linalg.vector_norm(F, dim=1).max())
+    cl.close()
+    out = q.cpu().numpy()
+    del q, F
+    torch.cuda.empty_cache()
+    return out, fmax
+
+
 def tier_split(cl, dt):
     """Fraction of the interactions the fp32 far tier evaluates, measured by one extra (untimed)
     SLLOD step with k_pairs' counting instantiation (nc_profile mode 3) after the timed region."""
@@ -186,7 +223,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
         "config": {"workload": f"C{args.config}", "n": w.n, "variant": args.variant, "box": box_text(w)},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle",
+        "ms_per_step_note": "extrapolated: each step is the O(N) cell build plus a bounded particle sample, "
+                            "scaled to one force evaluation of all particles",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": thr, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"per step: full O(N) {args.variant.upper()} cell build + pair loop of {sample} random particles, "
                                    f"extrapolated to one force evaluation of all {w.n}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -291,10 +330,12 @@ def run_slab(args):
     # after the halo arrives): time per EVALUATION
     pairs_eval_ms = pairs_ms / evals
     achieved = flops0 / (pairs_eval_ms * 1e-3) / 1e12
-    roof = {"bound": "alu", "achieved": achieved, "peak": flops0 / t_bound / 1e12, "unit": "TFLOP/s",
-            "frac": achieved / (flops0 / t_bound / 1e12), "traffic": None, "kernel": "k_pairs (rank 0)",
+    roof = {"bound": "alu", "achieved": achieved, "peak": p32 / 1e12, "unit": "TFLOP/s",
+            "frac": achieved / (p32 / 1e12), "traffic": None, "kernel": "k_pairs (rank 0)",
             "kernel_ms": pairs_eval_ms, "launches_per_eval": pairs_n / evals,
-            "peak_note": f"FP32/FP64 blend as the 1-GPU line; {split:.1%} of rank 0's interactions in the fp32 tier"}
+            "peak_note": f"FP32 {p32/1e12:.1f} TFLOP/s ({nsm} SMs x 128 x 2 x {fmax/1e6:.0f} MHz)",
+            "peak_blend": flops0 / t_bound / 1e12, "frac_blend": achieved / (flops0 / t_bound / 1e12),
+            "peak_blend_note": f"FP32/FP64 blend; {split:.1%} of rank 0's interactions in the fp32 tier"}
 
     # end to end through the slab API, pipelined like nc_compute_forces_async: every evaluation each
     # rank copies its own positions from pinned host memory (copy stream, double-buffered, issued
@@ -381,8 +422,18 @@ def run_ours(args):
     peaks = load_peaks()
     prec = args.prec or w.prec[0]          # the config's precision (BASELINE: C0 fp64, C1-C4 fp32)
     npdt = np.float32 if prec == "f32" else np.float64
+    if args.t0 is not None and w.policy == "kr":  # a point of the KR period (fraction of t*)
+        w.t0 = float(args.t0) * w.extra["tstar"]
+        w.L = W.box_at(w.L0, w.A, w.policy, w.t0, w.extra)
     # the same seeded workload per rank (independent replicas; slab decomposition is the next row)
-    q = W.positions(w, dtype=npdt, k=args.config, r=0)
+    input_kind = args.input if args.config != 0 else "lattice"  # C0 is an FCC crystal by BASELINE's spec
+    relax_fmax = None
+    if input_kind == "fluid":
+        qf, relax_fmax = relaxed_fluid(w, args.variant, args.config, f"cuda:{lrank}")
+        q = qf.astype(npdt)
+        del qf
+    else:
+        q = W.positions(w, dtype=npdt, k=args.config, r=0)
     p = W.momenta(w, dtype=npdt, k=args.config, r=0)
     stream = torch.cuda.Stream(lrank)
     cl = CellList(args.variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
@@ -485,7 +536,14 @@ def run_ours(args):
         t_bound = flops / p64                           # NC_F64: every flop in fp64
         peak_note = f"FP64 {p64/1e12:.1f} TFLOP/s at {fmax/1e6:.0f} MHz x {nsm} SMs (NC_F64: all work in fp64)"
     achieved = flops / (pairs_ms_avg * 1e-3) / 1e12
-    peak = flops / t_bound / 1e12
+    peak_blend = flops / t_bound / 1e12
+    peak = (p32 if prec == "f32" else p64) / 1e12  # the FP32 pair-flop roofline (BASELINE), FP64 for NC_F64
+    # the bound that applies: max(T_ALU, T_HBM) with the compulsory force-step bytes
+    # (read q, write F, one cell-sorted copy written and read, key + gid: 56 B fp32 / 104 B fp64)
+    bytes_p = 56.0 if prec == "f32" else 104.0
+    hbm = (peaks.get("hbm_gbs") or 6456.5) * 1e9
+    t_alu, t_hbm = flops / (peak * 1e12), bytes_p * w.n / hbm
+    roof_bound = "alu" if t_alu >= t_hbm else "hbm"
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
@@ -523,7 +581,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         v, tf, r, thr = oracle_sample(w, q, min(args.ref_sample, w.n), prec=prec, variant=args.variant)
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle",
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"full O(N) {args.variant.upper()} cell build + pair loop of {args.ref_sample} random particles of C{args.config}, "
                          f"extrapolated to one force evaluation ({tf:.1f} s)"}
 
@@ -531,8 +589,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_total / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": prec, "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
-            "config": {"workload": f"C{args.config}", "n_per_gpu": w.n, "variant": args.variant,
+            "dtype": prec,
+            "data": ("synthetic fluid: seeded uniform fractional positions + 200 capped steepest-descent overlap-"
+                     f"removal steps through the library (max |F| after: {relax_fmax:.3g}), Gaussian momenta T=1"
+                     if input_kind == "fluid" else
+                     "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)"),
+            "config": {"workload": f"C{args.config}", "n_per_gpu": w.n, "variant": args.variant, "input": input_kind,
+                       "t0": w.t0, "t0_over_period": (w.t0 / w.extra["tstar"] if w.policy == "kr" else None),
                        "box": box_text(w), "potential": pot_text(w),
                        "precision": ("fp32 storage + fp32 filter, fp32/fp64 two-tier interactions" if prec == "f32"
                                      else "fp64 throughout"),
@@ -541,10 +604,17 @@ def run_ours(args):
             "ms_per_step_median": per_step[len(per_step) // 2] if per_step else None,
             "ms_per_step_min": per_step[0] if per_step else None,
             "interactions_per_particle": inter / w.n, "candidates_per_particle": cand / w.n,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "k_pairs",
-                         "kernel_ms": pairs_ms_avg,
-                         "peak_note": peak_note, "pair_kernel": cl.pair_kernel_used()},
+            "roofline": ({"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                          "frac": achieved / peak} if roof_bound == "alu" else
+                         {"bound": "hbm", "achieved": bytes_p * w.n / (pairs_ms_avg * 1e-3) / 1e9,
+                          "peak": hbm / 1e9, "unit": "GB/s", "frac": t_hbm / (pairs_ms_avg * 1e-3)}) | {
+                         "traffic": traffic, "kernel": "k_pairs",
+                         "kernel_ms": pairs_ms_avg, "t_alu_ms": t_alu * 1e3, "t_hbm_ms": t_hbm * 1e3,
+                         "peak_note": (f"FP32 {p32/1e12:.1f} TFLOP/s = {nsm} SMs x 128 x 2 x {fmax/1e6:.0f} MHz"
+                                       if prec == "f32" else peak_note) + "; algorithmic flops 9/candidate + "
+                                       "30/interaction (SURVEY 8(d3)); bytes 56 B/particle (fp32) / 104 (fp64)",
+                         "frac_alu": achieved / peak, "peak_blend": peak_blend, "frac_blend": achieved / peak_blend,
+                         "peak_blend_note": peak_note, "pair_kernel": cl.pair_kernel_used()},
             "kernel_ms_per_step": kernel_ms,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks,
         }
@@ -574,6 +644,9 @@ def main():
     ap.add_argument("--steps-per-call", type=int, default=1,
                     help="SLLOD steps per nc_step_sllod call (0 = all timed steps in one call; measured the same)")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) path even on one GPU")
+    ap.add_argument("--input", default="fluid", choices=["fluid", "lattice"],
+                    help="fluid: BASELINE's relaxed uniform positions (default); lattice: the jittered crystal")
+    ap.add_argument("--t0", type=float, default=None, help="KR configs: start at t0 = this fraction of t*")
     ap.add_argument("--weak", action="store_true",
                     help="slab path, weak scaling: 8,388,608 particles per GPU (box elongated along v3)")
     args = ap.parse_args()

@@ -152,6 +152,19 @@ def positions(w: Workload, dtype=np.float64, k: int = 0, r: int = 0) -> np.ndarr
     return out
 
 
+def uniform_positions(w: Workload, dtype=np.float64, k: int = 0, r: int = 0) -> np.ndarray:
+    """Lab-frame positions q = L lambda with lambda uniform in [0,1)^3 ("positions seeded uniform in
+    fractional coords", BASELINE configs 1-4, taken literally): the starting point of the overlap
+    removal that bench.py runs through the library; no method arithmetic here."""
+    out = np.empty((w.n, 3), dtype=dtype)
+    for c, lo in enumerate(range(0, w.n, CHUNK)):
+        hi = min(w.n, lo + CHUNK)
+        lam = rng_for(k, r, 3000 + c).uniform(0.0, 1.0, size=(hi - lo, 3))
+        q = lam[:, 0:1] * w.L[:, 0] + lam[:, 1:2] * w.L[:, 1] + lam[:, 2:3] * w.L[:, 2]
+        out[lo:hi] = q.astype(dtype)
+    return out
+
+
 def momenta(w: Workload, dtype=np.float64, T: float = 1.0, k: int = 0, r: int = 0) -> np.ndarray:
     """Peculiar momenta: Gaussian at temperature T, zero net momentum (R24)."""
     out = np.empty((w.n, 3), dtype=np.float64)

@@ -30,7 +30,7 @@ def test_bench_line_contract():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and "sm_mhz" in d["clocks"]
-    assert d["config"]["workload"] == "C2"
+    assert d["config"]["workload"] == "C2" and d["config"]["input"] == "fluid"
 
 
 def test_reference_arm_line():
