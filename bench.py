@@ -268,9 +268,11 @@ def run_slab(args):
     sr.set_flow(w.A, w.policy, w.t0, **kw)
     sr.load(q[idx], p[idx], idx.astype(np.int32))
     del q, p
-    from paper_1412_3784_b200.slab import LoopbackTransport
+    from paper_1412_3784_b200.slab import LoopbackTransport, NcclTransport
 
-    sysm = SlabSystem([sr], DistTransport(rank, ws, f"cuda:{lrank}") if ws > 1 else LoopbackTransport())
+    # N > 1: the library's own NCCL data plane (nc_slab_exchange / nc_slab_allgather); torch only
+    # broadcasts the unique id
+    sysm = SlabSystem([sr], NcclTransport(sr, rank, ws) if ws > 1 else LoopbackTransport())
     with torch.cuda.stream(stream):
         sysm.forces(False)
         for _ in range(args.warmup):
@@ -398,7 +400,8 @@ def run_slab(args):
                        "box": box_text(w), "potential": pot_text(w),
                        "precision": "fp32 storage + fp32 filter, fp64 interactions",
                        "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
-                                                                   "NCCL P2P halo + migration"},
+                                                                   "NCCL P2P halo + migration inside "
+                                                                   "libnemdcell (nc_slab_exchange)"},
             "particle_steps_per_s": w.n * args.steps / (ms_max * 1e-3),
             "kernel_ms_per_step_rank0": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(t[3]), "clocks": clocks,

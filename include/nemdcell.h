@@ -329,6 +329,37 @@ nc_status nc_slab_kick(nc_ctx *ctx, void *p, const void *F, int64_t n, double dt
  * rechecks): bitwise the same as a single-device evaluation. */
 nc_status nc_slab_reduce(nc_ctx *ctx, const double *parts, int nlayers, double *U, double W[6], double stats[4]);
 
+/* ---- The slab data plane over NCCL: the library moves the halo, migration and
+ * partial-sum bytes itself, ring neighbours r-1 / r+1, on its own communication stream.  NCCL is loaded
+ * at run time (the copy already in the process, else torch's wheel, else the system one).  The host
+ * only has to broadcast the 128-byte unique id of rank 0 (e.g. torch.distributed.broadcast).
+ * Errors: NC_E_NCCL (library missing or an NCCL call failed; text in nc_last_error), NC_E_ARG,
+ * NC_E_STATE (no communicator / no exchange in flight), NC_E_OOM (a count above the capacity). */
+
+/* A fresh NCCL unique id (rank 0 calls it and broadcasts the 128 bytes). */
+nc_status nc_nccl_unique_id(uint8_t id[128]);
+
+/* Join the communicator of nranks ranks (this context = rank `rank`, on cfg.device). */
+nc_status nc_slab_comm_init(nc_ctx *ctx, int rank, int nranks, const uint8_t id[128]);
+
+/* One ring exchange of records (`words` four-vectors of the storage type each: 2 for migration records,
+ * 1 for halo records; device buffers): send_lo (n_lo records) goes to rank r-1, send_hi (n_hi) to
+ * rank r+1; recv_lo receives rank r-1's upper send, recv_hi rank r+1's lower send, counts[2] = (from
+ * r-1, from r+1), each at most cap.  _start exchanges the counts (one host synchronization of the
+ * communication stream) and leaves the payload in flight on the communication stream after the work
+ * already queued on cfg.stream; _wait makes cfg.stream wait for it (so K3 on interior layers overlaps
+ * the transfer).  nc_slab_exchange = _start + _wait.  Messages to one peer are matched in issue
+ * order, which makes P = 1 (a self ring) and P = 2 pair up correctly. */
+nc_status nc_slab_exchange_start(nc_ctx *ctx, const void *send_lo, int64_t n_lo, const void *send_hi, int64_t n_hi,
+                                 void *recv_lo, void *recv_hi, int64_t cap, int words, int64_t counts[2]);
+nc_status nc_slab_exchange_wait(nc_ctx *ctx);
+nc_status nc_slab_exchange(nc_ctx *ctx, const void *send_lo, int64_t n_lo, const void *send_hi, int64_t n_hi,
+                           void *recv_lo, void *recv_hi, int64_t cap, int words, int64_t counts[2]);
+
+/* All-gather of the per-layer partials (host in / out): this rank's nloc rows of 13 doubles (as
+ * nc_slab_forces writes them), padded to max_rows; out receives nranks x max_rows rows in rank order. */
+nc_status nc_slab_allgather(nc_ctx *ctx, const double *local, int64_t nloc, int64_t max_rows, double *out);
+
 /* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
  * kernel).  Both evaluate the same neighborhoods, the same
  * candidates and the same pair set; they differ in how work maps to warps:

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC_DIR = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(SRC_DIR, "nemdcell.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("kernels.cuh", "k3_seg.cuh", "geom.hpp")] + [
+DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("kernels.cuh", "k3_seg.cuh", "geom.hpp", "nccl_slab.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "nemdcell.h")]
 LIB = os.path.join(HERE, "libnemdcell.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -20,6 +20,7 @@ NVCC_FLAGS = [
     # one CUDA runtime per process: share libcudart.so.12 with torch instead of a
     # private static copy (two runtimes tearing down the same context at exit crashed)
     "-cudart", "shared", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+    "-ldl",  # NCCL is dlopen'ed at run time (csrc/nccl_slab.cuh)
 ]
 
 

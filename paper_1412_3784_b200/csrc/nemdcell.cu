@@ -94,6 +94,16 @@ struct nc_ctx {
   int dbg_drop = 0;               // nc_debug negative control
   PairOut po{nullptr, nullptr, 0};  // nc_get_pairs: pair-list output of the next digest evaluation
 
+  // slab data plane over NCCL (nccl_slab.cuh): communicator, its stream, scratch
+  void* comm = nullptr;
+  int comm_rank = 0, comm_nranks = 1;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_comm_in = nullptr, ev_comm_out = nullptr;
+  int64_t* comm_cnt = nullptr;
+  void* comm_gather = nullptr;
+  size_t comm_gather_bytes = 0;
+  bool comm_pending = false;
+
   // live kernel timing (nc_profile)
   bool prof = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
@@ -1070,6 +1080,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
   return NC_OK;
 }
 
+void nc_comm_release(nc_ctx* ctx);  // nccl_slab.cuh
+
 void nc_destroy(nc_ctx* ctx) {
   if (!ctx) return;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
@@ -1099,6 +1111,7 @@ void nc_destroy(nc_ctx* ctx) {
     cudaEventDestroy(p.second.second);
   }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  nc_comm_release(ctx);
   delete ctx;
 }
 
@@ -1573,3 +1586,17 @@ nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* 
 }
 
 }  // extern "C"
+
+#include "nccl_slab.cuh"
+
+void nc_comm_release(nc_ctx* ctx) {
+  if (!ctx->comm) return;
+  if (ctx->s_comm) cudaStreamSynchronize(ctx->s_comm);
+  nccl().CommDestroy((ncclComm_t)ctx->comm);
+  ctx->comm = nullptr;
+  if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
+  if (ctx->ev_comm_in) cudaEventDestroy(ctx->ev_comm_in);
+  if (ctx->ev_comm_out) cudaEventDestroy(ctx->ev_comm_out);
+  if (ctx->comm_cnt) cudaFree(ctx->comm_cnt);
+  if (ctx->comm_gather) cudaFree(ctx->comm_gather);
+}

@@ -30,7 +30,9 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_slab_unpack",
            "nc_slab_halo", "nc_slab_forces", "nc_slab_forces_begin", "nc_slab_forces_end", "nc_slab_kick",
            "nc_slab_reduce", "nc_set_pair_kernel",
-           "nc_pair_kernel_used", "nc_get_pairs", "nc_get_cell_gids", "nc_get_pair_counts", "nc_debug"]
+           "nc_pair_kernel_used", "nc_get_pairs", "nc_get_cell_gids", "nc_get_pair_counts", "nc_debug",
+           "nc_nccl_unique_id", "nc_slab_comm_init", "nc_slab_exchange_start", "nc_slab_exchange_wait",
+           "nc_slab_exchange", "nc_slab_allgather"]
 NC_DBG_DROP_ENTRIES = 1
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
@@ -104,6 +106,12 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_get_cell_gids.argtypes = [vp, vp]
         L.nc_get_pair_counts.argtypes = [vp, vp]
         L.nc_debug.argtypes = [vp, i32, i32]
+        L.nc_nccl_unique_id.argtypes = [vp]
+        L.nc_slab_comm_init.argtypes = [vp, i32, i32, vp]
+        L.nc_slab_exchange_start.argtypes = [vp, vp, i64, vp, i64, vp, vp, i64, i32, vp]
+        L.nc_slab_exchange_wait.argtypes = [vp]
+        L.nc_slab_exchange.argtypes = [vp, vp, i64, vp, i64, vp, vp, i64, i32, vp]
+        L.nc_slab_allgather.argtypes = [vp, vp, i64, i64, vp]
         L.nc_get_stencil_histogram.argtypes = [vp, vp]
         L.nc_profile.argtypes = [vp, i32]
         L.nc_profile_read.argtypes = [vp, vp, vp]
@@ -372,6 +380,43 @@ def nc_slab_reduce(ctx, parts: np.ndarray):
     st = np.zeros(4)
     _check(ctx, load().nc_slab_reduce(ctx, _ptr(parts), int(parts.shape[0]), ctypes.byref(U), _ptr(W), _ptr(st)))
     return U.value, W, {"interactions": st[0], "candidates": st[1], "stencil_cells": st[2], "rechecks": st[3]}
+
+
+def nc_nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(None, load().nc_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def nc_slab_comm_init(ctx, rank: int, nranks: int, uid: bytes) -> None:
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _check(ctx, load().nc_slab_comm_init(ctx, int(rank), int(nranks), buf))
+
+
+def nc_slab_exchange_start(ctx, send_lo, n_lo, send_hi, n_hi, recv_lo, recv_hi, cap, words):
+    c = np.zeros(2, dtype=np.int64)
+    _check(ctx, load().nc_slab_exchange_start(ctx, _ptr(send_lo), int(n_lo), _ptr(send_hi), int(n_hi), _ptr(recv_lo),
+                                              _ptr(recv_hi), int(cap), int(words), _ptr(c)))
+    return int(c[0]), int(c[1])
+
+
+def nc_slab_exchange_wait(ctx) -> None:
+    _check(ctx, load().nc_slab_exchange_wait(ctx))
+
+
+def nc_slab_exchange(ctx, send_lo, n_lo, send_hi, n_hi, recv_lo, recv_hi, cap, words):
+    c = np.zeros(2, dtype=np.int64)
+    _check(ctx, load().nc_slab_exchange(ctx, _ptr(send_lo), int(n_lo), _ptr(send_hi), int(n_hi), _ptr(recv_lo),
+                                        _ptr(recv_hi), int(cap), int(words), _ptr(c)))
+    return int(c[0]), int(c[1])
+
+
+def nc_slab_allgather(ctx, local: np.ndarray, max_rows: int, nranks: int) -> np.ndarray:
+    local = np.ascontiguousarray(local, dtype=np.float64).reshape(-1, NPART)
+    out = np.zeros((nranks * max_rows, NPART))
+    _check(ctx, load().nc_slab_allgather(ctx, _ptr(local) if len(local) else None, len(local), int(max_rows),
+                                         _ptr(out)))
+    return out
 
 
 def nc_launch_count(ctx) -> int:

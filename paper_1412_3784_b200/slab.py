@@ -177,13 +177,17 @@ class DistTransport:
     Messages to one peer are matched in issue order: each rank sends to r-1
     first, then to r+1, and receives from r+1 first, then from r-1."""
 
-    def __init__(self, rank, nranks, device):
+    def __init__(self, rank, nranks, device, stream=None):
         import torch
         import torch.distributed as dist
 
         self.torch, self.dist = torch, dist
         self.rank, self.P = rank, nranks
         self.device = device
+        # the stream the library's kernels run on (cfg.stream): the exchange is waited for ON it, so
+        # nc_slab_forces_end never reads a halo buffer before it has arrived, whatever the caller's
+        # current stream (ADVICE r01)
+        self.stream = stream
 
     def _p2p(self, tensors_out, tensors_in):
         dist = self.dist
@@ -216,8 +220,13 @@ class DistTransport:
 
     def finish(self, pending):
         works, out = pending
-        for w in works:
-            w.wait()  # the current stream waits for the exchange
+        if self.stream is not None and str(self.device).startswith("cuda"):
+            with self.torch.cuda.stream(self.torch.cuda.ExternalStream(self.stream)):
+                for w in works:
+                    w.wait()  # the library's stream waits for the exchange
+        else:
+            for w in works:
+                w.wait()
         return out
 
     def exchange(self, sends, recv_bufs):
@@ -245,6 +254,91 @@ class DistTransport:
         bufs = [torch.zeros_like(buf) for _ in range(self.P)]
         dist.all_gather(bufs, buf)
         return np.concatenate([b[:int(k.item())].cpu().numpy() for b, k in zip(bufs, ns)], axis=0)
+
+
+class HostStagedTransport(DistTransport):
+    """gloo between processes (e.g. ranks that share one GPU in a test): every device buffer crosses
+    through host memory, so no rank's kernels ever wait on another rank's on the device."""
+
+    def __init__(self, rank, nranks):
+        super().__init__(rank, nranks, "cpu")
+
+    def _p2p(self, tensors_out, tensors_in):
+        outs = [t.cpu() for t in tensors_out]
+        ins = [self.torch.empty(t.shape, dtype=t.dtype) for t in tensors_in]
+        super()._p2p(outs, ins)
+        for t, c in zip(tensors_in, ins):
+            t.copy_(c)
+
+    def start(self, sends, recv_bufs, counts):
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        b_lo, b_hi = recv_bufs[0]
+        (m_lo, m_hi), = counts
+        assert m_lo <= len(b_lo) and m_hi <= len(b_hi), "receive buffer too small"
+        self._p2p([s_lo[:max(n_lo, 1)], s_hi[:max(n_hi, 1)]], [b_lo[:max(m_lo, 1)], b_hi[:max(m_hi, 1)]])
+        return [(b_lo, m_lo, b_hi, m_hi)]
+
+    def finish(self, pending):
+        return pending
+
+
+class NcclTransport:
+    """The data plane inside libnemdcell.so (nc_slab_exchange*, nc_slab_allgather over NCCL, on the
+    library's communication stream): one rank per process, the host only broadcasts rank 0's NCCL
+    unique id (torch.distributed, any backend).  A single rank (P = 1) runs the same calls as a self
+    ring, which is how it is exercised on one GPU."""
+
+    def __init__(self, slab_rank, group_rank: int, nranks: int):
+        self.sr = slab_rank
+        self.rank, self.P = group_rank, nranks
+        if nranks > 1:
+            import torch
+            import torch.distributed as dist
+
+            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+            t = torch.zeros(128, dtype=torch.uint8, device=dev)
+            if group_rank == 0:
+                t.copy_(torch.frombuffer(bytearray(nc.nc_nccl_unique_id()), dtype=torch.uint8))
+            dist.broadcast(t, 0)
+            uid = bytes(t.cpu().numpy().tobytes())
+        else:
+            uid = nc.nc_nccl_unique_id()
+        nc.nc_slab_comm_init(slab_rank.ctx, group_rank, nranks, uid)
+
+    @staticmethod
+    def _words(buf):
+        return int(buf.shape[1]) // 4
+
+    def counts(self, sends):
+        """Counts AND the payload launch (the library exchanges the counts, then leaves the payload in
+        flight on its communication stream); start() hands the result over, finish() waits."""
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        b_lo, b_hi = self.sr.hrecv
+        m_lo, m_hi = nc.nc_slab_exchange_start(self.sr.ctx, s_lo, n_lo, s_hi, n_hi, b_lo, b_hi, len(b_lo),
+                                               self._words(s_lo))
+        self._inflight = [(b_lo, m_lo, b_hi, m_hi)]
+        return [(m_lo, m_hi)]
+
+    def start(self, sends, recv_bufs, counts):
+        return self._inflight
+
+    def finish(self, pending):
+        nc.nc_slab_exchange_wait(self.sr.ctx)
+        return pending
+
+    def exchange(self, sends, recv_bufs):
+        (s_lo, n_lo, s_hi, n_hi), = sends
+        b_lo, b_hi = recv_bufs[0]
+        m_lo, m_hi = nc.nc_slab_exchange(self.sr.ctx, s_lo, n_lo, s_hi, n_hi, b_lo, b_hi, len(b_lo), self._words(s_lo))
+        return [(b_lo, m_lo, b_hi, m_hi)]
+
+    def gather(self, parts):
+        part, = parts
+        klo, khi, l3 = self.sr.layers()
+        rows = -(-l3 // self.P)
+        allp = nc.nc_slab_allgather(self.sr.ctx, part, rows, self.P)
+        out = [allp[k * rows:k * rows + ((k + 1) * l3 // self.P - k * l3 // self.P)] for k in range(self.P)]
+        return np.concatenate(out, axis=0)
 
 
 # -------------------------------------------------------------------- driver

@@ -132,3 +132,42 @@ def test_slab_forces_bitwise_sparse_cells(P, variant):
     assert st["interactions"] == st1["interactions"] and st["candidates"] == st1["candidates"]
     for r in sysm.ranks:
         r.close()
+
+
+@pytest.mark.parametrize("variant", ["do", "ds"])
+def test_nccl_data_plane_self_ring_bitwise(variant):
+    """The library's NCCL data plane (nc_slab_comm_init / nc_slab_exchange* / nc_slab_allgather) on a
+    one-rank communicator: the ring neighbours are the rank itself, so every exchange and the
+    all-gather run through NCCL on one GPU; forces and an SLLOD run stay bitwise equal to the
+    single-device path."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+    from paper_1412_3784_b200.slab import NcclTransport, SlabRank, SlabSystem
+
+    w = W.make(2, scale=2)
+    q = W.positions(w, dtype=np.float32, k=2)
+    p = W.momenta(w, dtype=np.float32, k=2)
+    one = CellList(variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    one.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
+    F1 = torch.empty((len(q), 3), dtype=torch.float32, device="cuda")
+    U0, W0 = one.stats()["U"], one.stats()["W"]
+    U1, W1 = one.step(w.dt, 3)
+    qo = torch.empty((len(q), 3), dtype=torch.float32, device="cuda")
+    po = torch.empty_like(qo)
+    one.get_state(qo, po)
+    one.close()
+    sr = SlabRank(0, 1, variant=variant, prec="f32", rc=w.rc, u_shift=w.ushift, capacity=len(q),
+                  max_cells=4 * len(q) + 4096)
+    sr.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    sr.load(q, p, np.arange(len(q), dtype=np.int32))
+    sysm = SlabSystem([sr], NcclTransport(sr, 0, 1))
+    Uf, Wf, _ = sysm.forces(True)
+    assert Uf == U0 and np.array_equal(Wf, W0)
+    out = None
+    for _ in range(3):
+        out = sysm.step(w.dt, True)
+    qs, ps, _ = gather_state(sysm, len(q), np.float32)
+    assert np.array_equal(qs, qo.cpu().numpy()) and np.array_equal(ps, po.cpu().numpy())
+    assert out[0] == U1 and np.array_equal(out[1], W1)
+    sr.close()
