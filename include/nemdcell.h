@@ -290,6 +290,12 @@ nc_status nc_slab_migrate(nc_ctx *ctx, void *q, const void *p, const uint32_t *g
                           void *q_out, void *p_out, uint32_t *gid_out, void *send_lo, void *send_hi, int64_t cap,
                           int64_t counts[3]);
 
+/* Wrap q in place (R15) and write each particle's cell layer (DS floor(lambda_3 c_3), DO floor(z/w_3))
+ * to layer (int32, device): the ownership test after the layer count l3 changed (GKR boxes, DS under
+ * general flows), when particles can be further than one layer from their slab and the host driver
+ * repartitions instead of migrating. */
+nc_status nc_slab_layer_of(nc_ctx *ctx, void *q, int64_t n, int32_t *layer);
+
 /* Unpack n migration records into n x 3 q, p and gid (append arrivals). */
 nc_status nc_slab_unpack(nc_ctx *ctx, const void *rec, int64_t n, void *q, void *p, uint32_t *gid);
 

@@ -1731,9 +1731,10 @@ __global__ void k_kick3(int64_t n, T* __restrict__ p, const T* __restrict__ F, S
 // mode 0 (migration): wrap q in place (R15); class 0 = layer owned, 1 = layer klo-1 (to rank r-1),
 //                     2 = layer khi (to rank r+1), 3 = further away (error).
 // mode 1 (halo):      class 1 = layer klo (copy to r-1), 2 = layer khi-1 (copy to r+1), else 0.
+// mode 2 (layers):    wrap q in place and write each particle's cell layer to layer_out.
 template <typename T>
 __global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_constant__ Geom g, int klo, int khi,
-                                int mode, uint8_t* __restrict__ cls) {
+                                int mode, uint8_t* __restrict__ cls, int32_t* __restrict__ layer_out = nullptr) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double q0 = (double)q[3 * i], q1 = (double)q[3 * i + 1], q2 = (double)q[3 * i + 2];
@@ -1750,6 +1751,10 @@ __global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_const
   CellPos cp;
   cell_of(g, lam, cp);
   const int k = cp.a[2], l3 = g.dims[2];
+  if (mode == 2) {  // the layer itself (repartition after a change of l3)
+    layer_out[i] = k;
+    return;
+  }
   uint8_t c;
   if (mode == 0) {
     if (k >= klo && k < khi) c = 0;

@@ -1473,6 +1473,21 @@ nc_status nc_slab_migrate(nc_ctx* ctx, void* q, const void* p, const uint32_t* g
   return NC_OK;
 }
 
+nc_status nc_slab_layer_of(nc_ctx* ctx, void* q, int64_t n, int32_t* layer) {
+  if (!ctx || (n > 0 && (!q || !layer)) || n < 0) return fail(ctx, NC_E_ARG, "null argument");
+  if (!ctx->have_box) return fail(ctx, NC_E_STATE, "nc_set_box or nc_set_flow first");
+  if (n > 0) {
+    prof_begin(ctx);
+    if (ctx->cfg.prec == NC_F32)
+      k_slab_classify<float><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (float*)q, ctx->g, 0, 0, 2, nullptr, layer);
+    else
+      k_slab_classify<double><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (double*)q, ctx->g, 0, 0, 2, nullptr, layer);
+    LAUNCHED();
+    prof_end(ctx, NC_K_WRAPKEY);
+  }
+  return NC_OK;
+}
+
 nc_status nc_slab_unpack(nc_ctx* ctx, const void* rec, int64_t n, void* q, void* p, uint32_t* gid) {
   if (!ctx || (n > 0 && (!rec || !q || !p || !gid))) return fail(ctx, NC_E_ARG, "null argument");
   if (n <= 0) return NC_OK;

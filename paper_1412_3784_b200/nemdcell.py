@@ -32,7 +32,7 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_slab_reduce", "nc_set_pair_kernel",
            "nc_pair_kernel_used", "nc_get_pairs", "nc_get_cell_gids", "nc_get_pair_counts", "nc_debug",
            "nc_nccl_unique_id", "nc_slab_comm_init", "nc_slab_exchange_start", "nc_slab_exchange_wait",
-           "nc_slab_exchange", "nc_slab_allgather"]
+           "nc_slab_exchange", "nc_slab_allgather", "nc_slab_layer_of"]
 NC_DBG_DROP_ENTRIES = 1
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
@@ -112,6 +112,7 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_slab_exchange_wait.argtypes = [vp]
         L.nc_slab_exchange.argtypes = [vp, vp, i64, vp, i64, vp, vp, i64, i32, vp]
         L.nc_slab_allgather.argtypes = [vp, vp, i64, i64, vp]
+        L.nc_slab_layer_of.argtypes = [vp, vp, i64, vp]
         L.nc_get_stencil_histogram.argtypes = [vp, vp]
         L.nc_profile.argtypes = [vp, i32]
         L.nc_profile_read.argtypes = [vp, vp, vp]
@@ -334,6 +335,10 @@ def nc_slab_migrate(ctx, q, p, gid, n, klo, khi, q_out, p_out, gid_out, send_lo,
     _check(ctx, load().nc_slab_migrate(ctx, _ptr(q), _ptr(p), _ptr(gid), int(n), int(klo), int(khi), _ptr(q_out),
                                        _ptr(p_out), _ptr(gid_out), _ptr(send_lo), _ptr(send_hi), int(cap), _ptr(c)))
     return int(c[0]), int(c[1]), int(c[2])
+
+
+def nc_slab_layer_of(ctx, q, n, layer) -> None:
+    _check(ctx, load().nc_slab_layer_of(ctx, _ptr(q), int(n), _ptr(layer)))
 
 
 def nc_slab_unpack(ctx, rec, n, q, p, gid) -> None:

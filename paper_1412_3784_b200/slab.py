@@ -59,6 +59,7 @@ class SlabRank:
         self.hrecv = [t(self.bcap, 4), t(self.bcap, 4)]
         self.n = 0
         self.pending_dt = 0.0  # a deferred closing half kick (see kick)
+        self.last_l3 = None    # cell layers of the box the particles were last distributed on
 
     def set_flow(self, A, policy, t0, **kw):
         self.cl.set_flow(A, policy, t0, **kw)
@@ -74,12 +75,39 @@ class SlabRank:
         self.p[:n].copy_(self.torch.as_tensor(p_own))
         self.gid[:n].copy_(self.torch.as_tensor(np.asarray(gid_own, dtype=np.int32)))
         self.n = n
+        self.last_l3 = self.layers()[2]
 
     # ---------------------------------------------------------------- phases
     def kick_drift(self, dt):
         # the previous step's closing half kick, if deferred, runs in the same pass
         nc.nc_slab_kick_kick_drift(self.ctx, self.q, self.p, self.F, self.n, self.pending_dt, dt)
         self.pending_dt = 0.0
+
+    def l3_changed(self):
+        return self.layers()[2] != self.last_l3
+
+    def owned(self):
+        """(q, p, gid, owner rank) of the own particles, q wrapped, owners for the CURRENT l3
+        (nc_slab_layer_of): the input of a repartition."""
+        torch = self.torch
+        n = self.n
+        layer = torch.empty(max(n, 1), dtype=torch.int32, device=self.dev)
+        nc.nc_slab_layer_of(self.ctx, self.q, n, layer)
+        _, _, l3 = self.layers()
+        bounds = torch.tensor([r * l3 // self.nranks for r in range(1, self.nranks)], dtype=torch.int32,
+                              device=self.dev)
+        owner = torch.bucketize(layer[:n], bounds, right=True)  # r with floor(r l3/P) <= layer < floor((r+1) l3/P)
+        return self.q[:n].clone(), self.p[:n].clone(), self.gid[:n].clone(), owner
+
+    def take(self, q, p, gid):
+        """Replace the own particles (after a repartition)."""
+        n = len(q)
+        assert n <= self.cap, "slab capacity exceeded"
+        self.q[:n].copy_(q)
+        self.p[:n].copy_(p)
+        self.gid[:n].copy_(gid)
+        self.n = n
+        self.last_l3 = self.layers()[2]
 
     def migrate(self):
         klo, khi, _ = self.layers()
@@ -171,6 +199,32 @@ class LoopbackTransport:
     def gather(self, parts):
         return np.concatenate(parts, axis=0)
 
+    def allgather_tensors(self, per_rank):
+        """per_rank[r] = tuple of tensors of rank r -> tuple of concatenations over the ranks."""
+        import torch
+
+        return tuple(torch.cat([t[k] for t in per_rank]) for k in range(len(per_rank[0])))
+
+
+def _dist_allgather_tensors(dist, torch, device, tensors):
+    """All-gather of variable-length tensors (counts first, padded payload) through torch.distributed:
+    the rare repartition after an l3 change, not the per-step data plane."""
+    n = torch.tensor([len(tensors[0])], dtype=torch.int64, device=device)
+    P = dist.get_world_size()
+    ns = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(P)]
+    dist.all_gather(ns, n)
+    counts = [int(x.item()) for x in ns]
+    mx = max(max(counts), 1)
+    out = []
+    for t in tensors:
+        src = t.to(device)
+        buf = torch.zeros((mx,) + tuple(src.shape[1:]), dtype=src.dtype, device=device)
+        buf[:len(src)] = src
+        bufs = [torch.zeros_like(buf) for _ in range(P)]
+        dist.all_gather(bufs, buf)
+        out.append(torch.cat([b[:c] for b, c in zip(bufs, counts)]).to(t.device))
+    return tuple(out)
+
 
 class DistTransport:
     """One rank of a torch.distributed group (NCCL between GPUs, gloo on CPU).
@@ -241,6 +295,9 @@ class DistTransport:
         assert m_lo <= len(b_lo) and m_hi <= len(b_hi), "receive buffer too small"
         self._p2p([s_lo[:max(n_lo, 1)], s_hi[:max(n_hi, 1)]], [b_lo[:max(m_lo, 1)], b_hi[:max(m_hi, 1)]])
         return [(b_lo, m_lo, b_hi, m_hi)]
+
+    def allgather_tensors(self, per_rank):
+        return _dist_allgather_tensors(self.dist, self.torch, self.device, per_rank[0])
 
     def gather(self, parts):
         torch, dist = self.torch, self.dist
@@ -332,6 +389,15 @@ class NcclTransport:
         m_lo, m_hi = nc.nc_slab_exchange(self.sr.ctx, s_lo, n_lo, s_hi, n_hi, b_lo, b_hi, len(b_lo), self._words(s_lo))
         return [(b_lo, m_lo, b_hi, m_hi)]
 
+    def allgather_tensors(self, per_rank):
+        import torch
+        import torch.distributed as dist
+
+        if self.P == 1:
+            return per_rank[0]
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        return _dist_allgather_tensors(dist, torch, dev, per_rank[0])
+
     def gather(self, parts):
         part, = parts
         klo, khi, l3 = self.sr.layers()
@@ -364,6 +430,7 @@ class SlabSystem:
     def __init__(self, ranks, transport):
         self.ranks = ranks
         self.tr = transport
+        self.repartitions = 0
 
     def forces(self, want_uw=True):
         hs = [r.halo() for r in self.ranks]
@@ -389,13 +456,27 @@ class SlabSystem:
             if hasattr(r, "flush"):
                 r.flush()
 
+    def repartition(self):
+        """After the cell-layer count l3 changed (GKR boxes, DS under general flows): every
+        particle goes to the rank owning its layer in the new grid (all-gather, then each rank keeps its
+        own).  Rare; results stay bitwise those of one device (cells are rebuilt in (cell, gid) order)."""
+        owned = [r.owned() for r in self.ranks]
+        q, p, gid, owner = self.tr.allgather_tensors(owned)
+        for r in self.ranks:
+            m = owner == r.rank
+            r.take(q[m], p[m], gid[m])
+        self.repartitions += 1
+
     def step(self, dt, want_uw=True):
         for r in self.ranks:
             r.kick_drift(dt)
-        sends = [r.migrate() for r in self.ranks]
-        recvs = self.tr.exchange(sends, [r.recv for r in self.ranks])
-        for r, rv in zip(self.ranks, recvs):
-            r.absorb(*rv)
+        if any(getattr(r, "l3_changed", lambda: False)() for r in self.ranks):
+            self.repartition()
+        else:
+            sends = [r.migrate() for r in self.ranks]
+            recvs = self.tr.exchange(sends, [r.recv for r in self.ranks])
+            for r, rv in zip(self.ranks, recvs):
+                r.absorb(*rv)
         out = self.forces(want_uw)
         for r in self.ranks:
             r.kick(dt)

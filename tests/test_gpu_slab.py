@@ -171,3 +171,44 @@ def test_nccl_data_plane_self_ring_bitwise(variant):
     assert np.array_equal(qs, qo.cpu().numpy()) and np.array_equal(ps, po.cpu().numpy())
     assert out[0] == U1 and np.array_equal(out[1], W1)
     sr.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("variant", ["do", "ds"])
+def test_slab_repartition_when_l3_changes(P, variant):
+    """Generalized KR (uniaxial, fast strain): the cell-layer count l3 changes inside the run (the box
+    stretches along v3 and a GKR reset remaps it), so slab ownership is recomputed and particles move
+    by many layers (SlabSystem.repartition); the trajectory stays bitwise that of one device."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(3, scale=4)  # 32768 WCA particles, GKR box
+    w.A = w.A * 20.0        # eps = 2: several l3 changes within 12 steps
+    w.extra = dict(w.extra, eps=w.extra["eps"] * 20.0)
+    w.t0 = 0.01
+    w.L = W.box_at(w.L0, w.A, w.policy, w.t0, w.extra)
+    q = W.positions(w, dtype=np.float32, k=3)
+    p = W.momenta(w, dtype=np.float32, k=3)
+    nsteps = 12
+    one = CellList(variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q), max_cells=4 * len(q) + 4096)
+    one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    one.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
+    l3s = [one.stats()["dims"][2]]
+    for _ in range(nsteps):
+        U1, W1 = one.step(w.dt, 1)
+        l3s.append(one.stats()["dims"][2])
+    qo = torch.empty((len(q), 3), dtype=torch.float32, device="cuda")
+    po = torch.empty_like(qo)
+    one.get_state(qo, po)
+    one.close()
+    assert len(set(l3s)) > 1, l3s  # the layer count really changes
+    sysm = make_system(w, q, p, P, variant, "f32")
+    sysm.forces(False)
+    for _ in range(nsteps):
+        out = sysm.step(w.dt, True)
+    assert sysm.repartitions >= 1
+    qs, ps, _ = gather_state(sysm, len(q), np.float32)
+    assert np.array_equal(qs, qo.cpu().numpy()) and np.array_equal(ps, po.cpu().numpy())
+    assert out[0] == U1 and np.array_equal(out[1], W1)
+    for r in sysm.ranks:
+        r.close()

@@ -169,3 +169,40 @@ def test_slab_protocol_gloo(P):
         assert werr <= 1e-12 * wmax
         assert inter == iref
         assert conserved and lay_ok
+
+
+def _allgather_worker(rank, P, port, out):
+    from paper_1412_3784_b200.slab import DistTransport
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=P)
+    try:
+        n = 3 + 2 * rank  # variable lengths
+        q = torch.full((n, 3), float(rank))
+        gid = torch.arange(n, dtype=torch.int32) + 100 * rank
+        owner = torch.full((n,), (rank + 1) % P, dtype=torch.int64)
+        tq, tg, to = DistTransport(rank, P, "cpu").allgather_tensors([(q, gid, owner)])
+        out.put((rank, tq.tolist(), tg.tolist(), to.tolist()))
+    finally:
+        torch.distributed.destroy_process_group()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_repartition_allgather_gloo(P):
+    """The all-gather behind SlabSystem.repartition (counts, padded payload, rank order) over gloo."""
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_allgather_worker, args=(r, P, port, out)) for r in range(P)]
+    for pr in procs:
+        pr.start()
+    res = sorted(out.get(timeout=300) for _ in range(P))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    exp_g = sum([[k + 100 * r for k in range(3 + 2 * r)] for r in range(P)], [])
+    exp_q = sum([[[float(r)] * 3] * (3 + 2 * r) for r in range(P)], [])
+    for rank, tq, tg, to in res:
+        assert tg == exp_g and tq == exp_q
+        assert to == sum([[(r + 1) % P] * (3 + 2 * r) for r in range(P)], [])
