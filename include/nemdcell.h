@@ -369,14 +369,16 @@ nc_status nc_slab_allgather(nc_ctx *ctx, const double *local, int64_t nloc, int6
 /* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
  * kernel).  Both evaluate the same neighborhoods, the same
  * candidates and the same pair set; they differ in how work maps to warps:
- *  NC_PK_AUTO    (default) segment kernel when the mean occupancy is below 4
+ *  NC_PK_AUTO    (default) the row-segment kernel when the mean occupancy is below 4
  *                particles per cell (WCA at rho = 0.8442: ~1.3), else per cell;
  *  NC_PK_CELL    one warp per center cell (k_pairs);
  *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
- *                union of their neighborhoods (k_pairs_seg), fp64 pair forces.
+ *                union of their neighborhoods (k_pairs_seg, round 1), fp64 pair forces;
+ *  NC_PK_SPARSE  one thread per particle, 32 consecutive particles of a cell row per warp walking
+ *                their exact stencils in lockstep through L1 (k_pairs_sparse), fp64 pair forces.
  * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT on an NC_F64 context).
- * nc_pair_kernel_used returns the kernel of the last evaluation (1 or 2, 0 = none). */
-typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2 } nc_pair_kernel;
+ * nc_pair_kernel_used returns the kernel of the last evaluation (1, 2 or 3, 0 = none). */
+typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2, NC_PK_SPARSE = 3 } nc_pair_kernel;
 nc_status nc_set_pair_kernel(nc_ctx *ctx, int which);
 int nc_pair_kernel_used(const nc_ctx *ctx);
 

@@ -1,0 +1,340 @@
+// k3_sparse.cuh -- K3 for sparse cells (WCA at rho = 0.8442: ~1.3 particles per cell), NC_F32.
+// Included at the end of kernels.cuh.
+//
+// One thread per particle i, the paper's loop literally: for each cell of
+// i's neighborhood (27 DS / 27-36 DO by the exact interval rule, the same fp64 expressions as
+// build_entries, so stencils and candidate counts are the oracle's bit for bit), each particle j of
+// that cell, distance check.  The 32 lanes of a warp hold 32 CONSECUTIVE particles of the
+// (cell, gid) order -- consecutive cells of one row -- and walk the stencil rows in lockstep: in row
+// r, lane i scans the contiguous particle range of its 3-4 neighbour columns, and because the lanes'
+// cells are consecutive, each warp-wide load touches a few consecutive 128-byte lines (coalesced,
+// L1/L2-resident: no shared-memory staging, no per-segment setup).  Lattice images: the column
+// shift of a wrapped column and the row's (n2, n3) shift, applied as a bracket in i's cell-local
+// rotated frame (|d| stays ~ r_c: fp32 filter with the superset band), exactly as k_pairs' entries.
+// Filter survivors are queued per lane (shared memory) and evaluated in fp64 from the fp64
+// cell-local coordinates with the canonical R16 test inside the 1e-12 band (WCA pairs all lie below
+// r_split: every interaction is fp64).  Full i-side accumulation, no atomics; block partials are a
+// fixed-order sum over a fixed particle range of ONE layer (layer-aligned, P-invariant).
+#pragma once
+
+namespace nc {
+
+constexpr int SP_NT = 128;    // threads per block (one particle each per chunk)
+constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane could overflow)
+
+struct SpSmem {
+  uint32_t qj[SP_QCAP][SP_NT];  // sorted index of a queued j
+  uint32_t qd[SP_QCAP][SP_NT];  // its neighbour cell's unwrapped deltas: column (low 16 bits), row (high)
+  uint16_t qn[SP_QCAP][SP_NT];  // layer delta and image shifts (3 bits each, +4): d2, n1, n2, n3
+  double part[SP_NT / 32][NPART];
+};
+
+// row ri of cell (a0, a1, a2)'s neighborhood: columns [c0, c1) (unwrapped), row image shifts and the
+// row's unwrapped deltas.  Returns false if the row does not exist (DO: 3 of the 4 slots of a layer
+// when the y offset is a multiple of the cell height; DS: ri >= 9).  The expressions are
+// build_entries' (canonical fp64 for DO).
+struct SpRow {
+  int c0, c1;          // unwrapped columns
+  int n2, n3, d1, d2;  // image shifts (y, z) and unwrapped row deltas (m - a1, kk - a2)
+  uint32_t base;       // first cell id of the row: l1 (jd + l2 kd)
+};
+__device__ __forceinline__ bool sp_row(const Geom& g, int ri, int a0, int a1, int a2, SpRow& r) {
+  const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
+  if (g.variant == 0) {
+    if (ri >= 9) return false;
+    const int d1 = ri % 3 - 1, d2 = ri / 3 - 1;
+    const int m1 = a1 + d1, m2 = a2 + d2;
+    const int n1 = floordiv(m1, l2), n2 = floordiv(m2, l3);
+    r.c0 = a0 - 1;
+    r.c1 = a0 + 2;
+    r.n2 = n1;  // DS: the y and z lattice shifts of the row
+    r.n3 = n2;
+    r.d1 = d1;
+    r.d2 = d2;
+    r.base = (uint32_t)l1 * ((uint32_t)(m1 - n1 * l2) + (uint32_t)l2 * (uint32_t)(m2 - n2 * l3));
+    return true;
+  }
+  const int dz = ri / 4 - 1, rr = ri % 4;
+  const int kk = a2 + dz;
+  const int n3 = floordiv(kk, l3);
+  const int kd = kk - n3 * l3;
+  const double oy = __dmul_rn((double)n3, g.d32);
+  const int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
+  const int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
+  if (rr >= m1 - m0) return false;
+  const int m = m0 + rr;
+  const int n2 = floordiv(m, l2);
+  const int jd = m - n2 * l2;
+  const double ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
+  r.c0 = (int)floor(__dsub_rn((double)(a0 - 1), ox));
+  r.c1 = (int)ceil(__dsub_rn((double)(a0 + 2), ox));
+  r.n2 = n2;
+  r.n3 = n3;
+  r.d1 = m - a1;
+  r.d2 = dz;
+  r.base = (uint32_t)l1 * ((uint32_t)jd + (uint32_t)l2 * (uint32_t)kd);
+  return true;
+}
+
+// A neighbour cell relative to i's cell: unwrapped deltas (d0 column, d1 row, d2 layer) and the
+// lattice image n (DO: the column's x shift n1 and the row's n2, n3; DS: the x, y, z wraps).  The
+// column / row deltas can be large in DO (the rows of the offset faces sit ~n2 d21 cells away), so
+// they take 16 bits each; the rest 3 bits each.
+struct SpCell {
+  int d0, d1, d2, n1, n2, n3;
+};
+__device__ __forceinline__ uint32_t sp_pack_d(int d0, int d1) {
+  return (uint32_t)(d0 + 32768) | ((uint32_t)(d1 + 32768) << 16);
+}
+__device__ __forceinline__ uint16_t sp_pack_n(int d2, int n1, int n2, int n3) {
+  return (uint16_t)((uint32_t)(d2 + 4) | ((uint32_t)(n1 + 4) << 3) | ((uint32_t)(n2 + 4) << 6) |
+                    ((uint32_t)(n3 + 4) << 9));
+}
+__device__ __forceinline__ SpCell sp_unpack(uint32_t pd, uint32_t pn) {
+  SpCell c;
+  c.d0 = (int)(pd & 0xffffu) - 32768;
+  c.d1 = (int)(pd >> 16) - 32768;
+  c.d2 = (int)(pn & 7u) - 4;
+  c.n1 = (int)((pn >> 3) & 7u) - 4;
+  c.n2 = (int)((pn >> 6) & 7u) - 4;
+  c.n3 = (int)((pn >> 9) & 7u) - 4;
+  return c;
+}
+
+// fp64 bracket of a neighbour cell relative to i's cell (build_entries' formulas): DS R (delta / c);
+// DO (d0 w0 + n1 e0 + n2 r12 + n3 r13, d1 w1 + n2 e1 + n3 r23, d2 w2 + n3 e2)
+__device__ __forceinline__ void sp_bracket(const Geom& g, const SpCell& c, double& bx, double& by, double& bz) {
+  if (g.variant == 0) {
+    const double u0 = (double)c.d0 * g.cinv[0], u1 = (double)c.d1 * g.cinv[1], u2 = (double)c.d2 * g.cinv[2];
+    bx = g.R[0] * u0 + g.R[1] * u1 + g.R[2] * u2;
+    by = g.R[4] * u1 + g.R[5] * u2;
+    bz = g.R[8] * u2;
+  } else {
+    bx = (double)c.d0 * g.w[0] + (double)c.n1 * g.e[0] + (double)c.n2 * g.R[1] + (double)c.n3 * g.R[2];
+    by = (double)c.d1 * g.w[1] + (double)c.n2 * g.e[1] + (double)c.n3 * g.R[5];
+    bz = (double)c.d2 * g.w[2] + (double)c.n3 * g.e[2];
+  }
+}
+
+// fp64 evaluation of this thread's queued candidates (two per iteration, loads first)
+template <bool DIGEST>
+__device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4* __restrict__ u,
+                                        const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
+                                        const uint32_t* __restrict__ gid, int nq, int tid, uint32_t me, uint32_t nh_i,
+                                        double uix, double uiy, double uiz, double lo64, double hi64, Acc& acc,
+                                        const PairOut& po, uint32_t gi) {
+  const int lane = tid & 31;
+  const int qmax = __reduce_max_sync(0xffffffffu, nq);
+  const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
+  for (int k0 = 0; k0 < qmax; k0 += 2) {
+    uint32_t jj[2];
+    SpCell cc[2];
+    bool ok0[2];
+    double4 uj[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      ok0[h] = k0 + h < nq;
+      jj[h] = ok0[h] ? sm.qj[k0 + h][tid] : me;
+      cc[h] = sp_unpack(ok0[h] ? sm.qd[k0 + h][tid] : sp_pack_d(0, 0), ok0[h] ? sm.qn[k0 + h][tid] : sp_pack_n(0, 0, 0, 0));
+      uj[h] = u[jj[h]];
+    }
+    (void)lane;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double bx, by, bz;
+      sp_bracket(g, cc[h], bx, by, bz);
+      const double dx = (uj[h].x + bx) - uix, dy = (uj[h].y + by) - uiy, dz = (uj[h].z + bz) - uiz;
+      const double r2 = dx * dx + dy * dy + dz * dz;
+      bool ok = ok0[h] && (jj[h] != me) && (r2 < hi64);
+      int n0 = 0, n1 = 0, n2 = 0;
+      if (ok && (DIGEST || r2 >= lo64)) {
+        n0 = cc[h].n1;
+        n1 = cc[h].n2;
+        n2 = cc[h].n3;
+        if (g.variant == 1) {
+          const uint32_t nh_j = nh[jj[h]];
+          n0 += nh_x(nh_j) - nh_x(nh_i);
+          n1 += nh_y(nh_j) - nh_y(nh_i);
+        }
+        if (r2 >= lo64) {
+          const float4 qi = qs[me], qj = qs[jj[h]];
+          ok = canonical_r2(g, (double)qj.x, (double)qj.y, (double)qj.z, (double)qi.x, (double)qi.y, (double)qi.z, n0,
+                            n1, n2) < g.rc2;
+          acc.nrc++;
+        }
+      }
+      const double ir = rcp64(r2);
+      const double s2 = sig2 * ir;
+      const double s6 = s2 * s2 * s2;
+      double fr = (eps24 * s6) * (2.0 * s6 - 1.0) * ir;
+      fr = ok ? fr : 0.0;
+      const double tx = fr * dx, ty = fr * dy, tz = fr * dz;
+      acc.fx -= tx; acc.fy -= ty; acc.fz -= tz;
+      acc.u += ok ? s6 * s6 - s6 : 0.0;
+      acc.w0 += tx * dx; acc.w1 += ty * dy; acc.w2 += tz * dz;
+      acc.w3 += tx * dy; acc.w4 += tx * dz; acc.w5 += ty * dz;
+      acc.cnt += ok ? 1u : 0u;
+      if (DIGEST && ok) digest_add<DIGEST>(acc, gid, jj[h], n0, n1, n2, po, gi);
+    }
+  }
+  __syncwarp();
+}
+
+// grid = nlay layers x bpl blocks; block b of layer L takes the layer's particles
+// [b SP_NT, (b+1) SP_NT) + k bpl SP_NT, k = 0, 1, ... (a fixed partition of the layer).  The cells of
+// the layer are walked the same way for the stencil-size statistic (empty cells included).
+template <bool DIGEST>
+__global__ void __launch_bounds__(SP_NT, 4)
+k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
+               const uint32_t* __restrict__ ckey, const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
+               const uint32_t* __restrict__ gid, float4* __restrict__ Fout, double* __restrict__ bpart,
+               uint32_t* __restrict__ dcnt, uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx,
+               const __grid_constant__ Geom g, int bpl, int layer0, const PairOut po) {
+  __shared__ SpSmem sm;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int l1 = g.dims[0], l2 = g.dims[1];
+  const int layer = layer0 + (int)(blockIdx.x / bpl);
+  const int b = (int)blockIdx.x - (layer - layer0) * bpl;
+  const uint32_t per_layer = (uint32_t)l1 * (uint32_t)l2;
+  const uint32_t cell0 = per_layer * (uint32_t)layer;
+  const uint32_t P0 = cs[cell0], P1 = cs[cell0 + per_layer];
+  const double lo64 = g.rc2 * (1.0 - K3_BAND64), hi64 = g.rc2 * (1.0 + K3_BAND64);
+  const float hi32 = (float)g.band_hi;
+  const float w0x = (float)(g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0]);
+  double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+
+  // stencil sizes of the layer's cells (empty ones included): the neighborhood-size statistic
+  for (uint32_t c = (uint32_t)b * SP_NT + tid; c < per_layer; c += (uint32_t)bpl * SP_NT) {
+    const int a0 = (int)(c % (uint32_t)l1), a1 = (int)(c / (uint32_t)l1);
+    int ns = 0;
+    for (int ri = 0; ri < 12; ++ri) {
+      SpRow r;
+      if (sp_row(g, ri, a0, a1, layer, r)) ns += r.c1 - r.c0;
+    }
+    tS += (double)(ns - g.dbg_drop);
+  }
+
+  for (uint32_t base = P0 + (uint32_t)b * SP_NT; base < P1; base += (uint32_t)bpl * SP_NT) {
+    const uint32_t i = base + (uint32_t)tid;
+    const bool act = i < P1;
+    const uint32_t me = act ? i : P0;
+    const uint32_t c = ckey[me];
+    const int a0 = (int)(c % (uint32_t)l1), a1 = (int)((c / (uint32_t)l1) % (uint32_t)l2);
+    const float4 ui32 = u32[me];
+    const double4 ui = u[me];
+    const uint32_t nh_i = (g.variant == 1) ? nh[me] : 0u;
+    const uint32_t gi = DIGEST ? gid[me] : 0u;
+    Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+    int nq = 0;
+    uint32_t ncand = 0;
+    // the last neighborhood entry is dropped in the negative-control mode (nc_debug): the last
+    // column of the last existing row
+    int last_ri = 0;
+    if (g.dbg_drop)
+      for (int ri = 0; ri < 12; ++ri) {
+        SpRow r;
+        if (sp_row(g, ri, a0, a1, layer, r)) last_ri = ri;
+      }
+    for (int ri = 0; ri < 12; ++ri) {
+      SpRow r = {a0, a0, 0, 0, 0, 0, 0u};
+      const bool has = act && sp_row(g, ri, a0, a1, layer, r);
+      if (!__any_sync(0xffffffffu, has)) continue;
+      if (!has) { r.c0 = r.c1 = a0; r.base = 0u; r.n2 = r.n3 = r.d1 = r.d2 = 0; }
+      const int c0 = r.c0;
+      const int c1 = (has && g.dbg_drop && ri == last_ri) ? r.c1 - 1 : r.c1;
+      // [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once: c1 - c0 <= 4 <= l1)
+      const int n1a = floordiv(c0, l1);
+      const int cut = (n1a + 1) * l1;            // first column of the next x image
+      const int ca1 = min(c1, cut);
+      const uint32_t pa0 = cs[r.base + (uint32_t)(c0 - n1a * l1)];
+      const uint32_t pa1 = cs[r.base + (uint32_t)(ca1 - n1a * l1)];
+      uint32_t pb0 = 0, pb1 = 0;
+      if (c1 > cut) {
+        pb0 = cs[r.base];
+        pb1 = cs[r.base + (uint32_t)(c1 - cut)];
+      }
+      const uint32_t la = pa1 - pa0, lb = pb1 - pb0;
+      ncand += la + lb;
+      // fp32 brackets of the two pieces' first columns (fp64, rounded once); per element only the
+      // small column step (col - first column) w0 is added
+      float bxa, bxb, byf, bzf;
+      {
+        double bx, by, bz;
+        sp_bracket(g, SpCell{c0 - a0, r.d1, r.d2, n1a, r.n2, r.n3}, bx, by, bz);
+        bxa = (float)bx;
+        byf = (float)by;
+        bzf = (float)bz;
+        sp_bracket(g, SpCell{cut - a0, r.d1, r.d2, n1a + 1, r.n2, r.n3}, bx, by, bz);
+        bxb = (float)bx;
+      }
+      const uint32_t pn_a = sp_pack_n(r.d2, n1a, r.n2, r.n3), pn_b = sp_pack_n(r.d2, n1a + 1, r.n2, r.n3);
+      const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
+      for (int k = 0; k < lmax; ++k) {
+        if (__any_sync(0xffffffffu, nq >= SP_QCAP)) {
+          sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
+          nq = 0;
+        }
+        const bool inb = (uint32_t)k >= la;
+        const uint32_t j = inb ? pb0 + ((uint32_t)k - la) : pa0 + (uint32_t)k;
+        const bool valid = (uint32_t)k < la + lb;
+        const float4 v = u32[valid ? j : me];
+        const int colw = __float_as_int(v.w);          // j's cell column (wrapped)
+        const int first = inb ? 0 : c0 - n1a * l1;     // the piece's first wrapped column
+        const float bx = (inb ? bxb : bxa) + (float)(colw - first) * w0x;
+        const float dx = (v.x + bx) - ui32.x, dy = (v.y + byf) - ui32.y, dz = (v.z + bzf) - ui32.z;
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const bool hit = valid && j != me && r2 < hi32;
+        if (hit) {
+          const int n1 = inb ? n1a + 1 : n1a;
+          sm.qj[nq][tid] = j;
+          sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, r.d1);
+          sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
+        }
+        nq += hit ? 1 : 0;
+      }
+    }
+    sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
+    if (act) {
+      const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
+      Fout[me] = make_float4((float)(g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz),
+                             (float)(g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz),
+                             (float)(g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz), __uint_as_float(acc.cnt));
+      if (DIGEST) { dcnt[me] = acc.cnt; dhs[me] = acc.hs; dhx[me] = acc.hx; }
+      tU += Ui;
+      tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
+      tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
+      tI += (double)acc.cnt;
+      tR += (double)acc.nrc;
+      tC += (double)ncand - 1.0;
+      tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0.0 : 1.0;
+    }
+  }
+  tU = warp_sum_d(tU);
+  tW[0] = warp_sum_d(tW[0]); tW[1] = warp_sum_d(tW[1]); tW[2] = warp_sum_d(tW[2]);
+  tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
+  tI = warp_sum_d(tI);
+  tC = warp_sum_d(tC);
+  tS = warp_sum_d(tS);
+  tR = warp_sum_d(tR);
+  tNF = warp_sum_d(tNF);
+  if (lane < NPART) {
+    double v = 0;
+    if (lane == 0) v = tU;
+    else if (lane <= 6) v = tW[lane - 1];
+    else if (lane == 7) v = tI;
+    else if (lane == 8) v = tC;
+    else if (lane == 9) v = tS;
+    else if (lane == 10) v = tR;
+    else if (lane == 11) v = 0.0;  // every interaction of this kernel is evaluated in fp64
+    else v = tNF;
+    sm.part[wid][lane] = v;
+  }
+  __syncthreads();
+  if (tid < NPART) {  // fixed-order combine of the warps
+    double v = 0.0;
+    for (int w = 0; w < SP_NT / 32; ++w) v += sm.part[w][tid];
+    bpart[(int64_t)blockIdx.x * NPART + tid] = v;
+  }
+}
+
+}  // namespace nc

@@ -34,8 +34,8 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_nccl_unique_id", "nc_slab_comm_init", "nc_slab_exchange_start", "nc_slab_exchange_wait",
            "nc_slab_exchange", "nc_slab_allgather", "nc_slab_layer_of"]
 NC_DBG_DROP_ENTRIES = 1
-NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT = 0, 1, 2
-PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT}
+NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE = 0, 1, 2, 3
+PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT, "sparse": NC_PK_SPARSE}
 KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
 
 
@@ -301,7 +301,7 @@ def nc_set_pair_kernel(ctx, which) -> None:
 
 
 def nc_pair_kernel_used(ctx) -> str:
-    return {0: "none", 1: "cell", 2: "segment"}[load().nc_pair_kernel_used(ctx)]
+    return {0: "none", 1: "cell", 2: "segment", 3: "sparse"}[load().nc_pair_kernel_used(ctx)]
 
 
 def nc_profile(ctx, enable) -> None:

@@ -97,30 +97,33 @@ def test_c1_shear(variant, prec):
     check_against_oracle(w, q, variant, prec)
 
 
-@pytest.mark.parametrize("kernel", ["cell", "segment"])
+@pytest.mark.parametrize("kernel", ["cell", "segment", "sparse"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
 def test_c1_both_pair_kernels(variant, kernel):
-    """Sparse WCA cells (C1, ~1.3 per cell): the warp-per-cell and the row-segment
-    pair kernels each reproduce the oracle's pair set and forces."""
+    """Sparse WCA cells (C1, ~1.3 per cell): the warp-per-cell, the row-segment and the
+    particle-per-thread pair kernels each reproduce the oracle's pair set and forces."""
     w, q = inputs(1, "f32")
     g, _ = check_against_oracle(w, q, variant, "f32", kernel=kernel)
     assert g["kernel"] == kernel
 
 
+@pytest.mark.parametrize("kernel", ["segment", "sparse"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
-def test_segment_kernel_on_dense_lj_cells(variant):
-    """The segment kernel forced onto dense LJ cells (~13 per cell): its staged
-    union overflows for long segments, so it must shrink segments down to one
-    cell and still match the oracle."""
+def test_segment_kernel_on_dense_lj_cells(variant, kernel):
+    """The sparse-cell kernels forced onto dense LJ cells (~13 per cell; the segment kernel's
+    staged union overflows for long segments and must shrink them, the particle-per-thread
+    kernel's queues flush often): both still match the oracle."""
     w, q = inputs(2, "f32", scale=2)
-    check_against_oracle(w, q, variant, "f32", kernel="segment")
+    check_against_oracle(w, q, variant, "f32", kernel=kernel)
 
 
-def test_segment_kernel_deterministic_and_equal_pair_set():
+@pytest.mark.parametrize("kernel", ["segment", "sparse"])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_segment_kernel_deterministic_and_equal_pair_set(kernel, variant):
     w, q = inputs(3, "f32", scale=2)
-    a = gpu_eval(w, q, "do", "f32", kernel="segment")
-    b = gpu_eval(w, q, "do", "f32", kernel="segment")
-    c = gpu_eval(w, q, "do", "f32", kernel="cell")
+    a = gpu_eval(w, q, variant, "f32", kernel=kernel)
+    b = gpu_eval(w, q, variant, "f32", kernel=kernel)
+    c = gpu_eval(w, q, variant, "f32", kernel="cell")
     assert np.array_equal(a["F"], b["F"]) and a["U"] == b["U"] and np.array_equal(a["W"], b["W"])
     for x, y in zip(a["dig"], c["dig"]):
         assert np.array_equal(x, y)
@@ -135,6 +138,8 @@ def test_pair_kernel_option_errors():
     cl = CellList("do", "f64", rc=2.5, capacity=16)
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel("segment")
+    with pytest.raises(NcError, match="NC_E_ARG"):
+        cl.pair_kernel("sparse")
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel(7)
     cl.close()
