@@ -369,8 +369,9 @@ nc_status nc_slab_allgather(nc_ctx *ctx, const double *local, int64_t nloc, int6
 /* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
  * kernel).  Both evaluate the same neighborhoods, the same
  * candidates and the same pair set; they differ in how work maps to warps:
- *  NC_PK_AUTO    (default) the row-segment kernel when the mean occupancy is below 4
- *                particles per cell (WCA at rho = 0.8442: ~1.3), else per cell;
+ *  NC_PK_AUTO    (default) per cell when the mean occupancy is at least 4 particles per
+ *                cell; below that (WCA at rho = 0.8442: ~1.3) per particle from 2^18
+ *                particles on, per row segment for smaller systems;
  *  NC_PK_CELL    one warp per center cell (k_pairs);
  *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
  *                union of their neighborhoods (k_pairs_seg, round 1), fp64 pair forces;

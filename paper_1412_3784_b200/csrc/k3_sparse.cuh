@@ -21,6 +21,13 @@ namespace nc {
 
 constexpr int SP_NT = 128;    // threads per block (one particle each per chunk)
 constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane could overflow)
+#ifndef NC_SP_UNR
+#define NC_SP_UNR 4
+#endif
+#ifndef NC_SP_MINB
+#define NC_SP_MINB 4
+#endif
+constexpr int SP_UNR = NC_SP_UNR;  // candidates per iteration (their loads in flight together)
 
 struct SpSmem {
   uint32_t qj[SP_QCAP][SP_NT];  // sorted index of a queued j
@@ -184,7 +191,7 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
 // [b SP_NT, (b+1) SP_NT) + k bpl SP_NT, k = 0, 1, ... (a fixed partition of the layer).  The cells of
 // the layer are walked the same way for the stencil-size statistic (empty cells included).
 template <bool DIGEST>
-__global__ void __launch_bounds__(SP_NT, 4)
+__global__ void __launch_bounds__(SP_NT, NC_SP_MINB)
 k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
                const uint32_t* __restrict__ ckey, const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                const uint32_t* __restrict__ gid, float4* __restrict__ Fout, double* __restrict__ bpart,
@@ -269,28 +276,38 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
       }
       const uint32_t pn_a = sp_pack_n(r.d2, n1a, r.n2, r.n3), pn_b = sp_pack_n(r.d2, n1a + 1, r.n2, r.n3);
       const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
-      for (int k = 0; k < lmax; ++k) {
-        if (__any_sync(0xffffffffu, nq >= SP_QCAP)) {
+      const int firsta = c0 - n1a * l1;  // piece a's first wrapped column (piece b starts at column 0)
+      for (int k0 = 0; k0 < lmax; k0 += SP_UNR) {
+        if (__any_sync(0xffffffffu, nq > SP_QCAP - SP_UNR)) {
           sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
           nq = 0;
         }
-        const bool inb = (uint32_t)k >= la;
-        const uint32_t j = inb ? pb0 + ((uint32_t)k - la) : pa0 + (uint32_t)k;
-        const bool valid = (uint32_t)k < la + lb;
-        const float4 v = u32[valid ? j : me];
-        const int colw = __float_as_int(v.w);          // j's cell column (wrapped)
-        const int first = inb ? 0 : c0 - n1a * l1;     // the piece's first wrapped column
-        const float bx = (inb ? bxb : bxa) + (float)(colw - first) * w0x;
-        const float dx = (v.x + bx) - ui32.x, dy = (v.y + byf) - ui32.y, dz = (v.z + bzf) - ui32.z;
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-        const bool hit = valid && j != me && r2 < hi32;
-        if (hit) {
-          const int n1 = inb ? n1a + 1 : n1a;
-          sm.qj[nq][tid] = j;
-          sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, r.d1);
-          sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
+        float4 v[SP_UNR];
+        uint32_t jv[SP_UNR];
+#pragma unroll
+        for (int h = 0; h < SP_UNR; ++h) {  // SP_UNR loads in flight before the first use
+          const uint32_t k = (uint32_t)(k0 + h);
+          jv[h] = k >= la ? pb0 + (k - la) : pa0 + k;
+          v[h] = u32[k < la + lb ? jv[h] : me];
         }
-        nq += hit ? 1 : 0;
+#pragma unroll
+        for (int h = 0; h < SP_UNR; ++h) {
+          const uint32_t k = (uint32_t)(k0 + h);
+          const bool inb = k >= la;
+          const bool valid = k < la + lb;
+          const int colw = __float_as_int(v[h].w);  // j's cell column (wrapped)
+          const float bx = (inb ? bxb : bxa) + (float)(colw - (inb ? 0 : firsta)) * w0x;
+          const float dx = (v[h].x + bx) - ui32.x, dy = (v[h].y + byf) - ui32.y, dz = (v[h].z + bzf) - ui32.z;
+          const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+          const bool hit = valid && jv[h] != me && r2 < hi32;
+          if (hit) {
+            const int n1 = inb ? n1a + 1 : n1a;
+            sm.qj[nq][tid] = jv[h];
+            sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, r.d1);
+            sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
+          }
+          nq += hit ? 1 : 0;
+        }
       }
     }
     sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
