@@ -27,13 +27,19 @@ constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane co
 #ifndef NC_SP_MINB
 #define NC_SP_MINB 4
 #endif
-constexpr int SP_UNR = NC_SP_UNR;  // candidates per iteration (their loads in flight together)
+constexpr int SP_UNR = NC_SP_UNR;
+constexpr int SP_CPB = 96;    // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
 
 struct SpSmem {
   uint32_t qj[SP_QCAP][SP_NT];  // sorted index of a queued j
   uint32_t qd[SP_QCAP][SP_NT];  // its neighbour cell's unwrapped deltas: column (low 16 bits), row (high)
   uint16_t qn[SP_QCAP][SP_NT];  // layer delta and image shifts (3 bits each, +4): d2, n1, n2, n3
   double part[SP_NT / 32][NPART];
+  struct RowW {           // the a0-independent part of a stencil row (sp_row_inv), per warp and cell row
+    double ox, bxr;       // DO x offset of the row (DS: 0); the row's part of the fp64 x bracket
+    float byf, bzf;       // fp32 y, z brackets
+    uint32_t base, meta;  // first cell id of the row; exists | d1 | n2 | n3 | d2 (sp_meta)
+  } rw[SP_NT / 32][2][12];
 };
 
 // row ri of cell (a0, a1, a2)'s neighborhood: columns [c0, c1) (unwrapped), row image shifts and the
@@ -81,6 +87,46 @@ __device__ __forceinline__ bool sp_row(const Geom& g, int ri, int a0, int a1, in
   r.d2 = dz;
   r.base = (uint32_t)l1 * ((uint32_t)jd + (uint32_t)l2 * (uint32_t)kd);
   return true;
+}
+
+// The part of row ri of the cells (*, a1, a2) that does not depend on the column a0 (lanes of a warp
+// share it: 32 consecutive particles sit in one or two cell rows).  With it, sp_row's columns are
+// c0 = floor(fl(a0 - 1 - ox)), c1 = ceil(fl(a0 + 2 - ox)) -- the same fp64 expressions (DS: ox = 0).
+__device__ __forceinline__ uint32_t sp_meta(bool ex, int d1, int n2, int n3, int d2) {
+  return (ex ? 1u : 0u) | ((uint32_t)(d1 + 32768) << 1) | ((uint32_t)(n2 + 8) << 17) | ((uint32_t)(n3 + 8) << 21) |
+         ((uint32_t)(d2 + 2) << 25);
+}
+__device__ __forceinline__ void sp_row_inv(const Geom& g, int ri, int a1, int a2, SpSmem::RowW& w) {
+  const int l1 = g.dims[0], l2 = g.dims[1], l3 = g.dims[2];
+  if (g.variant == 0) {
+    const int d1 = ri % 3 - 1, d2 = ri / 3 - 1;
+    const int m1 = a1 + d1, m2 = a2 + d2;
+    const int n1 = floordiv(m1, l2), n2 = floordiv(m2, l3);
+    const double u1 = (double)d1 * g.cinv[1], u2 = (double)d2 * g.cinv[2];
+    w.ox = 0.0;
+    w.bxr = g.R[1] * u1 + g.R[2] * u2;
+    w.byf = (float)(g.R[4] * u1 + g.R[5] * u2);
+    w.bzf = (float)(g.R[8] * u2);
+    w.base = (uint32_t)l1 * ((uint32_t)(m1 - n1 * l2) + (uint32_t)l2 * (uint32_t)(m2 - n2 * l3));
+    w.meta = sp_meta(ri < 9, d1, n1, n2, d2);
+    return;
+  }
+  const int dz = ri / 4 - 1, rr = ri % 4;
+  const int kk = a2 + dz;
+  const int n3 = floordiv(kk, l3);
+  const int kd = kk - n3 * l3;
+  const double oy = __dmul_rn((double)n3, g.d32);
+  const int m0 = (int)floor(__dsub_rn((double)(a1 - 1), oy));
+  const int m1 = (int)ceil(__dsub_rn((double)(a1 + 2), oy));
+  const int m = m0 + rr;
+  const int n2 = floordiv(m, l2);
+  const int jd = m - n2 * l2;
+  w.ox = __dadd_rn(__dmul_rn((double)n3, g.d31), __dmul_rn((double)n2, g.d21));
+  w.bxr = (double)n2 * g.R[1] + (double)n3 * g.R[2];
+  w.byf = (float)((double)(m - a1) * g.w[1] + (double)n2 * g.e[1] + (double)n3 * g.R[5]);
+  w.bzf = (float)((double)dz * g.w[2] + (double)n3 * g.e[2]);
+  w.base = (uint32_t)l1 * ((uint32_t)jd + (uint32_t)l2 * (uint32_t)kd);
+  w.meta = sp_meta(rr < m1 - m0, m - a1, n2, n3, dz);
 }
 
 // A neighbour cell relative to i's cell: unwrapped deltas (d0 column, d1 row, d2 layer) and the
@@ -242,39 +288,50 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
         SpRow r;
         if (sp_row(g, ri, a0, a1, layer, r)) last_ri = ri;
       }
+    // the a0-independent row data of the warp's (at most) two cell rows, built once by lanes 0-11 / 16-27;
+    // a lane of a third cell row (tiny grids) builds its own
+    __syncwarp();  // the previous particle batch's readers are done
+    const int a1A = __shfl_sync(0xffffffffu, a1, 0), a1B = __shfl_sync(0xffffffffu, a1, 31);
+    if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
+    __syncwarp();
+    const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
     for (int ri = 0; ri < 12; ++ri) {
-      SpRow r = {a0, a0, 0, 0, 0, 0, 0u};
-      const bool has = act && sp_row(g, ri, a0, a1, layer, r);
+      SpSmem::RowW w;
+      if (grp >= 0) w = sm.rw[wid][grp][ri];
+      else sp_row_inv(g, ri, a1, layer, w);
+      bool has = act && (w.meta & 1u);
       if (!__any_sync(0xffffffffu, has)) continue;
-      if (!has) { r.c0 = r.c1 = a0; r.base = 0u; r.n2 = r.n3 = r.d1 = r.d2 = 0; }
-      const int c0 = r.c0;
-      const int c1 = (has && g.dbg_drop && ri == last_ri) ? r.c1 - 1 : r.c1;
+      const int d1 = (int)((w.meta >> 1) & 0xffffu) - 32768, rn2 = (int)((w.meta >> 17) & 15u) - 8,
+                rn3 = (int)((w.meta >> 21) & 15u) - 8, d2 = (int)((w.meta >> 25) & 3u) - 2;
+      int c0 = (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
+      int c1 = (int)ceil(__dsub_rn((double)(a0 + 2), w.ox));
+      if (!has) { c0 = c1 = a0; w.base = 0u; }
+      if (has && g.dbg_drop && ri == last_ri) c1 -= 1;
       // [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once: c1 - c0 <= 4 <= l1)
       const int n1a = floordiv(c0, l1);
       const int cut = (n1a + 1) * l1;            // first column of the next x image
       const int ca1 = min(c1, cut);
-      const uint32_t pa0 = cs[r.base + (uint32_t)(c0 - n1a * l1)];
-      const uint32_t pa1 = cs[r.base + (uint32_t)(ca1 - n1a * l1)];
+      const uint32_t pa0 = cs[w.base + (uint32_t)(c0 - n1a * l1)];
+      const uint32_t pa1 = cs[w.base + (uint32_t)(ca1 - n1a * l1)];
       uint32_t pb0 = 0, pb1 = 0;
       if (c1 > cut) {
-        pb0 = cs[r.base];
-        pb1 = cs[r.base + (uint32_t)(c1 - cut)];
+        pb0 = cs[w.base];
+        pb1 = cs[w.base + (uint32_t)(c1 - cut)];
       }
       const uint32_t la = pa1 - pa0, lb = pb1 - pb0;
       ncand += la + lb;
       // fp32 brackets of the two pieces' first columns (fp64, rounded once); per element only the
       // small column step (col - first column) w0 is added
-      float bxa, bxb, byf, bzf;
-      {
-        double bx, by, bz;
-        sp_bracket(g, SpCell{c0 - a0, r.d1, r.d2, n1a, r.n2, r.n3}, bx, by, bz);
-        bxa = (float)bx;
-        byf = (float)by;
-        bzf = (float)bz;
-        sp_bracket(g, SpCell{cut - a0, r.d1, r.d2, n1a + 1, r.n2, r.n3}, bx, by, bz);
-        bxb = (float)bx;
+      float bxa, bxb;
+      const float byf = w.byf, bzf = w.bzf;
+      if (g.variant == 0) {
+        bxa = (float)(g.R[0] * ((double)(c0 - a0) * g.cinv[0]) + w.bxr);
+        bxb = (float)(g.R[0] * ((double)(cut - a0) * g.cinv[0]) + w.bxr);
+      } else {
+        bxa = (float)(((double)(c0 - a0) * g.w[0] + (double)n1a * g.e[0]) + w.bxr);
+        bxb = (float)(((double)(cut - a0) * g.w[0] + (double)(n1a + 1) * g.e[0]) + w.bxr);
       }
-      const uint32_t pn_a = sp_pack_n(r.d2, n1a, r.n2, r.n3), pn_b = sp_pack_n(r.d2, n1a + 1, r.n2, r.n3);
+      const uint32_t pn_a = sp_pack_n(d2, n1a, rn2, rn3), pn_b = sp_pack_n(d2, n1a + 1, rn2, rn3);
       const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
       const int firsta = c0 - n1a * l1;  // piece a's first wrapped column (piece b starts at column 0)
       for (int k0 = 0; k0 < lmax; k0 += SP_UNR) {
@@ -303,7 +360,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
           if (hit) {
             const int n1 = inb ? n1a + 1 : n1a;
             sm.qj[nq][tid] = jv[h];
-            sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, r.d1);
+            sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, d1);
             sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
           }
           nq += hit ? 1 : 0;

@@ -385,7 +385,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   if constexpr (sizeof(T) == 4) {
     const int Gseg = sparse_kind(ctx, g) == 1 ? seg_cells(ctx, g) : 0;
     if (sparse_kind(ctx, g) == 2) {  // sparse cells: one thread per particle (k3_sparse.cuh)
-      bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + 31) / 32);  // 4 particles per cell per layer; more loop
+      bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + SP_CPB - 1) / SP_CPB);  // a function of the grid only (P-invariant)
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;

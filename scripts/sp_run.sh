@@ -1,4 +1,5 @@
-for c in 1 3; do for v in do ds; do for k in sparse segment; do
+# k_pairs_sparse vs k_pairs_seg on C1 / C3, DO and DS (pair-kernel ms by the library's event profile)
+for c in ${CONFIGS:-1 3}; do for v in do ds; do for k in ${KERNELS:-sparse segment}; do
 python - <<PY
 import sys, json, numpy as np, torch
 sys.path.insert(0,'.')
@@ -9,7 +10,7 @@ cl=CellList('$v','f32',rc=w.rc,u_shift=w.ushift,capacity=w.n); cl.pair_kernel('$
 qt=torch.from_numpy(q).cuda()
 for _ in range(3): cl.compute_forces(qt)
 cl.profile(True)
-for _ in range(10): cl.compute_forces(qt)
+for _ in range(20): cl.compute_forces(qt)
 p=cl.profile_read(); print('c$c $v $k pairs_ms %.4f' % (p['pairs'][0]/p['pairs'][1]))
 PY
 done; done; done
