@@ -35,6 +35,10 @@ struct SpSmem {
   uint32_t qd[SP_QCAP][SP_NT];  // its neighbour cell's unwrapped deltas: column (low 16 bits), row (high)
   uint16_t qn[SP_QCAP][SP_NT];  // layer delta and image shifts (3 bits each, +4): d2, n1, n2, n3
   double part[SP_NT / 32][NPART];
+  // per-thread accumulators (live only inside sp_eval: the registers go to the candidate loop)
+  double acc[10][SP_NT];
+  uint32_t cnt[SP_NT], nrc[SP_NT];
+  uint64_t hs[SP_NT], hx[SP_NT];
   struct RowW {           // the a0-independent part of a stencil row (sp_row_inv), per warp and cell row
     double ox, bxr;       // DO x offset of the row (DS: 0); the row's part of the fp64 x bracket
     float byf, bzf;       // fp32 y, z brackets
@@ -174,10 +178,18 @@ template <bool DIGEST>
 __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4* __restrict__ u,
                                         const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                                         const uint32_t* __restrict__ gid, int nq, int tid, uint32_t me, uint32_t nh_i,
-                                        double uix, double uiy, double uiz, double lo64, double hi64, Acc& acc,
-                                        const PairOut& po, uint32_t gi) {
+                                        double lo64, double hi64, const PairOut& po, uint32_t gi) {
   const int lane = tid & 31;
   const int qmax = __reduce_max_sync(0xffffffffu, nq);
+  if (qmax == 0) return;
+  const double4 ui = u[me];
+  const double uix = ui.x, uiy = ui.y, uiz = ui.z;
+  Acc acc;
+  acc.fx = sm.acc[0][tid]; acc.fy = sm.acc[1][tid]; acc.fz = sm.acc[2][tid]; acc.u = sm.acc[3][tid];
+  acc.w0 = sm.acc[4][tid]; acc.w1 = sm.acc[5][tid]; acc.w2 = sm.acc[6][tid];
+  acc.w3 = sm.acc[7][tid]; acc.w4 = sm.acc[8][tid]; acc.w5 = sm.acc[9][tid];
+  acc.cnt = sm.cnt[tid]; acc.nrc = sm.nrc[tid];
+  if (DIGEST) { acc.hs = sm.hs[tid]; acc.hx = sm.hx[tid]; }
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   for (int k0 = 0; k0 < qmax; k0 += 2) {
     uint32_t jj[2];
@@ -230,6 +242,11 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
       if (DIGEST && ok) digest_add<DIGEST>(acc, gid, jj[h], n0, n1, n2, po, gi);
     }
   }
+  sm.acc[0][tid] = acc.fx; sm.acc[1][tid] = acc.fy; sm.acc[2][tid] = acc.fz; sm.acc[3][tid] = acc.u;
+  sm.acc[4][tid] = acc.w0; sm.acc[5][tid] = acc.w1; sm.acc[6][tid] = acc.w2;
+  sm.acc[7][tid] = acc.w3; sm.acc[8][tid] = acc.w4; sm.acc[9][tid] = acc.w5;
+  sm.cnt[tid] = acc.cnt; sm.nrc[tid] = acc.nrc;
+  if (DIGEST) { sm.hs[tid] = acc.hs; sm.hx[tid] = acc.hx; }
   __syncwarp();
 }
 
@@ -256,15 +273,28 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
   const float w0x = (float)(g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0]);
   double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
 
-  // stencil sizes of the layer's cells (empty ones included): the neighborhood-size statistic
-  for (uint32_t c = (uint32_t)b * SP_NT + tid; c < per_layer; c += (uint32_t)bpl * SP_NT) {
-    const int a0 = (int)(c % (uint32_t)l1), a1 = (int)(c / (uint32_t)l1);
+  // stencil sizes of the layer's cells (empty ones included): the neighborhood-size statistic, from the
+  // warp's shared row data (a row of cells (a0, a1) has ceil(fl(a0 + 2 - ox)) - floor(fl(a0 - 1 - ox))
+  // columns, sp_row's expressions)
+  for (uint32_t cb = (uint32_t)b * SP_NT; cb < per_layer; cb += (uint32_t)bpl * SP_NT) {
+    const uint32_t c = cb + (uint32_t)tid;
+    const bool cv = c < per_layer;
+    const uint32_t cc = cv ? c : cb;
+    const int a0 = (int)(cc % (uint32_t)l1), a1 = (int)(cc / (uint32_t)l1);
+    const int a1A = __shfl_sync(0xffffffffu, a1, 0), a1B = __shfl_sync(0xffffffffu, a1, 31);
+    __syncwarp();
+    if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
+    __syncwarp();
+    const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
     int ns = 0;
     for (int ri = 0; ri < 12; ++ri) {
-      SpRow r;
-      if (sp_row(g, ri, a0, a1, layer, r)) ns += r.c1 - r.c0;
+      SpSmem::RowW w;
+      if (grp >= 0) w = sm.rw[wid][grp][ri];
+      else sp_row_inv(g, ri, a1, layer, w);
+      if (w.meta & 1u)
+        ns += (int)ceil(__dsub_rn((double)(a0 + 2), w.ox)) - (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
     }
-    tS += (double)(ns - g.dbg_drop);
+    if (cv) tS += (double)(ns - g.dbg_drop);
   }
 
   for (uint32_t base = P0 + (uint32_t)b * SP_NT; base < P1; base += (uint32_t)bpl * SP_NT) {
@@ -274,10 +304,12 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     const uint32_t c = ckey[me];
     const int a0 = (int)(c % (uint32_t)l1), a1 = (int)((c / (uint32_t)l1) % (uint32_t)l2);
     const float4 ui32 = u32[me];
-    const double4 ui = u[me];
     const uint32_t nh_i = (g.variant == 1) ? nh[me] : 0u;
     const uint32_t gi = DIGEST ? gid[me] : 0u;
-    Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0u, 0u, 0ull, 0ull};
+#pragma unroll
+    for (int f = 0; f < 10; ++f) sm.acc[f][tid] = 0.0;
+    sm.cnt[tid] = 0u; sm.nrc[tid] = 0u;
+    if (DIGEST) { sm.hs[tid] = 0ull; sm.hx[tid] = 0ull; }
     int nq = 0;
     uint32_t ncand = 0;
     // the last neighborhood entry is dropped in the negative-control mode (nc_debug): the last
@@ -295,29 +327,48 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
     __syncwarp();
     const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
-    for (int ri = 0; ri < 12; ++ri) {
-      SpSmem::RowW w;
+    // row header: columns [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once:
+    // c1 - c0 <= 4 <= l1) and the pieces' cell starts; the next row's loads are issued before the
+    // current row's candidates (one row ahead)
+    auto row_w = [&](int ri, SpSmem::RowW& w) {
       if (grp >= 0) w = sm.rw[wid][grp][ri];
       else sp_row_inv(g, ri, a1, layer, w);
-      bool has = act && (w.meta & 1u);
-      if (!__any_sync(0xffffffffu, has)) continue;
-      const int d1 = (int)((w.meta >> 1) & 0xffffu) - 32768, rn2 = (int)((w.meta >> 17) & 15u) - 8,
-                rn3 = (int)((w.meta >> 21) & 15u) - 8, d2 = (int)((w.meta >> 25) & 3u) - 2;
-      int c0 = (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
-      int c1 = (int)ceil(__dsub_rn((double)(a0 + 2), w.ox));
+    };
+    auto header = [&](int ri, bool& has, int& c0, int& c1, int& n1a, uint32_t& pa0, uint32_t& pa1, uint32_t& pb0,
+                      uint32_t& pb1) {
+      SpSmem::RowW w;
+      row_w(ri, w);
+      has = act && (w.meta & 1u);
+      c0 = (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
+      c1 = (int)ceil(__dsub_rn((double)(a0 + 2), w.ox));
       if (!has) { c0 = c1 = a0; w.base = 0u; }
       if (has && g.dbg_drop && ri == last_ri) c1 -= 1;
-      // [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once: c1 - c0 <= 4 <= l1)
-      const int n1a = floordiv(c0, l1);
-      const int cut = (n1a + 1) * l1;            // first column of the next x image
-      const int ca1 = min(c1, cut);
-      const uint32_t pa0 = cs[w.base + (uint32_t)(c0 - n1a * l1)];
-      const uint32_t pa1 = cs[w.base + (uint32_t)(ca1 - n1a * l1)];
-      uint32_t pb0 = 0, pb1 = 0;
+      n1a = floordiv(c0, l1);
+      const int cut = (n1a + 1) * l1;
+      pa0 = cs[w.base + (uint32_t)(c0 - n1a * l1)];
+      pa1 = cs[w.base + (uint32_t)(min(c1, cut) - n1a * l1)];
+      pb0 = pb1 = 0u;
       if (c1 > cut) {
         pb0 = cs[w.base];
         pb1 = cs[w.base + (uint32_t)(c1 - cut)];
       }
+    };
+    bool nhas;
+    int nc0, nc1, nn1a;
+    uint32_t npa0, npa1, npb0, npb1;
+    header(0, nhas, nc0, nc1, nn1a, npa0, npa1, npb0, npb1);
+    for (int ri = 0; ri < 12; ++ri) {
+      const bool has = nhas;
+      const int c0 = nc0, n1a = nn1a;
+      const uint32_t pa0 = npa0, pa1 = npa1, pb0 = npb0, pb1 = npb1;
+      (void)nc1;
+      if (ri + 1 < 12) header(ri + 1, nhas, nc0, nc1, nn1a, npa0, npa1, npb0, npb1);
+      if (!__any_sync(0xffffffffu, has)) continue;
+      SpSmem::RowW w;
+      row_w(ri, w);
+      const int d1 = (int)((w.meta >> 1) & 0xffffu) - 32768, rn2 = (int)((w.meta >> 17) & 15u) - 8,
+                rn3 = (int)((w.meta >> 21) & 15u) - 8, d2 = (int)((w.meta >> 25) & 3u) - 2;
+      const int cut = (n1a + 1) * l1;            // first column of the next x image
       const uint32_t la = pa1 - pa0, lb = pb1 - pb0;
       ncand += la + lb;
       // fp32 brackets of the two pieces' first columns (fp64, rounded once); per element only the
@@ -333,10 +384,10 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
       }
       const uint32_t pn_a = sp_pack_n(d2, n1a, rn2, rn3), pn_b = sp_pack_n(d2, n1a + 1, rn2, rn3);
       const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
-      const int firsta = c0 - n1a * l1;  // piece a's first wrapped column (piece b starts at column 0)
+      const float firstaf = (float)(c0 - n1a * l1);  // piece a's first wrapped column (piece b: column 0)
       for (int k0 = 0; k0 < lmax; k0 += SP_UNR) {
         if (__any_sync(0xffffffffu, nq > SP_QCAP - SP_UNR)) {
-          sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
+          sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi);
           nq = 0;
         }
         float4 v[SP_UNR];
@@ -352,13 +403,14 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
           const uint32_t k = (uint32_t)(k0 + h);
           const bool inb = k >= la;
           const bool valid = k < la + lb;
-          const int colw = __float_as_int(v[h].w);  // j's cell column (wrapped)
-          const float bx = (inb ? bxb : bxa) + (float)(colw - (inb ? 0 : firsta)) * w0x;
+          // j's cell column (wrapped; exact in .w) relative to its piece's first column, times w0
+          const float bx = fmaf(v[h].w - (inb ? 0.0f : firstaf), w0x, inb ? bxb : bxa);
           const float dx = (v[h].x + bx) - ui32.x, dy = (v[h].y + byf) - ui32.y, dz = (v[h].z + bzf) - ui32.z;
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           const bool hit = valid && jv[h] != me && r2 < hi32;
           if (hit) {
             const int n1 = inb ? n1a + 1 : n1a;
+            const int colw = (int)v[h].w;
             sm.qj[nq][tid] = jv[h];
             sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, d1);
             sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
@@ -367,7 +419,13 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
         }
       }
     }
-    sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, ui.x, ui.y, ui.z, lo64, hi64, acc, po, gi);
+    sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi);
+    Acc acc;
+    acc.fx = sm.acc[0][tid]; acc.fy = sm.acc[1][tid]; acc.fz = sm.acc[2][tid]; acc.u = sm.acc[3][tid];
+    acc.w0 = sm.acc[4][tid]; acc.w1 = sm.acc[5][tid]; acc.w2 = sm.acc[6][tid];
+    acc.w3 = sm.acc[7][tid]; acc.w4 = sm.acc[8][tid]; acc.w5 = sm.acc[9][tid];
+    acc.cnt = sm.cnt[tid]; acc.nrc = sm.nrc[tid];
+    if (DIGEST) { acc.hs = sm.hs[tid]; acc.hx = sm.hx[tid]; }
     if (act) {
       const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
       Fout[me] = make_float4((float)(g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz),
@@ -383,31 +441,27 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
       tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0.0 : 1.0;
     }
   }
-  tU = warp_sum_d(tU);
-  tW[0] = warp_sum_d(tW[0]); tW[1] = warp_sum_d(tW[1]); tW[2] = warp_sum_d(tW[2]);
-  tW[3] = warp_sum_d(tW[3]); tW[4] = warp_sum_d(tW[4]); tW[5] = warp_sum_d(tW[5]);
-  tI = warp_sum_d(tI);
-  tC = warp_sum_d(tC);
-  tS = warp_sum_d(tS);
-  tR = warp_sum_d(tR);
-  tNF = warp_sum_d(tNF);
-  if (lane < NPART) {
-    double v = 0;
-    if (lane == 0) v = tU;
-    else if (lane <= 6) v = tW[lane - 1];
-    else if (lane == 7) v = tI;
-    else if (lane == 8) v = tC;
-    else if (lane == 9) v = tS;
-    else if (lane == 10) v = tR;
-    else if (lane == 11) v = 0.0;  // every interaction of this kernel is evaluated in fp64
-    else v = tNF;
-    sm.part[wid][lane] = v;
+  // warp sums of the 13 partials by a transposing butterfly (16 slots: each step halves the slots a
+  // lane carries; 16 shuffles instead of 13 x 5); lane l ends with slot (l >> 1) & 15, fixed order
+  double v[16] = {tU, tW[0], tW[1], tW[2], tW[3], tW[4], tW[5], tI, tC, tS, tR, 0.0, tNF, 0.0, 0.0, 0.0};
+  // (slot 11: the fp32-tier count -- every interaction of this kernel is evaluated in fp64)
+#pragma unroll
+  for (int o = 16, m = 8; o >= 2; o >>= 1, m >>= 1) {
+    const bool hi = (lane & o) != 0;
+#pragma unroll
+    for (int k = 0; k < m; ++k) {
+      const double keep = hi ? v[k + m] : v[k], send = hi ? v[k] : v[k + m];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
   }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  static_assert(NPART == 13, "slot layout");
+  if ((lane & 1) == 0 && (lane >> 1) < NPART) sm.part[wid][lane >> 1] = v[0];
   __syncthreads();
   if (tid < NPART) {  // fixed-order combine of the warps
-    double v = 0.0;
-    for (int w = 0; w < SP_NT / 32; ++w) v += sm.part[w][tid];
-    bpart[(int64_t)blockIdx.x * NPART + tid] = v;
+    double sum = 0.0;
+    for (int w = 0; w < SP_NT / 32; ++w) sum += sm.part[w][tid];
+    bpart[(int64_t)blockIdx.x * NPART + tid] = sum;
   }
 }
 

@@ -386,7 +386,7 @@ k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __res
   if (p_in) p_out[dst] = p_in[i];
   gid_out[dst] = gg;
   u_out[dst] = make_double4(u[0], u[1], u[2], (double)dst);
-  u32_out[dst] = make_float4((float)u[0], (float)u[1], (float)u[2], __int_as_float(cp.a[0]));  // .w: cell column
+  u32_out[dst] = make_float4((float)u[0], (float)u[1], (float)u[2], (float)cp.a[0]);  // .w: cell column (exact)
   nh_out[dst] = pack_nh(cp.nh0, cp.nh1);
   if (idx_out) idx_out[dst] = i;
 }
