@@ -28,12 +28,12 @@ constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane co
 #define NC_SP_MINB 4
 #endif
 constexpr int SP_UNR = NC_SP_UNR;
+constexpr int SP_QD = SP_QCAP * SP_NT * 4;  // byte offset of qd from qj
 constexpr int SP_CPB = 96;    // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
 
 struct SpSmem {
   uint32_t qj[SP_QCAP][SP_NT];  // sorted index of a queued j
-  uint32_t qd[SP_QCAP][SP_NT];  // its neighbour cell's unwrapped deltas: column (low 16 bits), row (high)
-  uint16_t qn[SP_QCAP][SP_NT];  // layer delta and image shifts (3 bits each, +4): d2, n1, n2, n3
+  uint32_t qd[SP_QCAP][SP_NT];  // its neighbour cell: unwrapped column delta d0 + 32768 | stencil row << 16
   double part[SP_NT / 32][NPART];
   // per-thread accumulators (live only inside sp_eval: the registers go to the candidate loop)
   double acc[10][SP_NT];
@@ -135,28 +135,11 @@ __device__ __forceinline__ void sp_row_inv(const Geom& g, int ri, int a1, int a2
 
 // A neighbour cell relative to i's cell: unwrapped deltas (d0 column, d1 row, d2 layer) and the
 // lattice image n (DO: the column's x shift n1 and the row's n2, n3; DS: the x, y, z wraps).  The
-// column / row deltas can be large in DO (the rows of the offset faces sit ~n2 d21 cells away), so
-// they take 16 bits each; the rest 3 bits each.
+// column / row deltas can be large in DO (the rows of the offset faces sit ~n2 d21 cells away): a
+// queued hit carries d0 in 16 bits and its stencil row; the rest comes from the row data (sp_meta).
 struct SpCell {
   int d0, d1, d2, n1, n2, n3;
 };
-__device__ __forceinline__ uint32_t sp_pack_d(int d0, int d1) {
-  return (uint32_t)(d0 + 32768) | ((uint32_t)(d1 + 32768) << 16);
-}
-__device__ __forceinline__ uint16_t sp_pack_n(int d2, int n1, int n2, int n3) {
-  return (uint16_t)((uint32_t)(d2 + 4) | ((uint32_t)(n1 + 4) << 3) | ((uint32_t)(n2 + 4) << 6) |
-                    ((uint32_t)(n3 + 4) << 9));
-}
-__device__ __forceinline__ SpCell sp_unpack(uint32_t pd, uint32_t pn) {
-  SpCell c;
-  c.d0 = (int)(pd & 0xffffu) - 32768;
-  c.d1 = (int)(pd >> 16) - 32768;
-  c.d2 = (int)(pn & 7u) - 4;
-  c.n1 = (int)((pn >> 3) & 7u) - 4;
-  c.n2 = (int)((pn >> 6) & 7u) - 4;
-  c.n3 = (int)((pn >> 9) & 7u) - 4;
-  return c;
-}
 
 // fp64 bracket of a neighbour cell relative to i's cell (build_entries' formulas): DS R (delta / c);
 // DO (d0 w0 + n1 e0 + n2 r12 + n3 r13, d1 w1 + n2 e1 + n3 r23, d2 w2 + n3 e2)
@@ -178,7 +161,8 @@ template <bool DIGEST>
 __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4* __restrict__ u,
                                         const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                                         const uint32_t* __restrict__ gid, int nq, int tid, uint32_t me, uint32_t nh_i,
-                                        double lo64, double hi64, const PairOut& po, uint32_t gi) {
+                                        double lo64, double hi64, const PairOut& po, uint32_t gi, int a0, int a1,
+                                        int grp, int wid, int layer) {
   const int lane = tid & 31;
   const int qmax = __reduce_max_sync(0xffffffffu, nq);
   if (qmax == 0) return;
@@ -200,7 +184,19 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
     for (int h = 0; h < 2; ++h) {
       ok0[h] = k0 + h < nq;
       jj[h] = ok0[h] ? sm.qj[k0 + h][tid] : me;
-      cc[h] = sp_unpack(ok0[h] ? sm.qd[k0 + h][tid] : sp_pack_d(0, 0), ok0[h] ? sm.qn[k0 + h][tid] : sp_pack_n(0, 0, 0, 0));
+      // the queue code: unwrapped column delta d0 and the stencil row; the row's deltas and image
+      // shifts from the warp's row data; the column's x image from the unwrapped column a0 + d0
+      const uint32_t code = ok0[h] ? sm.qd[k0 + h][tid] : 32768u;
+      const int ri = (int)(code >> 16);
+      uint32_t meta;
+      if (grp >= 0) meta = sm.rw[wid][grp][ri].meta;
+      else { SpSmem::RowW w; sp_row_inv(g, ri, a1, layer, w); meta = w.meta; }
+      cc[h].d0 = (int)(code & 0xffffu) - 32768;
+      cc[h].d1 = (int)((meta >> 1) & 0xffffu) - 32768;
+      cc[h].n2 = (int)((meta >> 17) & 15u) - 8;
+      cc[h].n3 = (int)((meta >> 21) & 15u) - 8;
+      cc[h].d2 = (int)((meta >> 25) & 3u) - 2;
+      cc[h].n1 = floordiv(a0 + cc[h].d0, g.dims[0]);
       uj[h] = u[jj[h]];
     }
     (void)lane;
@@ -327,68 +323,57 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
     __syncwarp();
     const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
-    // row header: columns [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once:
-    // c1 - c0 <= 4 <= l1) and the pieces' cell starts; the next row's loads are issued before the
-    // current row's candidates (one row ahead)
-    auto row_w = [&](int ri, SpSmem::RowW& w) {
+    // queue slot addresses of this thread: qj[k][tid] at qa0 + 512 k, qd[k][tid] SP_QD bytes further
+    const uint32_t qa0 = smem_u32(&sm.qj[0][tid]);
+    uint32_t qa = qa0;
+    for (int ri = 0; ri < 12; ++ri) {
+      SpSmem::RowW w;
       if (grp >= 0) w = sm.rw[wid][grp][ri];
       else sp_row_inv(g, ri, a1, layer, w);
-    };
-    auto header = [&](int ri, bool& has, int& c0, int& c1, int& n1a, uint32_t& pa0, uint32_t& pa1, uint32_t& pb0,
-                      uint32_t& pb1) {
-      SpSmem::RowW w;
-      row_w(ri, w);
-      has = act && (w.meta & 1u);
-      c0 = (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
-      c1 = (int)ceil(__dsub_rn((double)(a0 + 2), w.ox));
+      const bool has = act && (w.meta & 1u);
+      if (!__any_sync(0xffffffffu, has)) continue;
+      // columns [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once:
+      // c1 - c0 <= 4 <= l1) and the pieces' cell starts
+      int c0 = (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
+      int c1 = (int)ceil(__dsub_rn((double)(a0 + 2), w.ox));
       if (!has) { c0 = c1 = a0; w.base = 0u; }
       if (has && g.dbg_drop && ri == last_ri) c1 -= 1;
-      n1a = floordiv(c0, l1);
-      const int cut = (n1a + 1) * l1;
-      pa0 = cs[w.base + (uint32_t)(c0 - n1a * l1)];
-      pa1 = cs[w.base + (uint32_t)(min(c1, cut) - n1a * l1)];
-      pb0 = pb1 = 0u;
+      const int n1a = floordiv(c0, l1);
+      const int cut = (n1a + 1) * l1;            // first column of the next x image
+      const uint32_t pa0 = cs[w.base + (uint32_t)(c0 - n1a * l1)];
+      const uint32_t pa1 = cs[w.base + (uint32_t)(min(c1, cut) - n1a * l1)];
+      uint32_t pb0 = 0u, pb1 = 0u;
       if (c1 > cut) {
         pb0 = cs[w.base];
         pb1 = cs[w.base + (uint32_t)(c1 - cut)];
       }
-    };
-    bool nhas;
-    int nc0, nc1, nn1a;
-    uint32_t npa0, npa1, npb0, npb1;
-    header(0, nhas, nc0, nc1, nn1a, npa0, npa1, npb0, npb1);
-    for (int ri = 0; ri < 12; ++ri) {
-      const bool has = nhas;
-      const int c0 = nc0, n1a = nn1a;
-      const uint32_t pa0 = npa0, pa1 = npa1, pb0 = npb0, pb1 = npb1;
-      (void)nc1;
-      if (ri + 1 < 12) header(ri + 1, nhas, nc0, nc1, nn1a, npa0, npa1, npb0, npb1);
-      if (!__any_sync(0xffffffffu, has)) continue;
-      SpSmem::RowW w;
-      row_w(ri, w);
-      const int d1 = (int)((w.meta >> 1) & 0xffffu) - 32768, rn2 = (int)((w.meta >> 17) & 15u) - 8,
-                rn3 = (int)((w.meta >> 21) & 15u) - 8, d2 = (int)((w.meta >> 25) & 3u) - 2;
-      const int cut = (n1a + 1) * l1;            // first column of the next x image
       const uint32_t la = pa1 - pa0, lb = pb1 - pb0;
       ncand += la + lb;
-      // fp32 brackets of the two pieces' first columns (fp64, rounded once); per element only the
-      // small column step (col - first column) w0 is added
+      // fp32 brackets of the two pieces' first columns (fp64, rounded once; pinned in registers so the
+      // compiler does not re-derive them per candidate); per element only (column - first) w0 is added
       float bxa, bxb;
-      const float byf = w.byf, bzf = w.bzf;
-      if (g.variant == 0) {
-        bxa = (float)(g.R[0] * ((double)(c0 - a0) * g.cinv[0]) + w.bxr);
-        bxb = (float)(g.R[0] * ((double)(cut - a0) * g.cinv[0]) + w.bxr);
-      } else {
-        bxa = (float)(((double)(c0 - a0) * g.w[0] + (double)n1a * g.e[0]) + w.bxr);
-        bxb = (float)(((double)(cut - a0) * g.w[0] + (double)(n1a + 1) * g.e[0]) + w.bxr);
+      {
+        double xa, xb;
+        if (g.variant == 0) {
+          xa = g.R[0] * ((double)(c0 - a0) * g.cinv[0]) + w.bxr;
+          xb = g.R[0] * ((double)(cut - a0) * g.cinv[0]) + w.bxr;
+        } else {
+          xa = ((double)(c0 - a0) * g.w[0] + (double)n1a * g.e[0]) + w.bxr;
+          xb = ((double)(cut - a0) * g.w[0] + (double)(n1a + 1) * g.e[0]) + w.bxr;
+        }
+        asm volatile("mov.b32 %0, %1;" : "=f"(bxa) : "f"((float)xa));
+        asm volatile("mov.b32 %0, %1;" : "=f"(bxb) : "f"((float)xb));
       }
-      const uint32_t pn_a = sp_pack_n(d2, n1a, rn2, rn3), pn_b = sp_pack_n(d2, n1a + 1, rn2, rn3);
-      const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
+      const float byf = w.byf, bzf = w.bzf;
       const float firstaf = (float)(c0 - n1a * l1);  // piece a's first wrapped column (piece b: column 0)
+      // queue code of a hit: its unwrapped column delta d0 = column + n1 l1 - a0 (16 bits) and the row
+      const int ka = n1a * l1 - a0 + 32768 + (ri << 16), kb = ka + l1;
+      const int lmax = (int)__reduce_max_sync(0xffffffffu, la + lb);
       for (int k0 = 0; k0 < lmax; k0 += SP_UNR) {
         if (__any_sync(0xffffffffu, nq > SP_QCAP - SP_UNR)) {
-          sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi);
+          sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi, a0, a1, grp, wid, layer);
           nq = 0;
+          qa = qa0;
         }
         float4 v[SP_UNR];
         uint32_t jv[SP_UNR];
@@ -409,17 +394,15 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
           const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
           const bool hit = valid && jv[h] != me && r2 < hi32;
           if (hit) {
-            const int n1 = inb ? n1a + 1 : n1a;
-            const int colw = (int)v[h].w;
-            sm.qj[nq][tid] = jv[h];
-            sm.qd[nq][tid] = sp_pack_d(colw + n1 * l1 - a0, d1);
-            sm.qn[nq][tid] = (uint16_t)(inb ? pn_b : pn_a);
+            stsu(qa, jv[h]);
+            stsu(qa + SP_QD, (uint32_t)((int)v[h].w + (inb ? kb : ka)));
           }
+          qa += hit ? 512u : 0u;
           nq += hit ? 1 : 0;
         }
       }
     }
-    sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi);
+    sp_eval<DIGEST>(g, sm, u, qs, nh, gid, nq, tid, me, nh_i, lo64, hi64, po, gi, a0, a1, grp, wid, layer);
     Acc acc;
     acc.fx = sm.acc[0][tid]; acc.fy = sm.acc[1][tid]; acc.fz = sm.acc[2][tid]; acc.u = sm.acc[3][tid];
     acc.w0 = sm.acc[4][tid]; acc.w1 = sm.acc[5][tid]; acc.w2 = sm.acc[6][tid];
