@@ -37,6 +37,7 @@ struct SpSmem {
   double part[SP_NT / 32][NPART];
   // per-thread accumulators (live only inside sp_eval: the registers go to the candidate loop)
   double acc[10][SP_NT];
+  double tuw[7][SP_NT];   // per-thread block statistics U, W0..W5
   uint32_t cnt[SP_NT], nrc[SP_NT];
   uint64_t hs[SP_NT], hx[SP_NT];
   struct RowW {           // the a0-independent part of a stencil row (sp_row_inv), per warp and cell row
@@ -267,7 +268,11 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
   const double lo64 = g.rc2 * (1.0 - K3_BAND64), hi64 = g.rc2 * (1.0 + K3_BAND64);
   const float hi32 = (float)g.band_hi;
   const float w0x = (float)(g.variant == 0 ? g.R[0] * g.cinv[0] : g.w[0]);
-  double tU = 0, tW[6] = {0, 0, 0, 0, 0, 0}, tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
+  // block statistics: U and W per thread in shared memory (registers go to the candidate loop), counts
+  // as integers
+#pragma unroll
+  for (int f = 0; f < 7; ++f) sm.tuw[f][tid] = 0.0;
+  uint32_t tI = 0, tC = 0, tS = 0, tR = 0, tNF = 0;
 
   // stencil sizes of the layer's cells (empty ones included): the neighborhood-size statistic, from the
   // warp's shared row data (a row of cells (a0, a1) has ceil(fl(a0 + 2 - ox)) - floor(fl(a0 - 1 - ox))
@@ -290,7 +295,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
       if (w.meta & 1u)
         ns += (int)ceil(__dsub_rn((double)(a0 + 2), w.ox)) - (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
     }
-    if (cv) tS += (double)(ns - g.dbg_drop);
+    if (cv) tS += (uint32_t)(ns - g.dbg_drop);
   }
 
   for (uint32_t base = P0 + (uint32_t)b * SP_NT; base < P1; base += (uint32_t)bpl * SP_NT) {
@@ -415,18 +420,19 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
                              (float)(g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz),
                              (float)(g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz), __uint_as_float(acc.cnt));
       if (DIGEST) { dcnt[me] = acc.cnt; dhs[me] = acc.hs; dhx[me] = acc.hx; }
-      tU += Ui;
-      tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
-      tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
-      tI += (double)acc.cnt;
-      tR += (double)acc.nrc;
-      tC += (double)ncand - 1.0;
-      tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0.0 : 1.0;
+      sm.tuw[0][tid] += Ui;
+      sm.tuw[1][tid] += 0.5 * acc.w0; sm.tuw[2][tid] += 0.5 * acc.w1; sm.tuw[3][tid] += 0.5 * acc.w2;
+      sm.tuw[4][tid] += 0.5 * acc.w3; sm.tuw[5][tid] += 0.5 * acc.w4; sm.tuw[6][tid] += 0.5 * acc.w5;
+      tI += acc.cnt;
+      tR += acc.nrc;
+      tC += ncand - 1u;
+      tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0u : 1u;
     }
   }
   // warp sums of the 13 partials by a transposing butterfly (16 slots: each step halves the slots a
   // lane carries; 16 shuffles instead of 13 x 5); lane l ends with slot (l >> 1) & 15, fixed order
-  double v[16] = {tU, tW[0], tW[1], tW[2], tW[3], tW[4], tW[5], tI, tC, tS, tR, 0.0, tNF, 0.0, 0.0, 0.0};
+  double v[16] = {sm.tuw[0][tid], sm.tuw[1][tid], sm.tuw[2][tid], sm.tuw[3][tid], sm.tuw[4][tid], sm.tuw[5][tid],
+                  sm.tuw[6][tid], (double)tI, (double)tC, (double)tS, (double)tR, 0.0, (double)tNF, 0.0, 0.0, 0.0};
   // (slot 11: the fp32-tier count -- every interaction of this kernel is evaluated in fp64)
 #pragma unroll
   for (int o = 16, m = 8; o >= 2; o >>= 1, m >>= 1) {
