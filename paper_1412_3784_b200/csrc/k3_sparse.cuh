@@ -253,7 +253,7 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
 template <bool DIGEST>
 __global__ void __launch_bounds__(SP_NT, NC_SP_MINB)
 k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
-               const uint32_t* __restrict__ ckey, const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
+               const uint4* __restrict__ rec, const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
                const uint32_t* __restrict__ gid, float4* __restrict__ Fout, double* __restrict__ bpart,
                uint32_t* __restrict__ dcnt, uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx,
                const __grid_constant__ Geom g, int bpl, int layer0, const PairOut po) {
@@ -302,7 +302,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     const uint32_t i = base + (uint32_t)tid;
     const bool act = i < P1;
     const uint32_t me = act ? i : P0;
-    const uint32_t c = ckey[me];
+    const uint32_t c = rec[me].z;  // the cell of sorted slot me (bucket records: same cell order)
     const int a0 = (int)(c % (uint32_t)l1), a1 = (int)((c / (uint32_t)l1) % (uint32_t)l2);
     const float4 ui32 = u32[me];
     const uint32_t nh_i = (g.variant == 1) ? nh[me] : 0u;

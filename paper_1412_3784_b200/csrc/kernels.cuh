@@ -332,16 +332,15 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __r
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
 __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ cs, const uint32_t* __restrict__ gid_in,
-                          uint32_t* __restrict__ tmp, uint32_t* __restrict__ tmpgid, uint32_t* __restrict__ tmpkey,
-                          int64_t i0 = 0) {
-  // particles [i0, i0 + n) (a slab evaluation scatters its own and its halo particles separately)
+                          uint4* __restrict__ rec, int64_t i0 = 0) {
+  // particles [i0, i0 + n) (a slab evaluation scatters its own and its halo particles separately).
+  // One 16-byte record per particle (source index, gid, cell): a random-order input costs one sector
+  // per particle, not three; k_rank_gather reads the records in bucket order (coalesced)
   int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= i0 + n) return;
   const uint32_t c = key[i];
-  uint32_t pos = cs[c] + slot[i];
-  tmp[pos] = (uint32_t)i;
-  tmpgid[pos] = gid_in ? gid_in[i] : (uint32_t)i;
-  tmpkey[pos] = c;  // k_rank_gather reads the cell in bucket order (coalesced) instead of gathering key[i]
+  const uint32_t pos = cs[c] + slot[i];
+  rec[pos] = make_uint4((uint32_t)i, gid_in ? gid_in[i] : (uint32_t)i, c, 0u);
 }
 
 // cs[c] += b for c in [c0, c1): the own cells' starts after the halo particles that precede them
@@ -359,8 +358,7 @@ __global__ void k_add_range(uint32_t* __restrict__ cs, int64_t c0, int64_t c1, u
 // and the packed DO home shift.
 template <typename T>
 __global__ void __launch_bounds__(256, RG_MINB)
-k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ tmpgid,
-                              const uint32_t* __restrict__ tmpkey, const uint32_t* __restrict__ cs,
+k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restrict__ cs,
                               const typename V4<T>::t* __restrict__ qw, const typename V4<T>::t* __restrict__ p_in,
                               typename V4<T>::t* __restrict__ q_out, typename V4<T>::t* __restrict__ p_out,
                               uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
@@ -370,11 +368,12 @@ k_rank_gather(int64_t n, const uint32_t* __restrict__ tmp, const uint32_t* __res
   // bucket positions [s0, s0 + n) (a slab evaluation places own and halo particles in two phases)
   int64_t s = s0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= s0 + n) return;
-  const uint32_t i = tmp[s], c = tmpkey[s], gg = tmpgid[s];
+  const uint4 r = rec[s];
+  const uint32_t i = r.x, gg = r.y, c = r.z;
   const typename V4<T>::t q = qw[i];  // gathers issued before the rank loop
   const uint32_t c0 = cs[c], c1 = cs[c + 1];
   uint32_t rank = 0;
-  for (uint32_t t = c0; t < c1; ++t) rank += (tmpgid[t] < gg) ? 1u : 0u;
+  for (uint32_t t = c0; t < c1; ++t) rank += (rec[t].y < gg) ? 1u : 0u;
   uint32_t dst = c0 + rank;
   double lam[3];
   frac_c(g, (double)q.x, (double)q.y, (double)q.z, lam);

@@ -49,8 +49,9 @@ struct nc_ctx {
 
   // shared transient
   double4* u = nullptr;   // sorted cell-local rotated coords, fp64 (w = sorted index)
-  float4* u32 = nullptr;  // the same in fp32 (w = sorted index bits): the filter's staging source
-  uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr, *tmp = nullptr, *tmpgid = nullptr, *tmpkey = nullptr;
+  float4* u32 = nullptr;  // the same in fp32 (w = the cell column, exact): the filter's staging source
+  uint32_t *nh = nullptr, *key = nullptr, *slot = nullptr;
+  uint4* srec = nullptr;  // bucket records (source index, gid, cell key) of the counting sort
   uint32_t *counts = nullptr, *cs = nullptr, *bsum = nullptr, *tot = nullptr;
   // slab (multi-GPU) scratch
   uint32_t *gin = nullptr, *sidx = nullptr, *pbcnt = nullptr, *pboff = nullptr, *ptot = nullptr;
@@ -350,11 +351,11 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
   }
   if (n > 0) {
     prof_begin(ctx);
-    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, gid_in, ctx->tmp, ctx->tmpgid, ctx->tmpkey);
+    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, gid_in, ctx->srec);
     LAUNCHED();
     prof_end(ctx, NC_K_SCATTER);
     prof_begin(ctx);
-    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, qwrap, p_in, q_out,
+    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->srec, ctx->cs, qwrap, p_in, q_out,
                                                   p_out, gid_out, ctx->u, ctx->u32, ctx->nh, g);
     LAUNCHED();
     prof_end(ctx, NC_K_RANKGATHER);
@@ -389,7 +390,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      k_pairs_sparse<DIGEST><<<nblocks, SP_NT, 0, s>>>(ctx->u, ctx->u32, ctx->cs, ctx->tmpkey, (const float4*)qs,
+      k_pairs_sparse<DIGEST><<<nblocks, SP_NT, 0, s>>>(ctx->u, ctx->u32, ctx->cs, ctx->srec, (const float4*)qs,
                                                         ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx,
                                                         g, bpl, layer0, po);
     } else if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
@@ -664,11 +665,11 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
     }
     if (n > 0) {
       prof_begin(ctx);
-      k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->st_gid[c], ctx->tmp, ctx->tmpgid, ctx->tmpkey);
+      k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->st_gid[c], ctx->srec);
       LAUNCHED();
       prof_end(ctx, NC_K_SCATTER);
       prof_begin(ctx);
-      k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs,
+      k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->srec, ctx->cs,
                                                     (const typename V4<T>::t*)ctx->st_q[c],
                                                     (const typename V4<T>::t*)ctx->st_p[c],
                                                     (typename V4<T>::t*)ctx->st_q[o], (typename V4<T>::t*)ctx->st_p[o],
@@ -864,12 +865,11 @@ nc_status slab_begin_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_o
   }
   if (n_own > 0) {
     prof_begin(ctx);
-    k_scatter<<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp, ctx->tmpgid,
-                                               ctx->tmpkey);
+    k_scatter<<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->srec);
     LAUNCHED();
     prof_end(ctx, NC_K_SCATTER);
     prof_begin(ctx);
-    k_rank_gather<T><<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+    k_rank_gather<T><<<nblk(n_own, 256), 256, 0, s>>>(n_own, ctx->srec, ctx->cs, wq, nullptr,
                                                       (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
                                                       ctx->u32, ctx->nh, g, ctx->sidx, b_own);
     LAUNCHED();
@@ -915,19 +915,18 @@ nc_status slab_end_t(nc_ctx* ctx, const void* h1, const void* h2, T* F, double* 
   }
   if (n1 + n2 > 0) {
     prof_begin(ctx);
-    k_scatter<<<nblk(n1 + n2, 256), 256, 0, s>>>(n1 + n2, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->tmp,
-                                                 ctx->tmpgid, ctx->tmpkey, n_own);
+    k_scatter<<<nblk(n1 + n2, 256), 256, 0, s>>>(n1 + n2, ctx->key, ctx->slot, ctx->cs, ctx->gin, ctx->srec, n_own);
     LAUNCHED();
     prof_end(ctx, NC_K_SCATTER);
     // the halo buckets: [0, b_own) and [b_own + n_own, n)
     prof_begin(ctx);
     if (b_own > 0)
-      k_rank_gather<T><<<nblk(b_own, 256), 256, 0, s>>>(b_own, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+      k_rank_gather<T><<<nblk(b_own, 256), 256, 0, s>>>(b_own, ctx->srec, ctx->cs, wq, nullptr,
                                                         (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
                                                         ctx->u32, ctx->nh, g, ctx->sidx, 0);
     const int64_t rest = n - (b_own + n_own);
     if (rest > 0)
-      k_rank_gather<T><<<nblk(rest, 256), 256, 0, s>>>(rest, ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->cs, wq, nullptr,
+      k_rank_gather<T><<<nblk(rest, 256), 256, 0, s>>>(rest, ctx->srec, ctx->cs, wq, nullptr,
                                                        (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid, ctx->u,
                                                        ctx->u32, ctx->nh, g, ctx->sidx, b_own + n_own);
     LAUNCHED();
@@ -1054,7 +1053,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {&ctx->wq, v4 * N_}, {&ctx->sq, v4 * N_}, {(void**)&ctx->sgid, 4 * N_}, {&ctx->sF, v4 * N_},
       {&ctx->io_a, 3 * ts * N_}, {&ctx->io_b, 3 * ts * N_}, {(void**)&ctx->u, sizeof(double4) * N_}, {(void**)&ctx->u32, sizeof(float4) * N_},
       {(void**)&ctx->nh, 4 * N_}, {(void**)&ctx->key, 4 * N_}, {(void**)&ctx->slot, 4 * N_},
-      {(void**)&ctx->tmp, 4 * N_}, {(void**)&ctx->tmpgid, 4 * N_}, {(void**)&ctx->tmpkey, 4 * N_},
+      {(void**)&ctx->srec, sizeof(uint4) * N_},
       {(void**)&ctx->counts, 4 * (size_t)C1}, {(void**)&ctx->cs, 4 * (size_t)C1},
       {(void**)&ctx->bsum, 4 * (size_t)(C1 / SCAN_TILE + 2)}, {(void**)&ctx->tot, 16},
       {(void**)&ctx->bpart, sizeof(double) * NPART * (size_t)ctx->max_blocks},
@@ -1114,7 +1113,7 @@ void nc_destroy(nc_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   void* ps[] = {ctx->st_q[0], ctx->st_q[1], ctx->st_p[0], ctx->st_p[1], ctx->st_gid[0], ctx->st_gid[1], ctx->st_F,
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
-                ctx->tmp, ctx->tmpgid, ctx->tmpkey, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
+                ctx->srec, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
                 ctx->part_tot, ctx->part_acc, ctx->rcount, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
                 ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot};
   for (void* p : ps)
