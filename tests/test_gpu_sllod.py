@@ -111,6 +111,12 @@ CASES = [
     (3, 4, "biaxial", "f64", "ds"),
     (2, 2, "uniaxial", "f32", "do"),
     (3, 4, "biaxial", "f32", "do"),
+    # fp32 on every config / variant pair the fp64 cases cover
+    (1, 2, "uniaxial", "f32", "do"),
+    (1, 2, "uniaxial", "f32", "ds"),
+    (2, 2, "uniaxial", "f32", "ds"),
+    (3, 4, "uniaxial", "f32", "do"),
+    (3, 4, "biaxial", "f32", "ds"),
 ]
 
 
