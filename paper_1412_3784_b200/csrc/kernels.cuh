@@ -868,7 +868,15 @@ template <bool DIGEST>
 __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<float>& pc, K3Smem<float>& sm, Acc& acc,
                                                int qlen, int lane, uint32_t stage0, const double4* __restrict__ u64,
                                                K3QT (*queue)[32]) {
-  const int qmax = __reduce_max_sync(0xffffffffu, qlen);
+  // the two far lanes of a row (lanes 2r, 2r + 1: the same particle i, accumulators combined later
+  // in fixed order) split their queued items evenly: lane 2r takes the first ceil(T/2) items of the
+  // concatenation (its own queue, then its partner's), lane 2r + 1 the rest
+  const int qp = __shfl_xor_sync(0xffffffffu, qlen, 1);
+  const int odd = lane & 1, tot2 = qlen + qp, h0 = (tot2 + 1) >> 1;
+  const int q0 = odd ? qp : qlen;          // the even lane's own count
+  const int myn = odd ? tot2 - h0 : h0;    // items this lane evaluates
+  const int gbase = odd ? h0 : 0;
+  const int qmax = __reduce_max_sync(0xffffffffu, myn);
   const double sig2 = g.sig2, eps24 = 24.0 * g.eps;
   const uint32_t dummy = stage0 + 4u * K3_DUMMY;
   auto pair2 = [&](uint32_t ta, uint32_t tb, uint32_t ja, uint32_t jb, int ea, int eb, const double4& pa,
@@ -913,9 +921,11 @@ __device__ __forceinline__ void eval_close_f64(const Geom& g, const PairCtx<floa
   };
   // queue entry k of this lane -> staged index t, sorted index j (pc.my + dummy for none), entry e
   auto item = [&](int k, uint32_t& t, uint32_t& j, int& e) {
-    const uint32_t a = k < qlen ? qaddr(queue[k][lane], stage0) : dummy;
+    const int gk = gbase + k;
+    const int src = gk < q0 ? (lane & ~1) : (lane | 1), slot = gk < q0 ? gk : gk - q0;
+    const uint32_t a = k < myn ? qaddr(queue[slot][src], stage0) : dummy;
     t = (a - stage0) >> 2;
-    j = k < qlen ? sidx_of(sm, t, pc.base_off) : pc.my;
+    j = k < myn ? sidx_of(sm, t, pc.base_off) : pc.my;
     e = sm.sent[t];
   };
   for (int k = 0; k < qmax; k += 2) {
