@@ -107,6 +107,19 @@ def test_c1_both_pair_kernels(variant, kernel):
     assert g["kernel"] == kernel
 
 
+@pytest.mark.parametrize("scale", [3, 4])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_sparse_kernel_tiny_grid_many_rows_per_warp(variant, scale):
+    """k_pairs_sparse on a tiny WCA grid (C1 scaled to 7-10 cells a side, ~9-13 particles a cell
+    row): a warp's 32 particles span 3-5 cell rows, so most lanes build their own row data instead of
+    reading the warp's two shared rows -- both paths must give the oracle's pair set and forces."""
+    w, q = inputs(1, "f32", scale=scale)
+    g, _ = check_against_oracle(w, q, variant, "f32", kernel="sparse")
+    assert g["kernel"] == "sparse"
+    dims = g["dims"]
+    assert 32 > 2 * dims[0] * 1.0  # rows of < 16 cells: a warp spans >= 3 cell rows
+
+
 @pytest.mark.parametrize("kernel", ["segment", "sparse"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
 def test_segment_kernel_on_dense_lj_cells(variant, kernel):
