@@ -288,45 +288,49 @@ __global__ void k_scan_apply(const uint32_t* __restrict__ in, int64_t m, const u
 // three (C1's 24k cells, slab migration blocks, ...): rows of 1024 coalesced elements, each a
 // block scan, with a running carry.  out[m] = total.
 constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_R = 32, SCAN_SMALL = SCAN_SMALL_R * SCAN_SMALL_T;
+// m <= SCAN_SMALL in one block with three barriers: coalesced loads into shared memory (padded one word
+// per 32), each thread scans its own contiguous run of R = ceil(m / T) entries, one block scan of the
+// T run totals, each thread writes its run's exclusive prefixes back, coalesced stores.
+__host__ __device__ constexpr int scan_pad(int i) { return i + (i >> 5); }
 __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __restrict__ in, int64_t m,
                                                              uint32_t* __restrict__ out) {
+  extern __shared__ uint32_t sbuf[];  // scan_pad(SCAN_SMALL) words
   __shared__ uint32_t wsum[SCAN_SMALL_T / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int rows = (int)((m + SCAN_SMALL_T - 1) / SCAN_SMALL_T);
-  uint32_t v[SCAN_SMALL_R];
+  const int mm = (int)m;
+  for (int i = tid; i < mm; i += SCAN_SMALL_T) sbuf[scan_pad(i)] = in[i];
+  __syncthreads();
+  const int R = (mm + SCAN_SMALL_T - 1) / SCAN_SMALL_T;
+  const int b = tid * R, e = min(b + R, mm);
+  uint32_t run = 0;
+  for (int i = b; i < e; ++i) run += sbuf[scan_pad(i)];
+  uint32_t x = run;  // inclusive scan of the run totals: warp, then warp sums
 #pragma unroll
-  for (int r = 0; r < SCAN_SMALL_R; ++r) {  // every load in flight before the first scan
-    const int64_t i = (int64_t)r * SCAN_SMALL_T + tid;
-    v[r] = (r < rows && i < m) ? in[i] : 0u;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
-  uint32_t carry = 0;
-#pragma unroll
-  for (int r = 0; r < SCAN_SMALL_R; ++r) {
-    if (r >= rows) break;
-    uint32_t x = v[r];
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = wsum[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
     }
-    if (lane == 31) wsum[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-      uint32_t w = wsum[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      wsum[lane] = w;  // inclusive over warps
-    }
-    __syncthreads();
-    const int64_t i = (int64_t)r * SCAN_SMALL_T + tid;
-    if (i < m) out[i] = carry + (wid > 0 ? wsum[wid - 1] : 0u) + x - v[r];
-    carry += wsum[31];
-    __syncthreads();  // wsum is rewritten by the next row
+    wsum[lane] = w;  // inclusive over warps
   }
-  if (tid == 0) out[m] = carry;
+  __syncthreads();
+  uint32_t pre = (wid > 0 ? wsum[wid - 1] : 0u) + x - run;  // exclusive prefix of this run
+  for (int i = b; i < e; ++i) {
+    const uint32_t v = sbuf[scan_pad(i)];
+    sbuf[scan_pad(i)] = pre;
+    pre += v;
+  }
+  __syncthreads();
+  for (int i = tid; i < mm; i += SCAN_SMALL_T) out[i] = sbuf[scan_pad(i)];
+  if (tid == 0) out[m] = wsum[31];
 }
 
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
@@ -1564,9 +1568,19 @@ __global__ void __launch_bounds__(K3R_T) k_reduce(const double* __restrict__ bpa
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // the layer sum in layer order (bitwise the host's nc_slab_reduce), the layer partials staged through
+  // shared memory 64 layers at a time (all loads in flight, instead of one dependent L2 load per layer)
+  __shared__ double lbuf[64][NPART];
+  double s = 0.0;
+  for (int l0 = 0; l0 < nlayers; l0 += 64) {
+    const int nl = min(64, nlayers - l0);
+    for (int k = tid; k < nl * NPART; k += K3R_T) lbuf[k / NPART][k % NPART] = __ldcg(&lpart[(int64_t)l0 * NPART + k]);
+    __syncthreads();
+    if (tid < NPART)
+      for (int l = 0; l < nl; ++l) s += lbuf[l][tid];
+    __syncthreads();
+  }
   if (tid < NPART) {
-    double s = 0.0;
-    for (int l = 0; l < nlayers; ++l) s += __ldcg(&lpart[(int64_t)l * NPART + tid]);
     tot[tid] = s;
     acc[tid] += s;
   } else if (tid == NPART) {

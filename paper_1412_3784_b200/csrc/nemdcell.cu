@@ -310,7 +310,7 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
 nc_status launch_scan_raw(nc_ctx* ctx, const uint32_t* in, int64_t m, uint32_t* out) {
   cudaStream_t s = ctx->stream;
   if (m <= SCAN_SMALL) {
-    k_scan_small<<<1, SCAN_SMALL_T, 0, s>>>(in, m, out);
+    k_scan_small<<<1, SCAN_SMALL_T, sizeof(uint32_t) * (size_t)scan_pad((int)m + 32), s>>>(in, m, out);
     LAUNCHED();
   } else {
     const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
@@ -1093,7 +1093,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_seg<false, 2>, sizeof(SgSmem<2>)},
         {(const void*)k_pairs_seg<true, 2>, sizeof(SgSmem<2>)},
         {(const void*)k_pairs_seg<false, 4>, sizeof(SgSmem<4>)},
-        {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)}};
+        {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)},
+        {(const void*)k_scan_small, sizeof(uint32_t) * (size_t)scan_pad(SCAN_SMALL + 32)}};
     for (const KA& a : ka) {
       cudaError_t e = cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
       if (e != cudaSuccess) {
