@@ -244,12 +244,22 @@ def run_slab(args):
     torch.cuda.set_device(lrank)
     from paper_1412_3784_b200 import workloads as W
     from paper_1412_3784_b200.nemdcell import CellList
-    from paper_1412_3784_b200.slab import DistTransport, SlabRank, SlabSystem, own_particles
+    from paper_1412_3784_b200.slab import SlabRankDev, SlabSystem, own_particles
 
     # --weak: 8,388,608 particles per GPU in a box elongated along v3; else C<k> split
     w = W.make_weak(ws) if args.weak else workload(args.config)
-    q = W.positions(w, dtype=np.float32, k=args.config if not args.weak else 4, r=0)
-    p = W.momenta(w, dtype=np.float32, k=args.config if not args.weak else 4, r=0)
+    kq = args.config if not args.weak else 4
+    # the same input as the single-GPU line (BASELINE's relaxed fluid unless --input lattice); every rank
+    # relaxes the same seeded system (deterministic) and keeps its own slab
+    input_kind = args.input if (args.weak or args.config != 0) else "lattice"
+    relax_fmax = None
+    if input_kind == "fluid":
+        qf, relax_fmax = relaxed_fluid(w, args.variant, kq, f"cuda:{lrank}")
+        q = qf.astype(np.float32)
+        del qf
+    else:
+        q = W.positions(w, dtype=np.float32, k=kq, r=0)
+    p = W.momenta(w, dtype=np.float32, k=kq, r=0)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
@@ -259,19 +269,30 @@ def run_slab(args):
     full = CellList(args.variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=maxc, device=lrank)
     full.set_flow(w.A, w.policy, w.t0, **kw)
     idx = own_particles(full, torch.from_numpy(q).to(f"cuda:{lrank}"), rank, ws)
+    from paper_1412_3784_b200 import nemdcell as ncm
+    l3 = int(ncm.nc_slab_layers(full.ctx, 0, 1)[2])
     full.close()
     torch.cuda.empty_cache()
     stream = torch.cuda.Stream(lrank)
-    cap = int(1.3 * w.n / ws) + 4 * w.n // 171 + 65536
-    sr = SlabRank(rank, ws, variant=args.variant, prec="f32", rc=w.rc, u_shift=w.ushift, mass=w.mass, capacity=cap,
-                  max_cells=maxc, device=lrank, stream=stream.cuda_stream)
+    cap = int(1.15 * w.n / ws) + 4 * w.n // l3 + 65536
+    # the host-synchronization-free step (SlabRankDev): fixed-capacity halo messages of 1.5 layers,
+    # migration messages of 1/8 layer (a step moves ~0.1% of a boundary layer)
+    layer = w.n // l3
+    if os.environ.get("NC_SLAB_HOSTCOUNTS") == "1":  # A/B: the round-1 step with host-read counts
+        from paper_1412_3784_b200.slab import SlabRank
+        sr = SlabRank(rank, ws, variant=args.variant, prec="f32", rc=w.rc, u_shift=w.ushift, mass=w.mass,
+                      capacity=cap, max_cells=maxc, device=lrank, stream=stream.cuda_stream)
+    else:
+        sr = SlabRankDev(rank, ws, variant=args.variant, prec="f32", rc=w.rc, u_shift=w.ushift, mass=w.mass,
+                         capacity=cap, hcap=int(1.5 * layer) + 4096, mcap=layer // 8 + 4096, max_cells=maxc,
+                         device=lrank, stream=stream.cuda_stream)
     sr.set_flow(w.A, w.policy, w.t0, **kw)
     sr.load(q[idx], p[idx], idx.astype(np.int32))
     del q, p
     from paper_1412_3784_b200.slab import LoopbackTransport, NcclTransport
 
-    # N > 1: the library's own NCCL data plane (nc_slab_exchange / nc_slab_allgather); torch only
-    # broadcasts the unique id
+    # N > 1: the library's own NCCL data plane (whole fixed-capacity messages, nc_sd_exchange_start /
+    # nc_slab_allgather); torch only broadcasts the unique id.  No host synchronization inside a step.
     sysm = SlabSystem([sr], NcclTransport(sr, rank, ws) if ws > 1 else LoopbackTransport())
     with torch.cuda.stream(stream):
         sysm.forces(False)
@@ -297,6 +318,8 @@ def run_slab(args):
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop()
+    if hasattr(sr, "status"):
+        sr.status()  # after the timed region: raises if a message or the own capacity overflowed
     ms = ev0.elapsed_time(ev1)
     launches = sr.cl.launches() - l0
     prof = sr.cl.profile_read()
@@ -394,14 +417,19 @@ def run_slab(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)",
+            "dtype": "f32",
+            "data": ("synthetic fluid: seeded uniform fractional positions + 200 capped steepest-descent overlap-"
+                     f"removal steps through the library (max |F| after: {relax_fmax:.3g}), Gaussian momenta T=1"
+                     if input_kind == "fluid" else
+                     "synthetic (seeded jittered lattice in fractional coordinates, DESIGN.md section 4)"),
             "config": {"workload": w.name if args.weak else f"C{args.config}", "n_total": w.n,
-                       "n_per_gpu": w.n // ws, "variant": args.variant,
+                       "n_per_gpu": w.n // ws, "variant": args.variant, "input": input_kind,
                        "box": box_text(w), "potential": pot_text(w),
-                       "precision": "fp32 storage + fp32 filter, fp64 interactions",
+                       "precision": "fp32 storage + fp32 filter, fp32/fp64 two-tier interactions",
                        "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
                                                                    "NCCL P2P halo + migration inside "
-                                                                   "libnemdcell (nc_slab_exchange)"},
+                                                                   "libnemdcell, host-synchronization-free "
+                                                                   "step (fixed-capacity messages, nc_sd_*)"},
             "particle_steps_per_s": w.n * args.steps / (ms_max * 1e-3),
             "kernel_ms_per_step_rank0": {k: v[0] / max(args.steps, 1) for k, v in prof.items() if v[1]},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(t[3]), "clocks": clocks,

@@ -366,6 +366,54 @@ nc_status nc_slab_exchange(nc_ctx *ctx, const void *send_lo, int64_t n_lo, const
  * nc_slab_forces writes them), padded to max_rows; out receives nranks x max_rows rows in rank order. */
 nc_status nc_slab_allgather(nc_ctx *ctx, const double *local, int64_t nloc, int64_t max_rows, double *out);
 
+/* ---- Host-synchronization-free slab step (csrc/slab_dc.cuh, the step above without
+ * any device-to-host read).  The context keeps the rank's own-particle count in device memory
+ * (nc_sd_load sets it); every call below launches over the CAPACITY ncap and reads that count on the
+ * device.  Messages are fixed-capacity device buffers of (1 + cap) records: record 0 is a header whose
+ * first 4 bytes hold the record count (uint32), records 1..cap the payload (migration: 2 T4 words per
+ * record = q.xyz + gid, p.xyz; halo: 1 word = q.xyz + gid); whole buffers are exchanged, so no count
+ * crosses to the host.  The own particles of a force evaluation are sorted to fixed slots [H, H + n),
+ * H = hcap per halo layer that precedes the own layers in cell order, so the interior layers' pair kernel
+ * runs before the halo arrives.  F, U, W, the per-layer partials and whole trajectories are bitwise
+ * those of nc_slab_* (and of one device).  Overflow of a message (more records than its capacity) or of
+ * the own capacity drops the excess and sets a device flag; nc_sd_status reads count and flags (the
+ * only synchronizing call) and fails with NC_E_OOM (overflow) or NC_E_STATE (a particle moved more
+ * than one layer past its slab).
+ *   nc_sd_load        the own count (device word) after the caller filled q, p, gid (n x 3, n, device).
+ *   nc_sd_kick_drift  nc_slab_kick_kick_drift over the device count (box advanced on the host).
+ *   nc_sd_kick        closing half kick over the device count.
+ *   nc_sd_migrate     nc_slab_migrate into two migration messages (stayers to q_out, p_out, gid_out).
+ *   nc_sd_absorb      both received migration messages appended after the own particles.
+ *   nc_sd_halo        the boundary layers' particles into two halo messages.
+ *   nc_sd_exchange_start  whole-buffer exchange with r-1 / r+1 over NCCL (nc_slab_comm_init first) on the
+ *                     communication stream after the work queued on cfg.stream; nc_slab_exchange_wait
+ *                     makes cfg.stream wait for it.
+ *   nc_sd_forces_begin  own particles into cells at fixed slots, K3 on the interior own layers
+ *                     (requires the context capacity >= ncap + 2 hcap).
+ *   nc_sd_forces_end  received halo messages into cells, K3 on the boundary layers, reduction, forces of
+ *                     the own particles in their local order into F (n x 3); parts (nlayers x 13
+ *                     doubles, host) or NULL -- only a non-NULL parts synchronizes. */
+nc_status nc_sd_load(nc_ctx *ctx, int64_t n);
+nc_status nc_sd_status(nc_ctx *ctx, int64_t *n_own, uint32_t *flags);
+nc_status nc_sd_kick_drift(nc_ctx *ctx, void *q, void *p, const void *F, int64_t ncap, double dt_prev, double dt);
+nc_status nc_sd_kick(nc_ctx *ctx, void *p, const void *F, int64_t ncap, double dt);
+nc_status nc_sd_migrate(nc_ctx *ctx, void *q, const void *p, const uint32_t *gid, int64_t ncap, int klo, int khi,
+                        void *q_out, void *p_out, uint32_t *gid_out, void *msg_lo, void *msg_hi, int64_t mcap);
+nc_status nc_sd_absorb(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, int64_t mcap, void *q, void *p,
+                       uint32_t *gid, int64_t ncap);
+nc_status nc_sd_halo(nc_ctx *ctx, void *q, const uint32_t *gid, int64_t ncap, int klo, int khi, void *msg_lo,
+                     void *msg_hi, int64_t hcap);
+nc_status nc_sd_exchange_start(nc_ctx *ctx, const void *send_lo, const void *send_hi, void *recv_lo, void *recv_hi,
+                               int64_t cap, int words);
+nc_status nc_sd_forces_begin(nc_ctx *ctx, const void *q, const uint32_t *gid, int64_t ncap, int64_t hcap, int klo,
+                             int khi);
+nc_status nc_sd_forces_end(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, void *F, double *parts);
+/* nc_sd_forces_end, and the own particles adopt their sorted (cell, gid) order: q_out (wrapped q), p_out
+ * (p gathered from the caller's p), gid_out and F in that order (all n x 3 / n, device; q_out, p_out,
+ * gid_out distinct from the inputs) -- the next step then reads spatially ordered arrays. */
+nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, const void *p, void *q_out,
+                                  void *p_out, uint32_t *gid_out, void *F, double *parts);
+
 /* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
  * kernel).  Both evaluate the same neighborhoods, the same
  * candidates and the same pair set; they differ in how work maps to warps:

@@ -336,10 +336,12 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __r
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
 __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ cs, const uint32_t* __restrict__ gid_in,
-                          uint4* __restrict__ rec, int64_t i0 = 0) {
+                          uint4* __restrict__ rec, int64_t i0 = 0, const uint32_t* __restrict__ dn = nullptr) {
   // particles [i0, i0 + n) (a slab evaluation scatters its own and its halo particles separately).
   // One 16-byte record per particle (source index, gid, cell): a random-order input costs one sector
   // per particle, not three; k_rank_gather reads the records in bucket order (coalesced)
+  // (dn: the count lives on the device -- the grid covers a capacity; host-synchronization-free slab step)
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= i0 + n) return;
   const uint32_t c = key[i];
@@ -348,7 +350,9 @@ __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uin
 }
 
 // cs[c] += b for c in [c0, c1): the own cells' starts after the halo particles that precede them
-__global__ void k_add_range(uint32_t* __restrict__ cs, int64_t c0, int64_t c1, uint32_t b) {
+__global__ void k_add_range(uint32_t* __restrict__ cs, int64_t c0, int64_t c1, uint32_t b,
+                            const uint32_t* __restrict__ db = nullptr) {
+  if (db) b += *db;  // device-side part of the offset (host-synchronization-free slab step)
   const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (c < c1) cs[c] += b;
 }
@@ -368,10 +372,13 @@ k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restri
                               uint32_t* __restrict__ gid_out, double4* __restrict__ u_out,
                               float4* __restrict__ u32_out, uint32_t* __restrict__ nh_out,
                               const __grid_constant__ Geom g, uint32_t* __restrict__ idx_out = nullptr,
-                              int64_t s0 = 0) {
-  // bucket positions [s0, s0 + n) (a slab evaluation places own and halo particles in two phases)
+                              int64_t s0 = 0, const uint32_t* __restrict__ drange = nullptr) {
+  // bucket positions [s0, s0 + n) (a slab evaluation places own and halo particles in two phases);
+  // drange: [drange[0], drange[1]) from the device (the grid covers a capacity)
+  int64_t send = s0 + n;
+  if (drange) { s0 = drange[0]; send = (int64_t)min((long long)drange[1], (long long)(s0 + n)); }
   int64_t s = s0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= s0 + n) return;
+  if (s >= send) return;
   const uint4 r = rec[s];
   const uint32_t i = r.x, gg = r.y, c = r.z;
   const typename V4<T>::t q = qw[i];  // gathers issued before the rank loop
@@ -1716,7 +1723,8 @@ __global__ void k_kick(int64_t n, typename V4<T>::t* __restrict__ p, const typen
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void k_kick_drift3(int64_t n, T* __restrict__ q, T* __restrict__ p, const T* __restrict__ F, SllodParams sp,
-                              int pending = 0, const K3Kick pk = K3Kick{}) {
+                              int pending = 0, const K3Kick pk = K3Kick{}, const uint32_t* __restrict__ dn = nullptr) {
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double hd = 0.5 * sp.dt;
@@ -1740,7 +1748,9 @@ __global__ void k_kick_drift3(int64_t n, T* __restrict__ q, T* __restrict__ p, c
 }
 
 template <typename T>
-__global__ void k_kick3(int64_t n, T* __restrict__ p, const T* __restrict__ F, SllodParams sp) {
+__global__ void k_kick3(int64_t n, T* __restrict__ p, const T* __restrict__ F, SllodParams sp,
+                        const uint32_t* __restrict__ dn = nullptr) {
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double ax, ay, az;
@@ -1757,7 +1767,9 @@ __global__ void k_kick3(int64_t n, T* __restrict__ p, const T* __restrict__ F, S
 // mode 2 (layers):    wrap q in place and write each particle's cell layer to layer_out.
 template <typename T>
 __global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_constant__ Geom g, int klo, int khi,
-                                int mode, uint8_t* __restrict__ cls, int32_t* __restrict__ layer_out = nullptr) {
+                                int mode, uint8_t* __restrict__ cls, int32_t* __restrict__ layer_out = nullptr,
+                                const uint32_t* __restrict__ dn = nullptr) {
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double q0 = (double)q[3 * i], q1 = (double)q[3 * i + 1], q2 = (double)q[3 * i + 2];
@@ -1793,7 +1805,9 @@ __global__ void k_slab_classify(int64_t n, T* __restrict__ q, const __grid_const
 constexpr int PART_T = 256;
 // per-block counts of classes 0..3, CLASS-MAJOR (bcnt[c * nb + b]) so that one
 // exclusive scan of the 4 nb entries gives every class's block offsets
-__global__ void k_class_count(int64_t n, int64_t nb, const uint8_t* __restrict__ cls, uint32_t* __restrict__ bcnt) {
+__global__ void k_class_count(int64_t n, int64_t nb, const uint8_t* __restrict__ cls, uint32_t* __restrict__ bcnt,
+                              const uint32_t* __restrict__ dn = nullptr) {
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   __shared__ uint32_t c[4];
   if (threadIdx.x < 4) c[threadIdx.x] = 0;
   __syncthreads();
@@ -1813,7 +1827,11 @@ template <typename T>
 __global__ void k_class_scatter(int64_t n, const uint8_t* __restrict__ cls, const uint32_t* __restrict__ boff,
                                 const T* __restrict__ q, const T* __restrict__ p, const uint32_t* __restrict__ gid,
                                 T* __restrict__ q0, T* __restrict__ p0, uint32_t* __restrict__ g0,
-                                typename V4<T>::t* __restrict__ r1, typename V4<T>::t* __restrict__ r2, int words) {
+                                typename V4<T>::t* __restrict__ r1, typename V4<T>::t* __restrict__ r2, int words,
+                                const uint32_t* __restrict__ dn = nullptr, int64_t rcap = INT64_MAX) {
+  // (dn: device count, the grid covers a capacity; rcap: records beyond a message's capacity are dropped
+  // -- the totals flag the overflow)
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   __shared__ uint32_t wsum[PART_T / 32][4];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int64_t i = (int64_t)blockIdx.x * PART_T + threadIdx.x;
@@ -1840,6 +1858,7 @@ __global__ void k_class_scatter(int64_t n, const uint8_t* __restrict__ cls, cons
     }
     return;
   }
+  if ((int64_t)pos >= rcap) return;
   typename V4<T>::t* r = (c == 1 ? r1 : r2) + (int64_t)pos * words;
   r[0] = mk4(x, y, z, idx_to_w(gg, T()));
   if (words == 2) r[1] = mk4(p[3 * i], p[3 * i + 1], p[3 * i + 2], (T)0);
@@ -1861,7 +1880,8 @@ template <typename T>
 __global__ void k_wrap_key_src(int64_t n, const T* __restrict__ qin, int stride, const uint32_t* __restrict__ gsrc,
                                int64_t off, typename V4<T>::t* __restrict__ qout, uint32_t* __restrict__ gout,
                                uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
-                               const __grid_constant__ Geom g) {
+                               const __grid_constant__ Geom g, const uint32_t* __restrict__ dn = nullptr) {
+  if (dn) n = (int64_t)min((unsigned long long)n, (unsigned long long)*dn);
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double q0 = (double)qin[i * stride], q1 = (double)qin[i * stride + 1], q2 = (double)qin[i * stride + 2];
@@ -1876,9 +1896,16 @@ __global__ void k_wrap_key_src(int64_t n, const T* __restrict__ qin, int stride,
 // F of the own particles back to their input order (sorted slot -> original local index)
 template <typename T>
 __global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ src, const uint32_t* __restrict__ sidx,
-                             int64_t n_own, T* __restrict__ dst) {
+                             int64_t n_own, T* __restrict__ dst, const uint32_t* __restrict__ drange = nullptr) {
+  // drange: sorted slots [drange[0], drange[1]) (the own particles of a device-count slab step)
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
+  if (drange) {
+    s += drange[0];
+    if (s >= (int64_t)drange[1]) return;
+    n_own = INT64_MAX;
+  } else if (s >= n) {
+    return;
+  }
   uint32_t i = sidx[s];
   if ((int64_t)i >= n_own) return;
   typename V4<T>::t v = src[s];

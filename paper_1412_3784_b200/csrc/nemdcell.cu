@@ -83,6 +83,11 @@ struct nc_ctx {
   int64_t slab_n_own = 0, slab_n1 = 0, slab_n2 = 0, slab_b_own = 0;
   int slab_klo = 0, slab_khi = 0;
   bool slab_open = false;
+  // host-synchronization-free slab step (csrc/slab_dc.cuh): device counters and host-side bookkeeping
+  uint32_t* sd = nullptr;
+  int64_t sd_ncap = 0, sd_hcap = 0, sd_H = 0, sd_n_hint = 0;
+  int sd_pre = 0;
+  bool sd_open = false;
   int seg_nw = 2;  // warps per block of the sparse-cell kernel (seg_cells)
   bool kick_pending = false;
   bool count_tiers = false;  // nc_profile mode 2: k_pairs counts its fp32-tier interactions
@@ -1065,6 +1070,7 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
       {(void**)&ctx->gin, 4 * N_}, {(void**)&ctx->sidx, 4 * N_}, {(void**)&ctx->cls, N_},
       {(void**)&ctx->pbcnt, 16 * (N_ / PART_T + 2)}, {(void**)&ctx->pboff, 16 * (N_ / PART_T + 2) + 4},
       {(void**)&ctx->ptot, 16},
+      {(void**)&ctx->sd, 4 * 16},
   };
   for (auto& a : allocs) {
     e = cudaMalloc(a.p, a.bytes);
@@ -1116,7 +1122,7 @@ void nc_destroy(nc_ctx* ctx) {
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->srec, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
                 ctx->part_tot, ctx->part_acc, ctx->rcount, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
-                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot};
+                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot, ctx->sd};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (ctx->s_h2d) {
@@ -1630,6 +1636,7 @@ nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* 
 }  // extern "C"
 
 #include "nccl_slab.cuh"
+#include "slab_dc.cuh"
 
 void nc_comm_release(nc_ctx* ctx) {
   if (!ctx->comm) return;

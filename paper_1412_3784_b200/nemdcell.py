@@ -32,7 +32,11 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_slab_reduce", "nc_set_pair_kernel",
            "nc_pair_kernel_used", "nc_get_pairs", "nc_get_cell_gids", "nc_get_pair_counts", "nc_debug",
            "nc_nccl_unique_id", "nc_slab_comm_init", "nc_slab_exchange_start", "nc_slab_exchange_wait",
-           "nc_slab_exchange", "nc_slab_allgather", "nc_slab_layer_of"]
+           "nc_slab_exchange", "nc_slab_allgather", "nc_slab_layer_of",
+           # host-synchronization-free slab step (csrc/slab_dc.cuh)
+           "nc_sd_load", "nc_sd_status", "nc_sd_kick_drift", "nc_sd_kick", "nc_sd_migrate", "nc_sd_absorb",
+           "nc_sd_halo", "nc_sd_exchange_start", "nc_sd_forces_begin", "nc_sd_forces_end",
+           "nc_sd_forces_end_sorted"]
 NC_DBG_DROP_ENTRIES = 1
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE = 0, 1, 2, 3
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT, "sparse": NC_PK_SPARSE}
@@ -127,6 +131,17 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_slab_forces_end.argtypes = [vp, vp, vp, vp, vp]
         L.nc_slab_kick.argtypes = [vp, vp, vp, i64, d]
         L.nc_slab_reduce.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.nc_sd_load.argtypes = [vp, i64]
+        L.nc_sd_status.argtypes = [vp, vp, vp]
+        L.nc_sd_kick_drift.argtypes = [vp, vp, vp, vp, i64, d, d]
+        L.nc_sd_kick.argtypes = [vp, vp, vp, i64, d]
+        L.nc_sd_migrate.argtypes = [vp, vp, vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, i64]
+        L.nc_sd_absorb.argtypes = [vp, vp, vp, i64, vp, vp, vp, i64]
+        L.nc_sd_halo.argtypes = [vp, vp, vp, i64, i32, i32, vp, vp, i64]
+        L.nc_sd_exchange_start.argtypes = [vp, vp, vp, vp, vp, i64, i32]
+        L.nc_sd_forces_begin.argtypes = [vp, vp, vp, i64, i64, i32, i32]
+        L.nc_sd_forces_end.argtypes = [vp, vp, vp, vp, vp]
+        L.nc_sd_forces_end_sorted.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.nc_launch_count.argtypes = [vp]
         L.nc_launch_count.restype = i64
         L.nc_set_pair_kernel.argtypes = [vp, i32]
@@ -376,6 +391,68 @@ def nc_slab_kick_kick_drift(ctx, q, p, F, n: int, dt_prev: float, dt: float) -> 
 
 def nc_slab_kick(ctx, p, F, n, dt) -> None:
     _check(ctx, load().nc_slab_kick(ctx, _ptr(p), _ptr(F), int(n), float(dt)))
+
+
+# ------------------------------------------------ host-synchronization-free slab step (csrc/slab_dc.cuh)
+# Counts stay on the device: messages are (1 + cap)-record buffers whose record 0 carries the count;
+# own particles are counted in the context.  nc_sd_status is the only call that reads anything back.
+
+def nc_sd_load(ctx, n: int) -> None:
+    _check(ctx, load().nc_sd_load(ctx, int(n)))
+
+
+def nc_sd_status(ctx):
+    """(own count, flags) -- synchronizes; raises NcError on an overflow / far move flag."""
+    n = np.zeros(1, dtype=np.int64)
+    f = np.zeros(1, dtype=np.uint32)
+    _check(ctx, load().nc_sd_status(ctx, _ptr(n), _ptr(f)))
+    return int(n[0]), int(f[0])
+
+
+def nc_sd_kick_drift(ctx, q, p, F, ncap: int, dt_prev: float, dt: float) -> None:
+    _check(ctx, load().nc_sd_kick_drift(ctx, _ptr(q), _ptr(p), _ptr(F), int(ncap), float(dt_prev), float(dt)))
+
+
+def nc_sd_kick(ctx, p, F, ncap: int, dt: float) -> None:
+    _check(ctx, load().nc_sd_kick(ctx, _ptr(p), _ptr(F), int(ncap), float(dt)))
+
+
+def nc_sd_migrate(ctx, q, p, gid, ncap, klo, khi, q_out, p_out, gid_out, msg_lo, msg_hi, mcap) -> None:
+    _check(ctx, load().nc_sd_migrate(ctx, _ptr(q), _ptr(p), _ptr(gid), int(ncap), int(klo), int(khi), _ptr(q_out),
+                                     _ptr(p_out), _ptr(gid_out), _ptr(msg_lo), _ptr(msg_hi), int(mcap)))
+
+
+def nc_sd_absorb(ctx, msg_lo, msg_hi, mcap, q, p, gid, ncap) -> None:
+    _check(ctx, load().nc_sd_absorb(ctx, _ptr(msg_lo), _ptr(msg_hi), int(mcap), _ptr(q), _ptr(p), _ptr(gid),
+                                    int(ncap)))
+
+
+def nc_sd_halo(ctx, q, gid, ncap, klo, khi, msg_lo, msg_hi, hcap) -> None:
+    _check(ctx, load().nc_sd_halo(ctx, _ptr(q), _ptr(gid), int(ncap), int(klo), int(khi), _ptr(msg_lo), _ptr(msg_hi),
+                                  int(hcap)))
+
+
+def nc_sd_exchange_start(ctx, send_lo, send_hi, recv_lo, recv_hi, cap, words) -> None:
+    _check(ctx, load().nc_sd_exchange_start(ctx, _ptr(send_lo), _ptr(send_hi), _ptr(recv_lo), _ptr(recv_hi),
+                                            int(cap), int(words)))
+
+
+def nc_sd_forces_begin(ctx, q, gid, ncap, hcap, klo, khi) -> None:
+    _check(ctx, load().nc_sd_forces_begin(ctx, _ptr(q), _ptr(gid), int(ncap), int(hcap), int(klo), int(khi)))
+
+
+def nc_sd_forces_end(ctx, msg_lo, msg_hi, F, want_parts: bool, nlayers: int):
+    parts = np.zeros((nlayers, NPART)) if want_parts else None
+    _check(ctx, load().nc_sd_forces_end(ctx, _ptr(msg_lo), _ptr(msg_hi), _ptr(F),
+                                        _ptr(parts) if parts is not None else None))
+    return parts
+
+
+def nc_sd_forces_end_sorted(ctx, msg_lo, msg_hi, p, q_out, p_out, gid_out, F, want_parts: bool, nlayers: int):
+    parts = np.zeros((nlayers, NPART)) if want_parts else None
+    _check(ctx, load().nc_sd_forces_end_sorted(ctx, _ptr(msg_lo), _ptr(msg_hi), _ptr(p), _ptr(q_out), _ptr(p_out),
+                                               _ptr(gid_out), _ptr(F), _ptr(parts) if parts is not None else None))
+    return parts
 
 
 def nc_slab_reduce(ctx, parts: np.ndarray):

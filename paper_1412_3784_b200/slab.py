@@ -36,13 +36,13 @@ class SlabRank:
     """State of one rank: own particles (device tensors), its context, buffers."""
 
     def __init__(self, rank: int, nranks: int, *, variant="do", prec="f32", rc=2.5, eps=1.0, sigma=1.0,
-                 u_shift=None, mass=1.0, capacity=1 << 16, max_cells=0, device=0, stream=None):
+                 u_shift=None, mass=1.0, capacity=1 << 16, max_cells=0, device=0, stream=None, ctx_capacity=None):
         import torch
 
         self.torch = torch
         self.rank, self.nranks = rank, nranks
         self.cl = nc.CellList(variant, prec, rc=rc, eps=eps, sigma=sigma, u_shift=u_shift, mass=mass,
-                              capacity=capacity, max_cells=max_cells, device=device, stream=stream)
+                              capacity=ctx_capacity or capacity, max_cells=max_cells, device=device, stream=stream)
         self.ctx = self.cl.ctx
         self.dev = f"cuda:{device}"
         self.dtype = self.cl.dtype
@@ -166,11 +166,108 @@ class SlabRank:
         self.cl.close()
 
 
+class SlabRankDev(SlabRank):
+    """A rank of the HOST-SYNCHRONIZATION-FREE slab step (csrc/slab_dc.cuh): the own count lives on the
+    device, every kernel runs over the capacity, messages are fixed-capacity buffers whose first record
+    carries the count, and the own particles of the force evaluation sit at fixed sorted slots so the
+    interior layers' pair kernel runs before any halo count is known.  Nothing in step() reads the
+    device; `n` (and status()) synchronize when asked.  Bitwise the same trajectory as SlabRank."""
+
+    def __init__(self, rank: int, nranks: int, *, capacity=1 << 16, hcap=None, mcap=None, **kw):
+        hcap = int(hcap or max(4096, capacity // 4))
+        mcap = int(mcap or max(4096, capacity // 16))
+        # the context indexes own + two halo layers' worth of slots
+        super().__init__(rank, nranks, capacity=capacity, ctx_capacity=capacity + 2 * hcap, **kw)
+        torch = self.torch
+        t = lambda *s: torch.zeros(*s, dtype=self.dtype, device=self.dev)  # noqa: E731
+        self.hcap, self.mcap = hcap, mcap
+        self.msend = [t(1 + mcap, 8), t(1 + mcap, 8)]    # migration messages (header record + records)
+        self.mrecv = [t(1 + mcap, 8), t(1 + mcap, 8)]
+        self.hsend = [t(1 + hcap, 4), t(1 + hcap, 4)]    # halo messages
+        self.hrecv = [t(1 + hcap, 4), t(1 + hcap, 4)]
+
+    @property
+    def n(self):
+        return nc.nc_sd_status(self.ctx)[0] if getattr(self, "_dev_ready", False) else self._n0
+
+    @n.setter
+    def n(self, v):
+        self._n0 = v
+
+    def status(self):
+        return nc.nc_sd_status(self.ctx)
+
+    def load(self, q_own, p_own, gid_own):
+        super().load(q_own, p_own, gid_own)
+        nc.nc_sd_load(self.ctx, len(q_own))
+        self._dev_ready = True
+
+    def take(self, q, p, gid):
+        super().take(q, p, gid)
+        nc.nc_sd_load(self.ctx, len(q))
+
+    def kick_drift(self, dt):
+        nc.nc_sd_kick_drift(self.ctx, self.q, self.p, self.F, self.cap, self.pending_dt, dt)
+        self.pending_dt = 0.0
+
+    def migrate(self):
+        klo, khi, _ = self.layers()
+        nc.nc_sd_migrate(self.ctx, self.q, self.p, self.gid, self.cap, klo, khi, self.q2, self.p2, self.gid2,
+                         self.msend[0], self.msend[1], self.mcap)
+        self.q, self.q2 = self.q2, self.q
+        self.p, self.p2 = self.p2, self.p
+        self.gid, self.gid2 = self.gid2, self.gid
+        return self.msend
+
+    def absorb_msgs(self):
+        nc.nc_sd_absorb(self.ctx, self.mrecv[0], self.mrecv[1], self.mcap, self.q, self.p, self.gid, self.cap)
+
+    def halo(self):
+        if self.nranks == 1:  # a single slab wraps onto itself: no halo (the receive headers stay 0)
+            return None
+        klo, khi, _ = self.layers()
+        nc.nc_sd_halo(self.ctx, self.q, self.gid, self.cap, klo, khi, self.hsend[0], self.hsend[1], self.hcap)
+        return self.hsend
+
+    def forces_begin_dev(self):
+        klo, khi, _ = self.layers()
+        nc.nc_sd_forces_begin(self.ctx, self.q, self.gid, self.cap, self.hcap, klo, khi)
+
+    def forces_end_dev(self, want_parts=True):
+        """Forces of the own particles, which adopt their sorted (cell, gid) order at the same time (q, p,
+        gid and F permuted together): the next step's kernels read spatially ordered arrays."""
+        klo, khi, _ = self.layers()
+        parts = nc.nc_sd_forces_end_sorted(self.ctx, self.hrecv[0], self.hrecv[1], self.p, self.q2, self.p2,
+                                           self.gid2, self.F, want_parts, khi - klo)
+        self.q, self.q2 = self.q2, self.q
+        self.p, self.p2 = self.p2, self.p
+        self.gid, self.gid2 = self.gid2, self.gid
+        return parts
+
+    def flush(self):
+        if self.pending_dt > 0:
+            nc.nc_sd_kick(self.ctx, self.p, self.F, self.cap, self.pending_dt)
+            self.pending_dt = 0.0
+
+
 # -------------------------------------------------------------------- transports
 
 class LoopbackTransport:
     """All ranks in one process (tests on one GPU): rank r's send_lo is rank r-1's
     from_hi, its send_hi is rank r+1's from_lo (periodic in the rank index)."""
+
+    # fixed-capacity messages of the host-synchronization-free step (whole buffers, counts inside)
+    def exchange_msgs(self, sends, recv_bufs):
+        P = len(sends)
+        for r in range(P):
+            recv_bufs[r][0].copy_(sends[(r - 1) % P][1])  # from r-1: its upper message
+            recv_bufs[r][1].copy_(sends[(r + 1) % P][0])  # from r+1: its lower message
+
+    def start_msgs(self, sends, recv_bufs):
+        self.exchange_msgs(sends, recv_bufs)
+
+    def finish_msgs(self):
+        pass
 
     # split exchange (counts first, then the payload) for the overlapped force evaluation
     def counts(self, sends):
@@ -250,6 +347,17 @@ class DistTransport:
                dist.P2POp(dist.irecv, tensors_in[1], hi), dist.P2POp(dist.irecv, tensors_in[0], lo)]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+
+    def exchange_msgs(self, sends, recv_bufs):
+        (s_lo, s_hi), = sends
+        r_lo, r_hi = recv_bufs[0]
+        self._p2p([s_lo, s_hi], [r_lo, r_hi])
+
+    def start_msgs(self, sends, recv_bufs):
+        self.exchange_msgs(sends, recv_bufs)
+
+    def finish_msgs(self):
+        pass
 
     def counts(self, sends):
         torch = self.torch
@@ -366,6 +474,18 @@ class NcclTransport:
     def _words(buf):
         return int(buf.shape[1]) // 4
 
+    def start_msgs(self, sends, recv_bufs):
+        (s_lo, s_hi), = sends
+        r_lo, r_hi = recv_bufs[0]
+        nc.nc_sd_exchange_start(self.sr.ctx, s_lo, s_hi, r_lo, r_hi, int(s_lo.shape[0]) - 1, self._words(s_lo))
+
+    def finish_msgs(self):
+        nc.nc_slab_exchange_wait(self.sr.ctx)
+
+    def exchange_msgs(self, sends, recv_bufs):
+        self.start_msgs(sends, recv_bufs)
+        self.finish_msgs()
+
     def counts(self, sends):
         """Counts AND the payload launch (the library exchanges the counts, then leaves the payload in
         flight on its communication stream); start() hands the result over, finish() waits."""
@@ -433,6 +553,8 @@ class SlabSystem:
         self.repartitions = 0
 
     def forces(self, want_uw=True):
+        if self._dev():
+            return self.forces_dev(want_uw)
         hs = [r.halo() for r in self.ranks]
         if hasattr(self.tr, "start") and all(hasattr(r, "forces_begin") for r in self.ranks):
             # overlapped: counts, then the payload in flight while the interior layers are evaluated
@@ -467,7 +589,40 @@ class SlabSystem:
             r.take(q[m], p[m], gid[m])
         self.repartitions += 1
 
+    def _dev(self):
+        return all(isinstance(r, SlabRankDev) for r in self.ranks)
+
+    def forces_dev(self, want_uw=True):
+        """The force evaluation of the host-synchronization-free step: halo messages in flight while the
+        interior layers are evaluated; nothing is read back unless the energies are wanted."""
+        hs = [r.halo() for r in self.ranks]
+        if all(h is not None for h in hs):
+            self.tr.start_msgs(hs, [r.hrecv for r in self.ranks])
+        for r in self.ranks:
+            r.forces_begin_dev()
+        if all(h is not None for h in hs):
+            self.tr.finish_msgs()
+        parts = [r.forces_end_dev(want_parts=want_uw) for r in self.ranks]
+        if not want_uw:
+            return None
+        allp = self.tr.gather(parts)
+        return self.ranks[0].reduce(allp)
+
     def step(self, dt, want_uw=True):
+        if self._dev():
+            for r in self.ranks:
+                r.kick_drift(dt)
+            if any(r.l3_changed() for r in self.ranks):
+                self.repartition()
+            else:
+                sends = [r.migrate() for r in self.ranks]
+                self.tr.exchange_msgs(sends, [r.mrecv for r in self.ranks])
+                for r in self.ranks:
+                    r.absorb_msgs()
+            out = self.forces_dev(want_uw)
+            for r in self.ranks:
+                r.kick(dt)
+            return out
         for r in self.ranks:
             r.kick_drift(dt)
         if any(getattr(r, "l3_changed", lambda: False)() for r in self.ranks):

@@ -27,7 +27,7 @@ def _flow_kw(w):
     return kw
 
 
-def _worker(rank, P, port, variant, out_dir):
+def _worker(rank, P, port, variant, out_dir, dev=False):
     import torch
     import torch.distributed as dist
 
@@ -36,7 +36,7 @@ def _worker(rank, P, port, variant, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_1412_3784_b200 import workloads as W
     from paper_1412_3784_b200.nemdcell import CellList
-    from paper_1412_3784_b200.slab import HostStagedTransport, SlabRank, SlabSystem, own_particles
+    from paper_1412_3784_b200.slab import HostStagedTransport, SlabRank, SlabRankDev, SlabSystem, own_particles
 
     w = W.make(2, scale=2)
     q = W.positions(w, dtype=np.float32, k=2)
@@ -45,8 +45,9 @@ def _worker(rank, P, port, variant, out_dir):
     full.set_flow(w.A, w.policy, w.t0, **_flow_kw(w))
     idx = own_particles(full, torch.from_numpy(q).cuda(), rank, P)
     full.close()
-    sr = SlabRank(rank, P, variant=variant, prec="f32", rc=w.rc, u_shift=w.ushift, capacity=len(q),
-                  max_cells=4 * len(q) + 4096)
+    # dev: the host-synchronization-free step (device counts, fixed-capacity messages moved whole)
+    sr = (SlabRankDev if dev else SlabRank)(rank, P, variant=variant, prec="f32", rc=w.rc, u_shift=w.ushift,
+                                            capacity=len(q), max_cells=4 * len(q) + 4096)
     sr.set_flow(w.A, w.policy, w.t0, **_flow_kw(w))
     sr.load(q[idx], p[idx], idx.astype(np.int32))
     sysm = SlabSystem([sr], HostStagedTransport(rank, P))
@@ -63,15 +64,16 @@ def _worker(rank, P, port, variant, out_dir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("dev", [False, True])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_two_processes_share_one_gpu_bitwise(variant, tmp_path):
+def test_two_processes_share_one_gpu_bitwise(variant, dev, tmp_path):
     import torch
     import torch.multiprocessing as mp
     from paper_1412_3784_b200 import workloads as W
     from paper_1412_3784_b200.nemdcell import CellList
 
     P = 2
-    mp.start_processes(_worker, args=(P, _free_port(), variant, str(tmp_path)), nprocs=P, join=True,
+    mp.start_processes(_worker, args=(P, _free_port(), variant, str(tmp_path), dev), nprocs=P, join=True,
                        start_method="spawn")
     w = W.make(2, scale=2)
     q = W.positions(w, dtype=np.float32, k=2)

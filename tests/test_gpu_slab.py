@@ -18,18 +18,19 @@ def flow_kw(w):
     return kw
 
 
-def make_system(w, q, p, P, variant, prec):
+def make_system(w, q, p, P, variant, prec, dev=False):
+    """dev: the host-synchronization-free step (SlabRankDev: device counts, fixed-capacity messages)."""
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
-    from paper_1412_3784_b200.slab import LoopbackTransport, SlabRank, SlabSystem, own_particles
+    from paper_1412_3784_b200.slab import LoopbackTransport, SlabRank, SlabRankDev, SlabSystem, own_particles
 
     full = CellList(variant, prec, rc=w.rc, u_shift=w.ushift, capacity=len(q), max_cells=4 * len(q) + 4096)
     full.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
     ranks = []
     for r in range(P):
         idx = own_particles(full, q, r, P)
-        sr = SlabRank(r, P, variant=variant, prec=prec, rc=w.rc, u_shift=w.ushift, capacity=len(q),
-                      max_cells=4 * len(q) + 4096)
+        sr = (SlabRankDev if dev else SlabRank)(r, P, variant=variant, prec=prec, rc=w.rc, u_shift=w.ushift,
+                                                capacity=len(q), max_cells=4 * len(q) + 4096)
         sr.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
         sr.load(q[idx], p[idx], idx.astype(np.int32))
         ranks.append(sr)
@@ -55,7 +56,8 @@ def gather_state(system, n, dtype):
 
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_slab_forces_bitwise(P, variant):
+@pytest.mark.parametrize("dev", [False, True])
+def test_slab_forces_bitwise(P, variant, dev):
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
 
@@ -67,7 +69,7 @@ def test_slab_forces_bitwise(P, variant):
     F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
     st1 = one.stats()
     one.close()
-    sysm = make_system(w, q, p, P, variant, "f32")
+    sysm = make_system(w, q, p, P, variant, "f32", dev=dev)
     U, Wv, st = sysm.forces(True)
     _, _, F = gather_state(sysm, len(q), np.float32)
     assert np.array_equal(F, F1.cpu().numpy())
@@ -78,7 +80,8 @@ def test_slab_forces_bitwise(P, variant):
 
 
 @pytest.mark.parametrize("P", [2, 4])
-def test_slab_sllod_bitwise(P):
+@pytest.mark.parametrize("dev", [False, True])
+def test_slab_sllod_bitwise(P, dev):
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
 
@@ -93,7 +96,7 @@ def test_slab_sllod_bitwise(P):
     po = torch.empty_like(qo)
     one.get_state(qo, po)
     one.close()
-    sysm = make_system(w, q, p, P, "do", "f32")
+    sysm = make_system(w, q, p, P, "do", "f32", dev=dev)
     sysm.forces(False)
     out = None
     for _ in range(5):
@@ -108,7 +111,8 @@ def test_slab_sllod_bitwise(P):
 
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_slab_forces_bitwise_sparse_cells(P, variant):
+@pytest.mark.parametrize("dev", [False, True])
+def test_slab_forces_bitwise_sparse_cells(P, variant, dev):
     """Sparse WCA cells (C1, ~1.3 per cell): every rank and the single device run
     the row-segment pair kernel; forces, U, W and counts stay bitwise equal."""
     import torch
@@ -123,7 +127,7 @@ def test_slab_forces_bitwise_sparse_cells(P, variant):
     st1 = one.stats()
     assert one.pair_kernel_used() == "segment"
     one.close()
-    sysm = make_system(w, q, p, P, variant, "f32")
+    sysm = make_system(w, q, p, P, variant, "f32", dev=dev)
     U, Wv, st = sysm.forces(True)
     assert all(r.cl.pair_kernel_used() == "segment" for r in sysm.ranks)
     _, _, F = gather_state(sysm, len(q), np.float32)
@@ -134,15 +138,16 @@ def test_slab_forces_bitwise_sparse_cells(P, variant):
         r.close()
 
 
+@pytest.mark.parametrize("dev", [False, True])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_nccl_data_plane_self_ring_bitwise(variant):
+def test_nccl_data_plane_self_ring_bitwise(variant, dev):
     """The library's NCCL data plane (nc_slab_comm_init / nc_slab_exchange* / nc_slab_allgather) on a
     one-rank communicator: the ring neighbours are the rank itself, so every exchange and the
     all-gather run through NCCL on one GPU; forces and an SLLOD run stay bitwise equal to the
     single-device path."""
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
-    from paper_1412_3784_b200.slab import NcclTransport, SlabRank, SlabSystem
+    from paper_1412_3784_b200.slab import NcclTransport, SlabRank, SlabRankDev, SlabSystem
 
     w = W.make(2, scale=2)
     q = W.positions(w, dtype=np.float32, k=2)
@@ -157,8 +162,8 @@ def test_nccl_data_plane_self_ring_bitwise(variant):
     po = torch.empty_like(qo)
     one.get_state(qo, po)
     one.close()
-    sr = SlabRank(0, 1, variant=variant, prec="f32", rc=w.rc, u_shift=w.ushift, capacity=len(q),
-                  max_cells=4 * len(q) + 4096)
+    sr = (SlabRankDev if dev else SlabRank)(0, 1, variant=variant, prec="f32", rc=w.rc, u_shift=w.ushift,
+                                            capacity=len(q), max_cells=4 * len(q) + 4096)
     sr.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
     sr.load(q, p, np.arange(len(q), dtype=np.int32))
     sysm = SlabSystem([sr], NcclTransport(sr, 0, 1))
@@ -175,7 +180,8 @@ def test_nccl_data_plane_self_ring_bitwise(variant):
 
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_slab_repartition_when_l3_changes(P, variant):
+@pytest.mark.parametrize("dev", [False, True])
+def test_slab_repartition_when_l3_changes(P, variant, dev):
     """Generalized KR (uniaxial, fast strain): the cell-layer count l3 changes inside the run (the box
     stretches along v3 and a GKR reset remaps it), so slab ownership is recomputed and particles move
     by many layers (SlabSystem.repartition); the trajectory stays bitwise that of one device."""
@@ -202,7 +208,7 @@ def test_slab_repartition_when_l3_changes(P, variant):
     one.get_state(qo, po)
     one.close()
     assert len(set(l3s)) > 1, l3s  # the layer count really changes
-    sysm = make_system(w, q, p, P, variant, "f32")
+    sysm = make_system(w, q, p, P, variant, "f32", dev=dev)
     sysm.forces(False)
     for _ in range(nsteps):
         out = sysm.step(w.dt, True)
@@ -215,7 +221,8 @@ def test_slab_repartition_when_l3_changes(P, variant):
 
 
 @pytest.mark.parametrize("P", [2, 3])
-def test_slab_forces_bitwise_particle_per_thread_kernel(P):
+@pytest.mark.parametrize("dev", [False, True])
+def test_slab_forces_bitwise_particle_per_thread_kernel(P, dev):
     """The particle-per-thread sparse kernel (NC_PK_SPARSE) on every rank and on one device: its
     block partials are fixed particle ranges of one layer, so U and W stay bitwise P-invariant."""
     import torch
@@ -230,7 +237,7 @@ def test_slab_forces_bitwise_particle_per_thread_kernel(P):
     F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
     st1 = one.stats()
     one.close()
-    sysm = make_system(w, q, p, P, "do", "f32")
+    sysm = make_system(w, q, p, P, "do", "f32", dev=dev)
     for r in sysm.ranks:
         r.cl.pair_kernel("sparse")
     U, Wv, st = sysm.forces(True)
@@ -240,4 +247,57 @@ def test_slab_forces_bitwise_particle_per_thread_kernel(P):
     assert U == U1 and np.array_equal(Wv, W1)
     assert st["interactions"] == st1["interactions"] and st["candidates"] == st1["candidates"]
     for r in sysm.ranks:
+        r.close()
+
+
+def test_device_count_step_reads_nothing_back():
+    """The host-synchronization-free step: steps and force evaluations without energies issue no
+    device-to-host read from the Python side (torch's sync debug mode raises on one), the library side
+    never synchronizes either (its only synchronizing calls are nc_sd_status and a forces_end with
+    parts); the count read afterwards matches the particles."""
+    import torch
+
+    w = W.make(2, scale=2)
+    q = W.positions(w, dtype=np.float32, k=2)
+    p = W.momenta(w, dtype=np.float32, k=2)
+    sysm = make_system(w, q, p, 3, "do", "f32", dev=True)
+    sysm.forces(False)
+    torch.cuda.set_sync_debug_mode("error")
+    try:
+        for _ in range(4):
+            sysm.step(w.dt, False)
+    finally:
+        torch.cuda.set_sync_debug_mode("default")
+    assert sum(r.n for r in sysm.ranks) == len(q)
+    assert all(r.status()[1] == 0 for r in sysm.ranks)
+    for r in sysm.ranks:
+        r.close()
+
+
+def test_device_count_message_overflow_is_flagged():
+    """A halo message smaller than the boundary layer: the excess is dropped (never written out of
+    bounds) and nc_sd_status reports NC_E_OOM."""
+    from paper_1412_3784_b200.nemdcell import NcError
+    from paper_1412_3784_b200.slab import LoopbackTransport, SlabRankDev, SlabSystem, own_particles
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(2, scale=2)
+    q = W.positions(w, dtype=np.float32, k=2)
+    p = W.momenta(w, dtype=np.float32, k=2)
+    full = CellList("do", "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q), max_cells=4 * len(q) + 4096)
+    full.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    ranks = []
+    for r in range(2):
+        idx = own_particles(full, q, r, 2)
+        sr = SlabRankDev(r, 2, variant="do", prec="f32", rc=w.rc, u_shift=w.ushift, capacity=len(q), hcap=64,
+                         max_cells=4 * len(q) + 4096)
+        sr.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+        sr.load(q[idx], p[idx], idx.astype(np.int32))
+        ranks.append(sr)
+    full.close()
+    sysm = SlabSystem(ranks, LoopbackTransport())
+    sysm.forces(False)
+    with pytest.raises(NcError, match="NC_E_OOM"):
+        ranks[0].status()
+    for r in ranks:
         r.close()
