@@ -431,9 +431,11 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
       const uint64_t hs = acc.hs, hx = acc.hx;
       if (act) {
         const double Ui = 2.0 * g.eps * uu - 0.5 * g.ushift * (double)cnt;
-        Fout[me] = make_float4((float)(g.Q[0] * fx + g.Q[1] * fy + g.Q[2] * fz),
-                               (float)(g.Q[3] * fx + g.Q[4] * fy + g.Q[5] * fz),
-                               (float)(g.Q[6] * fx + g.Q[7] * fy + g.Q[8] * fz), __uint_as_float(cnt));
+        const float4 fv = make_float4((float)(g.Q[0] * fx + g.Q[1] * fy + g.Q[2] * fz),
+                                      (float)(g.Q[3] * fx + g.Q[4] * fy + g.Q[5] * fz),
+                                      (float)(g.Q[6] * fx + g.Q[7] * fy + g.Q[8] * fz), __uint_as_float(cnt));
+        Fout[me] = fv;
+        store_user_F(po, gid, me, fv);
         if (DIGEST) { dcnt[me] = cnt; dhs[me] = hs; dhx[me] = hx; }
         tU += Ui;
         tW[0] += 0.5 * w0; tW[1] += 0.5 * w1; tW[2] += 0.5 * w2;

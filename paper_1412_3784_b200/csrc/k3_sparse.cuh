@@ -416,9 +416,12 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if (DIGEST) { acc.hs = sm.hs[tid]; acc.hx = sm.hx[tid]; }
     if (act) {
       const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
-      Fout[me] = make_float4((float)(g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz),
-                             (float)(g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz),
-                             (float)(g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz), __uint_as_float(acc.cnt));
+      const float4 fv = make_float4((float)(g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz),
+                                    (float)(g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz),
+                                    (float)(g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz),
+                                    __uint_as_float(acc.cnt));
+      Fout[me] = fv;
+      store_user_F(po, gid, me, fv);
       if (DIGEST) { dcnt[me] = acc.cnt; dhs[me] = acc.hs; dhx[me] = acc.hx; }
       sm.tuw[0][tid] += Ui;
       sm.tuw[1][tid] += 0.5 * acc.w0; sm.tuw[2][tid] += 0.5 * acc.w1; sm.tuw[3][tid] += 0.5 * acc.w2;

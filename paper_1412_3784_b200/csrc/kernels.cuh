@@ -489,7 +489,19 @@ struct PairOut {
   int32_t* ijn;            // 5 x int32 per pair: gid_i, gid_j, n1, n2, n3
   unsigned long long* n;   // pairs found (may exceed cap: the host reports the count)
   long long cap;
+  void* fu = nullptr;      // user-order forces (n x 3 of T, index = gid): the owner writes F there too,
+                           // so an evaluation from user positions needs no separate unsort pass
 };
+// F of particle `me` (sorted) into the user-order output at its gid (scattered; overlapped with K3's work)
+template <typename V>
+__device__ __forceinline__ void store_user_F(const PairOut& po, const uint32_t* __restrict__ gid, uint32_t me,
+                                             const V& f) {
+  if (po.fu) {
+    using T = decltype(f.x);
+    T* d = (T*)po.fu + 3 * (size_t)gid[me];
+    d[0] = f.x; d[1] = f.y; d[2] = f.z;
+  }
+}
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -1407,7 +1419,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
           const double Fx = g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz;
           const double Fy = g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz;
           const double Fz = g.Q[6] * acc.fx + g.Q[7] * acc.fy + g.Q[8] * acc.fz;
-          Fout[pc.my] = mk4((T)Fx, (T)Fy, (T)Fz, idx_to_w(acc.cnt, T()));
+          const typename V4<T>::t fv = mk4((T)Fx, (T)Fy, (T)Fz, idx_to_w(acc.cnt, T()));
+          Fout[pc.my] = fv;
+          store_user_F(pc.po, gid, pc.my, fv);
           if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
           tU += Ui;
           tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
@@ -1492,7 +1506,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         const bool owner = (lane < nb);
         const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
         if (owner) {
-          Fout[pc.my] = mk4((T)acc.fx, (T)acc.fy, (T)acc.fz, idx_to_w(acc.cnt, T()));
+          const typename V4<T>::t fv = mk4((T)acc.fx, (T)acc.fy, (T)acc.fz, idx_to_w(acc.cnt, T()));
+          Fout[pc.my] = fv;
+          store_user_F(pc.po, gid, pc.my, fv);
           if (DIGEST) { dcnt[pc.my] = acc.cnt; dhs[pc.my] = acc.hs; dhx[pc.my] = acc.hx; }
           tU += Ui;
           tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;

@@ -83,6 +83,7 @@ struct nc_ctx {
   int64_t slab_n_own = 0, slab_n1 = 0, slab_n2 = 0, slab_b_own = 0;
   int slab_klo = 0, slab_khi = 0;
   bool slab_open = false;
+  void* fuser = nullptr;  // user-order force output of the evaluation in flight (the pair kernel writes it)
   // host-synchronization-free slab step (csrc/slab_dc.cuh): device counters and host-side bookkeeping
   uint32_t* sd = nullptr;
   int64_t sd_ncap = 0, sd_hcap = 0, sd_H = 0, sd_n_hint = 0;
@@ -385,7 +386,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
-  const PairOut po = DIGEST ? ctx->po : PairOut{nullptr, nullptr, 0};
+  const PairOut po = DIGEST ? ctx->po : PairOut{nullptr, nullptr, 0, ctx->fuser};
   prof_begin(ctx);
   double* bp = nullptr;  // set once bpl is final (below)
   if constexpr (sizeof(T) == 4) {
@@ -526,12 +527,14 @@ template <typename T>
 nc_status compute_user(nc_ctx* ctx, const void* q, int64_t n, void* F, double* U, double* W) {
   nc_status st = build_user<T>(ctx, q, n);
   if (st) return st;
+  // the pair kernel writes F straight into the user order (device F, or the io_b staging buffer)
+  const bool dev = F && is_device_ptr(F);
+  ctx->fuser = F ? (dev ? F : ctx->io_b) : nullptr;
   st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF);
+  ctx->fuser = nullptr;
   if (st) return st;
-  if (F) {
-    st = unsort_out<T>(ctx, ctx->sF, ctx->sgid, n, F);
-    if (st) return st;
-  }
+  if (F && !dev && n > 0)
+    CK(cudaMemcpyAsync(F, ctx->io_b, 3 * sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
   st = check_finite(ctx);  // synchronizes the stream
   if (st) return st;
   totals_to_UW(ctx, U, W);
@@ -568,12 +571,10 @@ nc_status compute_async_t(nc_ctx* ctx, const void* q, int64_t n, void* F) {
   nc_status st = build_user<T>(ctx, ctx->ain[b], n);
   if (st) return st;
   CK(cudaEventRecord(ctx->ev_in_free[b], s));
+  ctx->fuser = F ? ctx->aout[b] : nullptr;  // the pair kernel writes F in the user order
   st = launch_pairs<T, false>(ctx, (const typename V4<T>::t*)ctx->sq, ctx->sgid, (typename V4<T>::t*)ctx->sF);
+  ctx->fuser = nullptr;
   if (st) return st;
-  if (F) {
-    st = unsort_out<T>(ctx, ctx->sF, ctx->sgid, n, ctx->aout[b]);
-    if (st) return st;
-  }
   CK(cudaEventRecord(ctx->ev_out_ready[b], s));
   // copy out
   CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[b], 0));

@@ -1,5 +1,5 @@
 # A/B of k_pairs_sparse build variants (NC_LIB) on C1/C3, DO and DS
-for lib in varlib/*.so; do for c in 3; do for v in do ds do ds; do
+for lib in varlib/*.so; do for c in 3; do for v in do ds; do
 NC_LIB=$lib python - <<PY
 import sys, numpy as np, torch
 sys.path.insert(0,'.')
