@@ -1909,6 +1909,17 @@ __global__ void k_wrap_key_src(int64_t n, const T* __restrict__ qin, int stride,
   slot[off + i] = arrival_slot(counts, c);
 }
 
+// positions of the caller's particles in a given order (build_user): slot s takes caller index perm[s]
+template <typename T>
+__global__ void k_pregather(int64_t n, const T* __restrict__ q, const uint32_t* __restrict__ perm, T* __restrict__ qo,
+                            uint32_t* __restrict__ go) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const uint32_t i = perm[s];
+  qo[3 * s] = q[3 * (int64_t)i]; qo[3 * s + 1] = q[3 * (int64_t)i + 1]; qo[3 * s + 2] = q[3 * (int64_t)i + 2];
+  go[s] = i;
+}
+
 // F of the own particles back to their input order (sorted slot -> original local index)
 template <typename T>
 __global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ src, const uint32_t* __restrict__ sidx,

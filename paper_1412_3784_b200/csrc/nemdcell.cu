@@ -84,6 +84,10 @@ struct nc_ctx {
   int slab_klo = 0, slab_khi = 0;
   bool slab_open = false;
   void* fuser = nullptr;  // user-order force output of the evaluation in flight (the pair kernel writes it)
+  // the previous user evaluation's sorted order (build_user pre-gathers the next input through it)
+  uint32_t *perm = nullptr, *pgid = nullptr;
+  void* pq = nullptr;
+  int64_t perm_n = -1;
   // host-synchronization-free slab step (csrc/slab_dc.cuh): device counters and host-side bookkeeping
   uint32_t* sd = nullptr;
   int64_t sd_ncap = 0, sd_hcap = 0, sd_H = 0, sd_n_hint = 0;
@@ -500,9 +504,33 @@ nc_status build_user(nc_ctx* ctx, const void* q, int64_t n) {
   const void* qd = nullptr;
   nc_status st = stage_in(ctx, q, ctx->io_a, n, &qd);
   if (st) return st;
-  st = launch_build<T>(ctx, (const T*)qd, 3, (typename V4<T>::t*)ctx->wq, n, nullptr, nullptr,
-                       (typename V4<T>::t*)ctx->sq, nullptr, ctx->sgid);
+  // A caller's particles keep their order from call to call (and move little): the previous call's
+  // sorted order (sorted slot -> caller index) pre-gathers this call's positions, so the counting sort
+  // sees an almost sorted input (coalesced scatter and gathers instead of random ones).  Only the
+  // ORDER of the input changes -- the gids are the caller's indices, the (cell, gid) sort and every
+  // result are exactly those without it.
+  const T* src = (const T*)qd;
+  const uint32_t* gsrc = nullptr;
+  if (n > 0 && ctx->perm_n == n) {
+    prof_begin(ctx);
+    k_pregather<T><<<nblk(n, 256), 256, 0, ctx->stream>>>(n, (const T*)qd, ctx->perm, (T*)ctx->pq, ctx->pgid);
+    LAUNCHED();
+    prof_end(ctx, NC_K_OTHER);
+    src = (const T*)ctx->pq;
+    gsrc = ctx->pgid;
+  }
+  st = launch_build<T>(ctx, src, 3, (typename V4<T>::t*)ctx->wq, n, gsrc, nullptr, (typename V4<T>::t*)ctx->sq,
+                       nullptr, ctx->sgid);
   if (st) return st;
+  if (n > 0) {  // this call's sorted order (the sorted gids ARE caller indices) for the next call
+    if (!ctx->perm) {
+      CK(cudaMalloc(&ctx->perm, sizeof(uint32_t) * (size_t)ctx->cap));
+      CK(cudaMalloc(&ctx->pgid, sizeof(uint32_t) * (size_t)ctx->cap));
+      CK(cudaMalloc(&ctx->pq, 3 * sizeof(T) * (size_t)ctx->cap));
+    }
+    CK(cudaMemcpyAsync(ctx->perm, ctx->sgid, sizeof(uint32_t) * (size_t)n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->perm_n = n;
+  }
   ctx->last_resident = false;
   return NC_OK;
 }
@@ -1123,7 +1151,8 @@ void nc_destroy(nc_ctx* ctx) {
                 ctx->wq, ctx->sq, ctx->sgid, ctx->sF, ctx->io_a, ctx->io_b, ctx->u, ctx->u32, ctx->nh, ctx->key, ctx->slot,
                 ctx->srec, ctx->counts, ctx->cs, ctx->bsum, ctx->tot, ctx->bpart, ctx->lpart,
                 ctx->part_tot, ctx->part_acc, ctx->rcount, ctx->dcnt, ctx->dhs, ctx->dhx, ctx->hist,
-                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot, ctx->sd};
+                ctx->gin, ctx->sidx, ctx->cls, ctx->pbcnt, ctx->pboff, ctx->ptot, ctx->sd,
+                ctx->perm, ctx->pgid, ctx->pq};
   for (void* p : ps)
     if (p) cudaFree(p);
   if (ctx->s_h2d) {
