@@ -301,3 +301,38 @@ def test_device_count_message_overflow_is_flagged():
         ranks[0].status()
     for r in ranks:
         r.close()
+
+
+@pytest.mark.parametrize("dev", [False, True])
+@pytest.mark.parametrize("variant", ["do", "ds"])
+def test_slab_fp64_forces_and_steps_bitwise(variant, dev):
+    """NC_F64 through the slab paths (host-count and host-synchronization-free): C2 scaled to 32,768 LJ
+    particles in its KR box, P = 2: forces, U, W and 3 SLLOD steps bitwise equal to one device."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(2, scale=2)
+    q = W.positions(w, dtype=np.float64, k=2)
+    p = W.momenta(w, dtype=np.float64, k=2)
+    one = CellList(variant, "f64", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
+    one.set_state(torch.from_numpy(q).cuda(), torch.from_numpy(p).cuda())
+    Us, Ws = one.step(w.dt, 3)
+    qo = torch.empty((len(q), 3), dtype=torch.float64, device="cuda")
+    po = torch.empty_like(qo)
+    one.get_state(qo, po)
+    one.close()
+    sysm = make_system(w, q, p, 2, variant, "f64", dev=dev)
+    U, Wv, _ = sysm.forces(True)
+    _, _, F = gather_state(sysm, len(q), np.float64)
+    assert np.array_equal(F, F1.cpu().numpy())
+    assert U == U1 and np.array_equal(Wv, W1)
+    out = None
+    for _ in range(3):
+        out = sysm.step(w.dt, True)
+    qs, ps, _ = gather_state(sysm, len(q), np.float64)
+    assert np.array_equal(qs, qo.cpu().numpy()) and np.array_equal(ps, po.cpu().numpy())
+    assert out[0] == Us and np.array_equal(out[1], Ws)
+    for r in sysm.ranks:
+        r.close()
