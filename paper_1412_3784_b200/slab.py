@@ -36,7 +36,8 @@ class SlabRank:
     """State of one rank: own particles (device tensors), its context, buffers."""
 
     def __init__(self, rank: int, nranks: int, *, variant="do", prec="f32", rc=2.5, eps=1.0, sigma=1.0,
-                 u_shift=None, mass=1.0, capacity=1 << 16, max_cells=0, device=0, stream=None, ctx_capacity=None):
+                 u_shift=None, mass=1.0, capacity=1 << 16, max_cells=0, device=0, stream=None, ctx_capacity=None,
+                 count_buffers=True):
         import torch
 
         self.torch = torch
@@ -53,10 +54,11 @@ class SlabRank:
         self.gid = torch.zeros(capacity, dtype=torch.int32, device=self.dev)
         self.gid2 = torch.zeros_like(self.gid)
         self.bcap = max(4096, capacity // 4)
-        self.send = [t(self.bcap, 8), t(self.bcap, 8)]           # migration records to r-1, r+1
-        self.recv = [t(self.bcap, 8), t(self.bcap, 8)]           # from r-1, r+1
-        self.hsend = [t(self.bcap, 4), t(self.bcap, 4)]          # halo records to r-1, r+1
-        self.hrecv = [t(self.bcap, 4), t(self.bcap, 4)]
+        if count_buffers:  # the host-count step's record buffers (SlabRankDev has its own messages)
+            self.send = [t(self.bcap, 8), t(self.bcap, 8)]           # migration records to r-1, r+1
+            self.recv = [t(self.bcap, 8), t(self.bcap, 8)]           # from r-1, r+1
+            self.hsend = [t(self.bcap, 4), t(self.bcap, 4)]          # halo records to r-1, r+1
+            self.hrecv = [t(self.bcap, 4), t(self.bcap, 4)]
         self.n = 0
         self.pending_dt = 0.0  # a deferred closing half kick (see kick)
         self.last_l3 = None    # cell layers of the box the particles were last distributed on
@@ -177,7 +179,7 @@ class SlabRankDev(SlabRank):
         hcap = int(hcap or max(4096, capacity // 4))
         mcap = int(mcap or max(4096, capacity // 16))
         # the context indexes own + two halo layers' worth of slots
-        super().__init__(rank, nranks, capacity=capacity, ctx_capacity=capacity + 2 * hcap, **kw)
+        super().__init__(rank, nranks, capacity=capacity, ctx_capacity=capacity + 2 * hcap, count_buffers=False, **kw)
         torch = self.torch
         t = lambda *s: torch.zeros(*s, dtype=self.dtype, device=self.dev)  # noqa: E731
         self.hcap, self.mcap = hcap, mcap
