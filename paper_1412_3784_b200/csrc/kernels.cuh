@@ -1037,23 +1037,28 @@ __device__ __forceinline__ void mma_filter(uint32_t stage0, uint32_t hw0, int W,
     for (int k = 0; k < 16; ++k) mma_step(b[k], a0, a1, c, m0, m1);
     const uint32_t x = __shfl_xor_sync(0xffffffffu, lo ? m1 : m0, 2);
     const uint32_t ma = lo ? m0 : x, mb = lo ? x : m1;  // streams s = t & 1 and s + 2
-    stsu(o0 + 8u * (uint32_t)w, (spread2(ma >> 16) << 2) | spread2(mb >> 16));               // blocks 0-7
-    stsu(o0 + 8u * (uint32_t)w + 4u, (spread2(ma & 0xffffu) << 2) | spread2(mb & 0xffffu));  // blocks 8-15
+    // stored bit-reversed (bit p = 31 - c): pop_hit takes the highest set bit p without a 31 - x
+    stsu(o0 + 8u * (uint32_t)w, __brev((spread2(ma >> 16) << 2) | spread2(mb >> 16)));               // blocks 0-7
+    stsu(o0 + 8u * (uint32_t)w + 4u, __brev((spread2(ma & 0xffffu) << 2) | spread2(mb & 0xffffu)));  // blocks 8-15
   }
 }
 
-// Hit cursor over one far lane's words (mma_filter's layout): bit c = 2q + h of the current word is the
-// staged element at address wa + 16 q + 4 h = wa + 4 c + 8 (c >> 1); pop the highest hit and refill the
-// word when it empties (predicated: next word +4 bytes, element base +64 elements).
+// Hit cursor over one far lane's words (mma_filter's layout, stored bit-reversed): bit position c = 2q + h
+// of the current word is the staged element at address wa + 16 q + 4 h = wa + 4 c + 8 (c >> 1); pop the
+// highest hit and refill the word when it empties (predicated: next word +4 bytes, element base +64).
 struct HitCur {
   uint32_t cur, wa, wq, wend;
 };
 __device__ __forceinline__ uint32_t pop_hit(HitCur& h, bool& valid) {
+  // words are stored bit-reversed, so bit POSITION p is element index c = p: the highest set bit
+  // (bfind, no 31 - x) is the element at wa + 4p + 8(p >> 1)
   valid = h.cur != 0;
-  const uint32_t c = (uint32_t)__clz(h.cur);  // highest hit (32 if none)
-  h.cur ^= 0x80000000u >> c;                  // shift by 32 gives 0: nothing to clear
-  const uint32_t cc = valid ? c : 0u;         // idle lanes read their word's first element: finite, masked
-  const uint32_t a = h.wa + 4u * cc + 8u * (cc >> 1);
+  uint32_t p, m;
+  asm("bfind.u32 %0, %1;" : "=r"(p) : "r"(h.cur));           // highest set bit (0xffffffff if none)
+  asm("shl.b32 %0, %1, %2;" : "=r"(m) : "r"(1u), "r"(p));     // shifts >= 32 give 0: nothing to clear
+  h.cur ^= m;
+  const uint32_t pp = valid ? p : 0u;  // idle lanes read their word's first element: finite, masked
+  const uint32_t a = h.wa + 4u * pp + 8u * (pp >> 1);
   if (h.cur == 0 && h.wq < h.wend) {
     h.cur = ldsu(h.wq);
     h.wq += 4u;
