@@ -277,7 +277,10 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
   g.band_hi = g.rc2 * (1.0 + tau);
   // two-tier evaluation: fp32 force math only where the LJ force is small
   // (r >= 1.2 sigma: |f| <= 2.4 eps/sigma), fp64 for closer pairs
-  g.rsplit2 = 1.44 * g.sig2;
+  // r_split = 1.2 sigma: the fp32 far tier's position rounding costs <= ~3e-5 eps/sigma per pair above it
+  // (NC_RSPLIT: an experiment override, in units of sigma)
+  static const double rsplit_env = [] { const char* e = getenv("NC_RSPLIT"); return e ? atof(e) : 1.2; }();
+  g.rsplit2 = rsplit_env * rsplit_env * g.sig2;
   g.f_split2 = (float)g.rsplit2;
   g.f_lo = (float)g.band_lo;
   g.f_hi = (float)g.band_hi;
