@@ -414,6 +414,7 @@ k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restri
 #ifndef K3_PF_L2
 #define K3_PF_L2 1  // L2 prefetch of the staged particles' fp64 coordinates (close tier): fluid -0.5%, lattice +0.4%
 #endif
+constexpr int K3_F64_SPLIT_B = 8;  // NC_F64 small grids: particles per i-batch when blocks share a cell
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 64;  // permanent far element (padding slot of the evaluation)
 constexpr int K3_STAGE = K3_CAP + 66;  // fp64 mode: + up to S far sentinels so the filter needs no bounds checks
@@ -1233,8 +1234,11 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
   const int layer = layer0 + (int)(blockIdx.x / bpl);  // global cell layer (slab mode: owned layers only)
   const int chunk = (int)blockIdx.x - (layer - layer0) * bpl;
   const int per_layer = l1 * l2;
-  const int cbeg = chunk * cpb;
-  const int cend = min(per_layer, cbeg + cpb);
+  // cpb < 0 (NC_F64 on small grids): -cpb blocks share one cell, block `sub` taking its i-batches
+  // sub, sub + nsplit, ... of K3_F64_SPLIT_B particles -- more warps in flight when the grid has few cells
+  const int nsplit = cpb < 0 ? -cpb : 1, sub = cpb < 0 ? chunk % nsplit : 0;
+  const int cbeg = cpb < 0 ? chunk / nsplit : chunk * cpb;
+  const int cend = cpb < 0 ? cbeg + 1 : min(per_layer, cbeg + cpb);
 
   PairCtx<T> pc;
   pc.hi = (T)g.band_hi;
@@ -1288,11 +1292,11 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
       tot += __shfl_sync(0xffffffffu, x, 31);
     }
     __syncwarp();
-    tS += (double)nst;
+    if (sub == 0) tS += (double)nst;  // cell-level statistics once per cell
     const uint32_t ibase = cs[cid];
     const int ni = (int)(cs[cid + 1] - ibase);
     if (ni == 0) continue;
-    tC += (double)ni * (double)tot - (double)ni;
+    if (sub == 0) tC += (double)ni * (double)tot - (double)ni;
 
     if constexpr (sizeof(T) == 4) {
       // ---------------- NC_F32: tensor-core filter, packed fp32 far tier, fp64 close tier
@@ -1446,8 +1450,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
       }
     } else {
       // ---------------- NC_F64: canonical fp64 filter on every candidate, error-free d
-      for (int ib = 0; ib < ni; ib += 32) {
-        const int nb = min(32, ni - ib);
+      const int fb = nsplit > 1 ? K3_F64_SPLIT_B : 32;  // particles per i-batch
+      for (int ib = sub * fb; ib < ni; ib += nsplit * fb) {
+        const int nb = min(fb, ni - ib);
         const int S = 32 / nb;               // streams over the j list
         const int il = lane % nb;
         const bool act = lane < S * nb;

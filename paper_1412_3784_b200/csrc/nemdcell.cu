@@ -201,6 +201,10 @@ bool defer_kick() {
 // K3_MIN_BLOCKS blocks (~32 waves of resident warps).  It depends on the global grid only, so
 // every rank of a slab decomposition groups the same cells (bitwise-equal partial sums).
 constexpr int64_t K3_MIN_BLOCKS = 75776;
+// NC_F64 on grids below K3_F64_SPLIT_CELLS cells (fewer than ~4 waves of one-warp blocks): each cell's
+// i-batches of 8 are spread over K3_F64_SPLIT blocks (a function of the global grid only: P-invariant)
+constexpr int64_t K3_F64_SPLIT_CELLS = 8192;
+constexpr int K3_F64_SPLIT = 4;
 int cells_per_block(const Geom& g) {
   int cpb = K3_CELLS;
   while (cpb * 2 <= K3_CELLS_MAX && g.ncells / (cpb * 2) >= K3_MIN_BLOCKS) cpb *= 2;
@@ -390,6 +394,10 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   if (nlay < 0) nlay = g.dims[2];
   int cpb = cells_per_block(g);
   int bpl = (int)((((int64_t)g.dims[0] * g.dims[1]) + cpb - 1) / cpb);
+  if (sizeof(T) == 8 && g.ncells < K3_F64_SPLIT_CELLS) {  // NC_F64 on a small grid: 4 blocks per cell
+    cpb = -K3_F64_SPLIT;
+    bpl = (int)((int64_t)g.dims[0] * g.dims[1] * K3_F64_SPLIT);
+  }
   int nblocks = bpl * nlay;
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
