@@ -242,7 +242,8 @@ nc_status nc_get_stencil_histogram(nc_ctx *ctx, int64_t hist[64]);
 /* Live per-kernel timing with CUDA events recorded on cfg.stream around
  * every launch of the path (enable = 1 starts a fresh accumulation, 0 stops;
  * enable = 3 also makes k_pairs count its fp32-tier interactions, reported in
- * nc_stats.interactions_fp32 -- a separate, ~1% slower instantiation).
+ * nc_stats.interactions_fp32 -- a separate, ~1% slower instantiation; bit 4 (enable = 5) times the
+ * pair kernel only: two events per evaluation, the least instrumentation inside a timed region).
  * nc_profile_read synchronizes the stream and returns, per kernel id
  * (NC_K_*), the summed device milliseconds and the launch counts. */
 enum { NC_K_WRAPKEY = 0, NC_K_SCAN = 1, NC_K_SCATTER = 2, NC_K_RANKGATHER = 3, NC_K_PAIRS = 4, NC_K_REDUCE = 5,

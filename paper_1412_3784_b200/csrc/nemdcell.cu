@@ -117,6 +117,7 @@ struct nc_ctx {
 
   // live kernel timing (nc_profile)
   bool prof = false;
+  bool prof_pairs_only = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t prof_start = nullptr;
@@ -164,13 +165,15 @@ cudaEvent_t pool_event(nc_ctx* ctx) {
 }
 
 // RAII-free helpers: mark the start / end of one kernel launch of kind k
-inline void prof_begin(nc_ctx* ctx) {
-  if (!ctx->prof) return;
+// (k: the kernel about to be timed; in pairs-only mode (nc_profile bit 4) only K3 gets events, so the
+// instrumentation of a timed region is two events per evaluation)
+inline void prof_begin(nc_ctx* ctx, int k = -1) {
+  if (!ctx->prof || (ctx->prof_pairs_only && k != NC_K_PAIRS)) return;
   ctx->prof_start = pool_event(ctx);
   cudaEventRecord(ctx->prof_start, ctx->stream);
 }
 inline void prof_end(nc_ctx* ctx, int k) {
-  if (!ctx->prof) return;
+  if (!ctx->prof || (ctx->prof_pairs_only && k != NC_K_PAIRS)) return;
   cudaEvent_t e = pool_event(ctx);
   cudaEventRecord(e, ctx->stream);
   ctx->prof_ev.push_back({k, {ctx->prof_start, e}});
@@ -402,7 +405,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   size_t smem = sizeof(K3Smem<T>);
   (void)nblocks;
   const PairOut po = DIGEST ? ctx->po : PairOut{nullptr, nullptr, 0, ctx->fuser};
-  prof_begin(ctx);
+  prof_begin(ctx, NC_K_PAIRS);
   double* bp = nullptr;  // set once bpl is final (below)
   if constexpr (sizeof(T) == 4) {
     const int Gseg = sparse_kind(ctx, g) == 1 ? seg_cells(ctx, g) : 0;
@@ -1047,6 +1050,7 @@ nc_status nc_profile(nc_ctx* ctx, int enable) {
   }
   ctx->prof = enable != 0;
   ctx->count_tiers = (enable & 2) != 0;
+  ctx->prof_pairs_only = (enable & 4) != 0;
   if (enable) ctx->prof_ev.reserve(4096);
   return NC_OK;
 }
