@@ -257,6 +257,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
                const uint32_t* __restrict__ gid, float4* __restrict__ Fout, double* __restrict__ bpart,
                uint32_t* __restrict__ dcnt, uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx,
                const __grid_constant__ Geom g, int bpl, int layer0, const PairOut po) {
+  PDL_ENTRY();
   __shared__ SpSmem sm;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int l1 = g.dims[0], l2 = g.dims[1];

@@ -33,6 +33,15 @@
 
 namespace nc {
 
+// Programmatic dependent launch (sm_90+): the step's kernels are launched with programmatic stream
+// serialization, so the next kernel's grid is set up while this one drains; every such kernel waits
+// for its predecessor's completion (and memory) before its first dependent access, and lets its
+// successor launch as soon as all its own blocks have started.  Without the launch attribute both are
+// no-ops.
+#define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" :::)
+#define PDL_ENTRY() do { PDL_WAIT(); PDL_LAUNCH(); } while (0)
+
 template <typename T> struct V4;
 template <> struct V4<float> { using t = float4; };
 template <> struct V4<double> { using t = double4; };
@@ -172,6 +181,7 @@ template <typename T>
 __global__ void k_wrap_key(int64_t n, const T* __restrict__ qin, int stride, typename V4<T>::t* __restrict__ qout,
                            uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
                            const __grid_constant__ Geom g) {
+  PDL_ENTRY();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double q0 = (double)qin[i * stride], q1 = (double)qin[i * stride + 1], q2 = (double)qin[i * stride + 2];
@@ -187,6 +197,7 @@ __global__ void k_wrap_key(int64_t n, const T* __restrict__ qin, int stride, typ
 constexpr int SCAN_T = 256, SCAN_E = 8, SCAN_TILE = SCAN_T * SCAN_E;
 
 __global__ void k_scan_reduce(const uint32_t* __restrict__ in, int64_t m, uint32_t* __restrict__ bsum) {
+  PDL_ENTRY();
   __shared__ uint32_t s[SCAN_T / 32];
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
   uint32_t acc = 0;
@@ -206,6 +217,7 @@ __global__ void k_scan_reduce(const uint32_t* __restrict__ in, int64_t m, uint32
 
 // single block: exclusive scan of nb block sums in place; total to *tot
 __global__ void k_scan_bsums(uint32_t* __restrict__ bsum, int64_t nb, uint32_t* __restrict__ tot) {
+  PDL_ENTRY();
   __shared__ uint32_t carry_s;
   __shared__ uint32_t wsum[32];
   if (threadIdx.x == 0) carry_s = 0;
@@ -244,6 +256,7 @@ __global__ void k_scan_bsums(uint32_t* __restrict__ bsum, int64_t nb, uint32_t* 
 // out[i] = exclusive prefix of in; out[m] = total (out has m+1 entries)
 __global__ void k_scan_apply(const uint32_t* __restrict__ in, int64_t m, const uint32_t* __restrict__ bsum,
                              uint32_t* __restrict__ out, const uint32_t* __restrict__ tot) {
+  PDL_ENTRY();
   __shared__ uint32_t wsum[SCAN_T / 32];
   __shared__ uint32_t carry_s;
   int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
@@ -294,6 +307,7 @@ constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_R = 32, SCAN_SMALL = SCAN_SMALL_R 
 __host__ __device__ constexpr int scan_pad(int i) { return i + (i >> 5); }
 __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __restrict__ in, int64_t m,
                                                              uint32_t* __restrict__ out) {
+  PDL_ENTRY();
   extern __shared__ uint32_t sbuf[];  // scan_pad(SCAN_SMALL) words
   __shared__ uint32_t wsum[SCAN_SMALL_T / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -336,7 +350,14 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __r
 // bucket each particle at (cell_start[key] + arrival slot); carry its gid
 __global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ cs, const uint32_t* __restrict__ gid_in,
-                          uint4* __restrict__ rec, int64_t i0 = 0, const uint32_t* __restrict__ dn = nullptr) {
+                          uint4* __restrict__ rec, int64_t i0 = 0, const uint32_t* __restrict__ dn = nullptr,
+                          uint32_t* __restrict__ zero = nullptr, int64_t nzero = 0) {
+  PDL_ENTRY();
+  // zero: the cell counts, consumed by the scan before this kernel, cleared for the next step's
+  // histogram (one memset fewer per step, so the step's launches chain without a break)
+  if (zero)
+    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nzero; c += (int64_t)gridDim.x * blockDim.x)
+      zero[c] = 0u;
   // particles [i0, i0 + n) (a slab evaluation scatters its own and its halo particles separately).
   // One 16-byte record per particle (source index, gid, cell): a random-order input costs one sector
   // per particle, not three; k_rank_gather reads the records in bucket order (coalesced)
@@ -373,6 +394,7 @@ k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restri
                               float4* __restrict__ u32_out, uint32_t* __restrict__ nh_out,
                               const __grid_constant__ Geom g, uint32_t* __restrict__ idx_out = nullptr,
                               int64_t s0 = 0, const uint32_t* __restrict__ drange = nullptr) {
+  PDL_ENTRY();
   // bucket positions [s0, s0 + n) (a slab evaluation places own and halo particles in two phases);
   // drange: [drange[0], drange[1]) from the device (the grid covers a capacity)
   int64_t send = s0 + n;
@@ -1226,6 +1248,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
         uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl,
         int layer0, const PairOut po) {
+  PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lane = threadIdx.x & 31;
   K3Smem<T>& sm = *reinterpret_cast<K3Smem<T>*>(smraw);
@@ -1578,6 +1601,7 @@ constexpr int K3R_T = 256;
 __global__ void __launch_bounds__(K3R_T) k_reduce(const double* __restrict__ bpart, int bpl, int nlayers,
                                                   double* __restrict__ lpart, double* __restrict__ tot,
                                                   double* __restrict__ acc, unsigned int* __restrict__ counter) {
+  PDL_ENTRY();
   __shared__ double wred[K3R_T / 32][NPART];
   __shared__ bool last;
   const int layer = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1705,6 +1729,7 @@ __global__ void __launch_bounds__(256, KDK_MINB) k_kick_drift_key(int64_t n, typ
                                  const typename V4<T>::t* __restrict__ F, SllodParams sp, const __grid_constant__ Geom g,
                                  uint32_t* __restrict__ key, uint32_t* __restrict__ slot, uint32_t* __restrict__ counts,
                                  int pending = 0, const K3Kick pk = K3Kick{}) {
+  PDL_ENTRY();
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   typename V4<T>::t qi = q[i], pi = p[i], fi = F[i];

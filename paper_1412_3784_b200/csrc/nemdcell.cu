@@ -118,6 +118,7 @@ struct nc_ctx {
   // live kernel timing (nc_profile)
   bool prof = false;
   bool prof_pairs_only = false;
+  int64_t counts_clean = 0;  // counts[0, counts_clean) known to be zero (cleared by the step's scatter)
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_ev;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t prof_start = nullptr;
@@ -180,6 +181,27 @@ inline void prof_end(nc_ctx* ctx, int k) {
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Launch with programmatic stream serialization (PDL, kernels.cuh PDL_ENTRY): the next grid is set up
+// while this one drains.  NC_PDL=0 turns it off (A/B).  Every argument is passed explicitly.
+inline bool pdl_on() {
+  static const bool on = [] { const char* e = getenv("NC_PDL"); return !(e && e[0] == '0'); }();
+  return on;
+}
+template <typename... P, typename... A>
+inline cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... a) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...);
+}
 
 bool is_device_ptr(const void* p) {
   if (!p) return false;
@@ -330,15 +352,17 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
 nc_status launch_scan_raw(nc_ctx* ctx, const uint32_t* in, int64_t m, uint32_t* out) {
   cudaStream_t s = ctx->stream;
   if (m <= SCAN_SMALL) {
-    k_scan_small<<<1, SCAN_SMALL_T, sizeof(uint32_t) * (size_t)scan_pad((int)m + 32), s>>>(in, m, out);
+    launch_pdl(k_scan_small, dim3(1), dim3(SCAN_SMALL_T), sizeof(uint32_t) * (size_t)scan_pad((int)m + 32), s, in, m,
+               out);
     LAUNCHED();
   } else {
     const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
-    k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, s>>>(in, m, ctx->bsum);
+    launch_pdl(k_scan_reduce, dim3((unsigned)nb), dim3(SCAN_T), 0, s, in, m, ctx->bsum);
     LAUNCHED();
-    k_scan_bsums<<<1, 1024, 0, s>>>(ctx->bsum, nb, ctx->tot);
+    launch_pdl(k_scan_bsums, dim3(1), dim3(1024), 0, s, ctx->bsum, nb, ctx->tot);
     LAUNCHED();
-    k_scan_apply<<<(unsigned)nb, SCAN_T, 0, s>>>(in, m, ctx->bsum, out, ctx->tot);
+    launch_pdl(k_scan_apply, dim3((unsigned)nb), dim3(SCAN_T), 0, s, in, m, (const uint32_t*)ctx->bsum, out,
+               (const uint32_t*)ctx->tot);
     LAUNCHED();
   }
   return NC_OK;
@@ -359,6 +383,7 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
   const Geom& g = ctx->g;
   int64_t C = g.ncells;
   CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
+  ctx->counts_clean = 0;  // this build leaves the histogram filled
   if (n > 0) {
     prof_begin(ctx);
     k_wrap_key<T><<<nblk(n, 256), 256, 0, s>>>(n, qin, stride, qwrap, ctx->key, ctx->slot, ctx->counts, g);
@@ -414,9 +439,9 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      k_pairs_sparse<DIGEST><<<nblocks, SP_NT, 0, s>>>(ctx->u, ctx->u32, ctx->cs, ctx->srec, (const float4*)qs,
-                                                        ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx,
-                                                        g, bpl, layer0, po);
+      launch_pdl(k_pairs_sparse<DIGEST>, dim3(nblocks), dim3(SP_NT), 0, s, (const double4*)ctx->u,
+                 (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
+                 (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
     } else if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
       const int nseg = (g.dims[0] + Gseg - 1) / Gseg;
       const int bpl_s = nseg * g.dims[1];
@@ -426,28 +451,31 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SEGMENT;
       if (ctx->seg_nw == 4)
-        k_pairs_seg<DIGEST, 4><<<nblocks, SgCfg<4>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
-                                                                   ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
-                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
+        launch_pdl(k_pairs_seg<DIGEST, 4>, dim3(nblocks), dim3(SgCfg<4>::NT), smem_s, s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const float4*)qs, (const uint32_t*)ctx->nh, gid,
+                   (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
       else
-        k_pairs_seg<DIGEST, 2><<<nblocks, SgCfg<2>::NT, smem_s, s>>>(ctx->u, ctx->u32, ctx->cs, (const float4*)qs,
-                                                                   ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs,
-                                                                   ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
+        launch_pdl(k_pairs_seg<DIGEST, 2>, dim3(nblocks), dim3(SgCfg<2>::NT), smem_s, s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const float4*)qs, (const uint32_t*)ctx->nh, gid,
+                   (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, Gseg, nseg, bpl, layer0, po);
     } else {
       ctx->pair_kernel_used = NC_PK_CELL;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       if (!DIGEST && ctx->count_tiers)
-        k_pairs<T, DIGEST, true><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
-                                                           ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
+        launch_pdl(k_pairs<T, DIGEST, true>, dim3(nblocks), dim3(32), smem, s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, qs, (const uint32_t*)ctx->nh, gid, F, bp,
+                   ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
       else
-        k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp,
-                                                     ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
+        launch_pdl(k_pairs<T, DIGEST, false>, dim3(nblocks), dim3(32), smem, s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, qs, (const uint32_t*)ctx->nh, gid, F, bp,
+                   ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
     }
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
     bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
-    k_pairs<T, DIGEST><<<nblocks, 32, smem, s>>>(ctx->u, ctx->u32, ctx->cs, qs, ctx->nh, gid, F, bp, ctx->dcnt,
-                                                 ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
+    launch_pdl(k_pairs<T, DIGEST, false>, dim3(nblocks), dim3(32), smem, s, (const double4*)ctx->u,
+               (const float4*)ctx->u32, (const uint32_t*)ctx->cs, qs, (const uint32_t*)ctx->nh, gid, F, bp, ctx->dcnt,
+               ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
   }
   LAUNCHED();
   prof_end(ctx, NC_K_PAIRS);
@@ -456,7 +484,8 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   if (reduce) {
     const int nl = layer0 + nlay - part_layer0;  // every layer whose partials start at bpart
     prof_begin(ctx);
-    k_reduce<<<nl, K3R_T, 0, s>>>(ctx->bpart, bpl, nl, ctx->lpart, ctx->part_tot, ctx->part_acc, ctx->rcount);
+    launch_pdl(k_reduce, dim3(nl), dim3(K3R_T), 0, s, (const double*)ctx->bpart, bpl, nl, ctx->lpart, ctx->part_tot,
+               ctx->part_acc, ctx->rcount);
     LAUNCHED();
     prof_end(ctx, NC_K_REDUCE);
   }
@@ -695,13 +724,16 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
     ctx->t += dt;
     int c = ctx->cur, o = 1 - c;
     const Geom& g = ctx->g;
-    CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (g.ncells + 1), s));
+    // the counts are zeroed by the previous step's scatter (below, up to its grid's C + 1); the first step
+    // of a call, and a step whose grid grew, clear them here
+    if (g.ncells + 1 > ctx->counts_clean)
+      CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (g.ncells + 1), s));
+    ctx->counts_clean = 0;  // (kick-drift-key fills it; the scatter below clears it again)
     if (n > 0) {
       prof_begin(ctx);
-      k_kick_drift_key<T><<<nblk(n, 256), 256, 0, s>>>(n, (typename V4<T>::t*)ctx->st_q[c],
-                                                      (typename V4<T>::t*)ctx->st_p[c],
-                                                      (const typename V4<T>::t*)ctx->st_F, sp, g, ctx->key,
-                                                      ctx->slot, ctx->counts, ctx->kick_pending ? 1 : 0, ctx->pend);
+      launch_pdl(k_kick_drift_key<T>, dim3(nblk(n, 256)), dim3(256), 0, s, n, (typename V4<T>::t*)ctx->st_q[c],
+                 (typename V4<T>::t*)ctx->st_p[c], (const typename V4<T>::t*)ctx->st_F, sp, g, ctx->key, ctx->slot,
+                 ctx->counts, ctx->kick_pending ? 1 : 0, ctx->pend);
       LAUNCHED();
       ctx->kick_pending = false;
       prof_end(ctx, NC_K_WRAPKEY);
@@ -713,15 +745,18 @@ nc_status step_t(nc_ctx* ctx, double dt, int nsteps, double* U, double* W) {
     }
     if (n > 0) {
       prof_begin(ctx);
-      k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, ctx->st_gid[c], ctx->srec);
+      launch_pdl(k_scatter, dim3(nblk(n, 256)), dim3(256), 0, s, n, (const uint32_t*)ctx->key,
+                 (const uint32_t*)ctx->slot, (const uint32_t*)ctx->cs, (const uint32_t*)ctx->st_gid[c], ctx->srec,
+                 (int64_t)0, (const uint32_t*)nullptr, ctx->counts, C + 1);
+      ctx->counts_clean = C + 1;
       LAUNCHED();
       prof_end(ctx, NC_K_SCATTER);
       prof_begin(ctx);
-      k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->srec, ctx->cs,
-                                                    (const typename V4<T>::t*)ctx->st_q[c],
-                                                    (const typename V4<T>::t*)ctx->st_p[c],
-                                                    (typename V4<T>::t*)ctx->st_q[o], (typename V4<T>::t*)ctx->st_p[o],
-                                                    ctx->st_gid[o], ctx->u, ctx->u32, ctx->nh, g);
+      launch_pdl(k_rank_gather<T>, dim3(nblk(n, 256)), dim3(256), 0, s, n, (const uint4*)ctx->srec,
+                 (const uint32_t*)ctx->cs, (const typename V4<T>::t*)ctx->st_q[c],
+                 (const typename V4<T>::t*)ctx->st_p[c], (typename V4<T>::t*)ctx->st_q[o],
+                 (typename V4<T>::t*)ctx->st_p[o], ctx->st_gid[o], ctx->u, ctx->u32, ctx->nh, g, (uint32_t*)nullptr,
+                 (int64_t)0, (const uint32_t*)nullptr);
       LAUNCHED();
       prof_end(ctx, NC_K_RANKGATHER);
     }
@@ -891,6 +926,7 @@ nc_status slab_begin_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_t n_o
   const int64_t C = g.ncells, per_layer = (int64_t)g.dims[0] * g.dims[1];
   const int l3 = g.dims[2];
   CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
+  ctx->counts_clean = 0;  // this build leaves the histogram filled
   typename V4<T>::t* wq = (typename V4<T>::t*)ctx->wq;
   prof_begin(ctx);
   if (n_own > 0)

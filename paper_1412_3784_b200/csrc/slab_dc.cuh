@@ -155,6 +155,7 @@ nc_status sd_forces_begin_t(nc_ctx* ctx, const T* q, const uint32_t* gid, int64_
   const int l3 = g.dims[2];
   const uint32_t* dn = ctx->sd + SD_N;
   CK(cudaMemsetAsync(ctx->counts, 0, sizeof(uint32_t) * (C + 1), s));
+  ctx->counts_clean = 0;
   typename V4<T>::t* wq = (typename V4<T>::t*)ctx->wq;
   prof_begin(ctx);
   k_wrap_key_src<T><<<nblk(ncap, 256), 256, 0, s>>>(ncap, q, 3, gid, 0, wq, ctx->gin, ctx->key, ctx->slot, ctx->counts,
