@@ -386,7 +386,8 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
   ctx->counts_clean = 0;  // this build leaves the histogram filled
   if (n > 0) {
     prof_begin(ctx);
-    k_wrap_key<T><<<nblk(n, 256), 256, 0, s>>>(n, qin, stride, qwrap, ctx->key, ctx->slot, ctx->counts, g);
+    launch_pdl(k_wrap_key<T>, dim3(nblk(n, 256)), dim3(256), 0, s, n, qin, stride, qwrap, ctx->key, ctx->slot,
+               ctx->counts, g);
     LAUNCHED();
     prof_end(ctx, NC_K_WRAPKEY);
   }
@@ -396,12 +397,15 @@ nc_status launch_build(nc_ctx* ctx, const T* qin, int stride, typename V4<T>::t*
   }
   if (n > 0) {
     prof_begin(ctx);
-    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->key, ctx->slot, ctx->cs, gid_in, ctx->srec);
+    launch_pdl(k_scatter, dim3(nblk(n, 256)), dim3(256), 0, s, n, (const uint32_t*)ctx->key,
+               (const uint32_t*)ctx->slot, (const uint32_t*)ctx->cs, gid_in, ctx->srec, (int64_t)0,
+               (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)0);
     LAUNCHED();
     prof_end(ctx, NC_K_SCATTER);
     prof_begin(ctx);
-    k_rank_gather<T><<<nblk(n, 256), 256, 0, s>>>(n, ctx->srec, ctx->cs, qwrap, p_in, q_out,
-                                                  p_out, gid_out, ctx->u, ctx->u32, ctx->nh, g);
+    launch_pdl(k_rank_gather<T>, dim3(nblk(n, 256)), dim3(256), 0, s, n, (const uint4*)ctx->srec,
+               (const uint32_t*)ctx->cs, (const typename V4<T>::t*)qwrap, p_in, q_out, p_out, gid_out, ctx->u, ctx->u32,
+               ctx->nh, g, (uint32_t*)nullptr, (int64_t)0, (const uint32_t*)nullptr);
     LAUNCHED();
     prof_end(ctx, NC_K_RANKGATHER);
   }
