@@ -266,7 +266,10 @@ def run_slab(args):
     if w.policy == "gkr":
         kw.update(om1=w.extra["om1"], om2=w.extra["om2"], beta=w.extra["beta"], eps=w.extra["eps"])
     maxc = 0
-    full = CellList(args.variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=maxc, device=lrank)
+    # a small context with the full box splits the particles by layer (chunks of 2^20): no full-size
+    # context per rank
+    full = CellList(args.variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=1 << 20, max_cells=2 * w.n + 4096,
+                    device=lrank)
     full.set_flow(w.A, w.policy, w.t0, **kw)
     idx = own_particles(full, torch.from_numpy(q).to(f"cuda:{lrank}"), rank, ws)
     from paper_1412_3784_b200 import nemdcell as ncm

@@ -531,16 +531,23 @@ class NcclTransport:
 
 # -------------------------------------------------------------------- driver
 
-def own_particles(cl_full, q_all, rank, nranks):
-    """Initial split (not on the timed path): the layer of every particle from
-    the library's own cell keys of the full system; returns the own indices."""
+def own_particles(cl, q_all, rank, nranks):
+    """Initial split (not on the timed path): the cell layer of every particle from the library
+    (nc_slab_layer_of, the same canonical wrap and layer as its cell keys), in chunks that fit the
+    context's capacity -- a small context with the full box suffices; returns the own indices."""
+    import torch
+
     n = len(q_all)
-    nc.nc_build_cells(cl_full.ctx, q_all, n)
-    cell = np.zeros(n, dtype=np.int64)
-    dims = np.zeros(3, dtype=np.int32)
-    nc._check(cl_full.ctx, nc.load().nc_get_cells(cl_full.ctx, nc._ptr(cell), None, nc._ptr(dims), None))
-    layer = cell // (int(dims[0]) * int(dims[1]))
-    l3 = int(dims[2])
+    chunk = max(1, min(int(cl.cfg.capacity), n))
+    dev = f"cuda:{cl.device}"
+    layer = np.empty(n, dtype=np.int64)
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        qc = torch.as_tensor(q_all[lo:hi]).to(dev, dtype=cl.dtype).contiguous().clone()  # wrapped in place
+        lc = torch.empty(hi - lo, dtype=torch.int32, device=dev)
+        nc.nc_slab_layer_of(cl.ctx, qc, hi - lo, lc)
+        layer[lo:hi] = lc.cpu().numpy()
+    _, _, l3 = nc.nc_slab_layers(cl.ctx, 0, 1)
     klo, khi = rank * l3 // nranks, (rank + 1) * l3 // nranks
     return np.nonzero((layer >= klo) & (layer < khi))[0]
 
