@@ -331,7 +331,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
             float4* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
             uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int G, int nseg,
             int bpl, int layer0, const PairOut po) {
-  PDL_ENTRY();
+  PDL_WAIT();  // (the successor is released at the end)
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int SG_NT = SgCfg<NW>::NT, SG_CAP = SgCfg<NW>::CAP, SG_NW = NW;
   (void)SG_NT;
@@ -475,6 +475,7 @@ k_pairs_seg(const double4* __restrict__ u, const float4* __restrict__ u32, const
     for (int w = 0; w < SG_NW; ++w) v += sm.part[w][tid];
     bpart[(int64_t)blockIdx.x * NPART + tid] = v;
   }
+  PDL_LAUNCH();
 }
 
 }  // namespace nc

@@ -19,7 +19,10 @@
 
 namespace nc {
 
-constexpr int SP_NT = 128;    // threads per block (one particle each per chunk)
+#ifndef NC_SP_NT
+#define NC_SP_NT 128
+#endif
+constexpr int SP_NT = NC_SP_NT;  // threads per block (one particle each per chunk)
 constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane could overflow)
 #ifndef NC_SP_UNR
 #define NC_SP_UNR 4
@@ -29,7 +32,7 @@ constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane co
 #endif
 constexpr int SP_UNR = NC_SP_UNR;
 constexpr int SP_QD = SP_QCAP * SP_NT * 4;  // byte offset of qd from qj
-constexpr int SP_CPB = 96;    // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
+constexpr int SP_CPB = 96 * SP_NT / 128;  // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
 
 struct SpSmem {
   uint32_t qj[SP_QCAP][SP_NT];  // sorted index of a queued j
@@ -257,8 +260,9 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
                const uint32_t* __restrict__ gid, float4* __restrict__ Fout, double* __restrict__ bpart,
                uint32_t* __restrict__ dcnt, uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx,
                const __grid_constant__ Geom g, int bpl, int layer0, const PairOut po) {
-  PDL_ENTRY();
-  __shared__ SpSmem sm;
+  PDL_WAIT();  // (the successor is released at the end)
+  extern __shared__ __align__(16) unsigned char sp_raw[];
+  SpSmem& sm = *reinterpret_cast<SpSmem*>(sp_raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int l1 = g.dims[0], l2 = g.dims[1];
   const int layer = layer0 + (int)(blockIdx.x / bpl);
@@ -329,7 +333,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
     __syncwarp();
     const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
-    // queue slot addresses of this thread: qj[k][tid] at qa0 + 512 k, qd[k][tid] SP_QD bytes further
+    // queue slot addresses of this thread: qj[k][tid] at qa0 + 4 SP_NT k, qd[k][tid] SP_QD bytes further
     const uint32_t qa0 = smem_u32(&sm.qj[0][tid]);
     uint32_t qa = qa0;
     for (int ri = 0; ri < 12; ++ri) {
@@ -403,7 +407,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
             stsu(qa, jv[h]);
             stsu(qa + SP_QD, (uint32_t)((int)v[h].w + (inb ? kb : ka)));
           }
-          qa += hit ? 512u : 0u;
+          qa += hit ? 4u * SP_NT : 0u;
           nq += hit ? 1 : 0;
         }
       }
@@ -456,6 +460,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     for (int w = 0; w < SP_NT / 32; ++w) sum += sm.part[w][tid];
     bpart[(int64_t)blockIdx.x * NPART + tid] = sum;
   }
+  PDL_LAUNCH();
 }
 
 }  // namespace nc

@@ -1248,7 +1248,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
         typename V4<T>::t* __restrict__ Fout, double* __restrict__ bpart, uint32_t* __restrict__ dcnt,
         uint64_t* __restrict__ dhs, uint64_t* __restrict__ dhx, const __grid_constant__ Geom g, int cpb, int bpl,
         int layer0, const PairOut po) {
-  PDL_ENTRY();
+  PDL_WAIT();  // (the successor is released at the end: PDL_LAUNCH below)
   extern __shared__ __align__(16) unsigned char smraw[];
   const int lane = threadIdx.x & 31;
   K3Smem<T>& sm = *reinterpret_cast<K3Smem<T>*>(smraw);
@@ -1587,6 +1587,7 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
     else v = tNF;
     bpart[(int64_t)blockIdx.x * NPART + lane] = v;
   }
+  PDL_LAUNCH();
 }
 
 // K3r: per-layer partials (one block per layer: each thread sums a fixed

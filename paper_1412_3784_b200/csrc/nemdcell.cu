@@ -443,7 +443,7 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      launch_pdl(k_pairs_sparse<DIGEST>, dim3(nblocks), dim3(SP_NT), 0, s, (const double4*)ctx->u,
+      launch_pdl(k_pairs_sparse<DIGEST>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
                  (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
                  (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
     } else if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
@@ -1184,7 +1184,9 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_seg<true, 2>, sizeof(SgSmem<2>)},
         {(const void*)k_pairs_seg<false, 4>, sizeof(SgSmem<4>)},
         {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)},
-        {(const void*)k_scan_small, sizeof(uint32_t) * (size_t)scan_pad(SCAN_SMALL + 32)}};
+        {(const void*)k_scan_small, sizeof(uint32_t) * (size_t)scan_pad(SCAN_SMALL + 32)},
+        {(const void*)k_pairs_sparse<false>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)}};
     for (const KA& a : ka) {
       cudaError_t e = cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
       if (e != cudaSuccess) {
