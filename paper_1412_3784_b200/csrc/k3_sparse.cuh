@@ -292,13 +292,31 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if ((lane & 15) < 12) sp_row_inv(g, lane & 15, lane < 16 ? a1A : a1B, layer, sm.rw[wid][lane >> 4][lane & 15]);
     __syncwarp();
     const int grp = a1 == a1A ? 0 : (a1 == a1B ? 1 : -1);
-    int ns = 0;
-    for (int ri = 0; ri < 12; ++ri) {
-      SpSmem::RowW w;
-      if (grp >= 0) w = sm.rw[wid][grp][ri];
-      else sp_row_inv(g, ri, a1, layer, w);
-      if (w.meta & 1u)
-        ns += (int)ceil(__dsub_rn((double)(a0 + 2), w.ox)) - (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
+    // a row's width c1 - c0 does not depend on a0 unless ox lies within 2^-30 of an integer without being
+    // one (then fl(a0 - 1 - ox) could round across it): 3 for an integral ox (DS: ox = 0), else 4; the
+    // building lanes sum their group's widths (64 flags a row that needs the per-cell expressions)
+    int wcode = 0;
+    if ((lane & 15) < 12) {
+      const SpSmem::RowW& wr = sm.rw[wid][lane >> 4][lane & 15];  // written by this lane above
+      if (wr.meta & 1u) {
+        const double f = wr.ox - floor(wr.ox);
+        wcode = f == 0.0 ? 3 : (fmin(f, 1.0 - f) > 0x1p-30 ? 4 : 64);
+      }
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) wcode += __shfl_xor_sync(0xffffffffu, wcode, o);
+    const int totA = __shfl_sync(0xffffffffu, wcode, 0), totB = __shfl_sync(0xffffffffu, wcode, 16);
+    const int tot = grp == 0 ? totA : (grp == 1 ? totB : 64);
+    int ns = tot;
+    if (tot >= 64) {  // the per-cell expressions (sp_row's)
+      ns = 0;
+      for (int ri = 0; ri < 12; ++ri) {
+        SpSmem::RowW w;
+        if (grp >= 0) w = sm.rw[wid][grp][ri];
+        else sp_row_inv(g, ri, a1, layer, w);
+        if (w.meta & 1u)
+          ns += (int)ceil(__dsub_rn((double)(a0 + 2), w.ox)) - (int)floor(__dsub_rn((double)(a0 - 1), w.ox));
+      }
     }
     if (cv) tS += (uint32_t)(ns - g.dbg_drop);
   }
