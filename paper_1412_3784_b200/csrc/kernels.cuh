@@ -436,7 +436,10 @@ k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restri
 #ifndef K3_PF_L2
 #define K3_PF_L2 1  // L2 prefetch of the staged particles' fp64 coordinates (close tier): fluid -0.5%, lattice +0.4%
 #endif
-constexpr int K3_F64_SPLIT_B = 8;  // NC_F64 small grids: particles per i-batch when blocks share a cell
+#ifndef NC_F64_SPLIT_B
+#define NC_F64_SPLIT_B 8
+#endif
+constexpr int K3_F64_SPLIT_B = NC_F64_SPLIT_B;  // NC_F64 small grids: particles per i-batch when blocks share a cell
 constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 64;  // permanent far element (padding slot of the evaluation)
 constexpr int K3_STAGE = K3_CAP + 66;  // fp64 mode: + up to S far sentinels so the filter needs no bounds checks

@@ -229,7 +229,10 @@ constexpr int64_t K3_MIN_BLOCKS = 75776;
 // NC_F64 on grids below K3_F64_SPLIT_CELLS cells (fewer than ~4 waves of one-warp blocks): each cell's
 // i-batches of 8 are spread over K3_F64_SPLIT blocks (a function of the global grid only: P-invariant)
 constexpr int64_t K3_F64_SPLIT_CELLS = 8192;
-constexpr int K3_F64_SPLIT = 4;
+#ifndef NC_F64_SPLIT
+#define NC_F64_SPLIT 4
+#endif
+constexpr int K3_F64_SPLIT = NC_F64_SPLIT;
 int cells_per_block(const Geom& g) {
   int cpb = K3_CELLS;
   while (cpb * 2 <= K3_CELLS_MAX && g.ncells / (cpb * 2) >= K3_MIN_BLOCKS) cpb *= 2;
