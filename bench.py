@@ -479,6 +479,8 @@ def run_ours(args):
     stream = torch.cuda.Stream(lrank)
     cl = CellList(args.variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
                   capacity=w.n, max_cells=0, device=lrank, stream=stream.cuda_stream)
+    if args.pair_kernel != "auto":
+        cl.pair_kernel(args.pair_kernel)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
@@ -703,6 +705,8 @@ def main():
     ap.add_argument("--input", default="fluid", choices=["fluid", "lattice"],
                     help="fluid: BASELINE's relaxed uniform positions (default); lattice: the jittered crystal")
     ap.add_argument("--t0", type=float, default=None, help="KR configs: start at t0 = this fraction of t*")
+    ap.add_argument("--pair-kernel", default="auto", choices=["auto", "cell", "segment", "sparse", "rows"],
+                    help="force one K3 pair kernel (A/B runs; default: the library's choice)")
     ap.add_argument("--weak", action="store_true",
                     help="slab path, weak scaling: 8,388,608 particles per GPU (box elongated along v3)")
     args = ap.parse_args()

@@ -425,10 +425,13 @@ nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *m
  *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
  *                union of their neighborhoods (k_pairs_seg, round 1), fp64 pair forces;
  *  NC_PK_SPARSE  one thread per particle, 32 consecutive particles of a cell row per warp walking
- *                their exact stencils in lockstep through L1 (k_pairs_sparse), fp64 pair forces.
- * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT on an NC_F64 context).
- * nc_pair_kernel_used returns the kernel of the last evaluation (1, 2 or 3, 0 = none). */
-typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2, NC_PK_SPARSE = 3 } nc_pair_kernel;
+ *                their exact stencils in lockstep through L1 (k_pairs_sparse), fp64 pair forces;
+ *  NC_PK_ROWS    one warp per cell row, batches of 32 consecutive particles whose neighbour rows
+ *                are staged once in shared memory (k_pairs_rows, round 2), fp64 pair forces
+ *                bitwise those of NC_PK_SPARSE.
+ * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT / NC_PK_SPARSE / NC_PK_ROWS on an NC_F64 context).
+ * nc_pair_kernel_used returns the kernel of the last evaluation (1, 2, 3 or 4, 0 = none). */
+typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2, NC_PK_SPARSE = 3, NC_PK_ROWS = 4 } nc_pair_kernel;
 nc_status nc_set_pair_kernel(nc_ctx *ctx, int which);
 int nc_pair_kernel_used(const nc_ctx *ctx);
 

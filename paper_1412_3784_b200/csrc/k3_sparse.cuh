@@ -212,7 +212,8 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
       const double r2 = dx * dx + dy * dy + dz * dz;
       bool ok = ok0[h] && (jj[h] != me) && (r2 < hi64);
       int n0 = 0, n1 = 0, n2 = 0;
-      if (ok && (DIGEST || r2 >= lo64)) {
+      // (a real branch: pairs inside the 1e-12 band are rare, the vote keeps the canonical test out of line)
+      if ((DIGEST || __any_sync(0xffffffffu, ok && r2 >= lo64)) && ok && (DIGEST || r2 >= lo64)) {
         n0 = cc[h].n1;
         n1 = cc[h].n2;
         n2 = cc[h].n3;

@@ -273,6 +273,7 @@ int sparse_kind(nc_ctx* ctx, const Geom& g) {
   if (ctx->cfg.prec != NC_F32 || ctx->pair_kernel == NC_PK_CELL) return 0;
   if (ctx->pair_kernel == NC_PK_SEGMENT) return 1;
   if (ctx->pair_kernel == NC_PK_SPARSE) return 2;
+  if (ctx->pair_kernel == NC_PK_ROWS) return 3;
   static int env_mode = [] {
     const char* e = getenv("NC_SEG");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
@@ -441,7 +442,15 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
   double* bp = nullptr;  // set once bpl is final (below)
   if constexpr (sizeof(T) == 4) {
     const int Gseg = sparse_kind(ctx, g) == 1 ? seg_cells(ctx, g) : 0;
-    if (sparse_kind(ctx, g) == 2) {  // sparse cells: one thread per particle (k3_sparse.cuh)
+    if (sparse_kind(ctx, g) == 3) {  // sparse cells: one warp per cell row, staged neighbour rows (k3_rows.cuh)
+      bpl = (g.dims[1] + RW_NW - 1) / RW_NW;  // a function of the grid only (P-invariant)
+      nblocks = bpl * nlay;
+      bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
+      ctx->pair_kernel_used = NC_PK_ROWS;
+      launch_pdl(k_pairs_rows<DIGEST>, dim3(nblocks), dim3(32 * RW_NW), sizeof(RwSmem), s, (const double4*)ctx->u,
+                 (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const float4*)qs, (const uint32_t*)ctx->nh, gid,
+                 (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+    } else if (sparse_kind(ctx, g) == 2) {  // sparse cells: one thread per particle (k3_sparse.cuh)
       bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + SP_CPB - 1) / SP_CPB);  // a function of the grid only (P-invariant)
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
@@ -1070,9 +1079,10 @@ int64_t nc_launch_count(const nc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 nc_status nc_set_pair_kernel(nc_ctx* ctx, int which) {
   if (!ctx) return fail(ctx, NC_E_ARG, "null ctx");
-  if (which != NC_PK_AUTO && which != NC_PK_CELL && which != NC_PK_SEGMENT && which != NC_PK_SPARSE)
-    return fail(ctx, NC_E_ARG, "pair kernel must be NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT or NC_PK_SPARSE");
-  if ((which == NC_PK_SEGMENT || which == NC_PK_SPARSE) && ctx->cfg.prec != NC_F32)
+  if (which != NC_PK_AUTO && which != NC_PK_CELL && which != NC_PK_SEGMENT && which != NC_PK_SPARSE &&
+      which != NC_PK_ROWS)
+    return fail(ctx, NC_E_ARG, "pair kernel must be NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE or NC_PK_ROWS");
+  if ((which == NC_PK_SEGMENT || which == NC_PK_SPARSE || which == NC_PK_ROWS) && ctx->cfg.prec != NC_F32)
     return fail(ctx, NC_E_ARG, "the segment pair kernel is NC_F32 only");
   ctx->pair_kernel = which;
   return NC_OK;
@@ -1189,7 +1199,9 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)},
         {(const void*)k_scan_small, sizeof(uint32_t) * (size_t)scan_pad(SCAN_SMALL + 32)},
         {(const void*)k_pairs_sparse<false>, sizeof(SpSmem)},
-        {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)}};
+        {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)},
+        {(const void*)k_pairs_rows<false>, sizeof(RwSmem)},
+        {(const void*)k_pairs_rows<true>, sizeof(RwSmem)}};
     for (const KA& a : ka) {
       cudaError_t e = cudaFuncSetAttribute(a.f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)a.smem);
       if (e != cudaSuccess) {

@@ -38,8 +38,8 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            "nc_sd_halo", "nc_sd_exchange_start", "nc_sd_forces_begin", "nc_sd_forces_end",
            "nc_sd_forces_end_sorted"]
 NC_DBG_DROP_ENTRIES = 1
-NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE = 0, 1, 2, 3
-PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT, "sparse": NC_PK_SPARSE}
+NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE, NC_PK_ROWS = 0, 1, 2, 3, 4
+PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT, "sparse": NC_PK_SPARSE, "rows": NC_PK_ROWS}
 KERNEL_IDS = ["wrap_key", "scan", "scatter", "rank_gather", "pairs", "reduce", "kick", "other"]
 
 
@@ -311,12 +311,12 @@ def nc_get_stencil_histogram(ctx) -> np.ndarray:
 
 
 def nc_set_pair_kernel(ctx, which) -> None:
-    """Pair kernel of the context: "auto" | "cell" | "segment" (or NC_PK_*)."""
+    """Pair kernel of the context: "auto" | "cell" | "segment" | "sparse" | "rows" (or NC_PK_*)."""
     _check(ctx, load().nc_set_pair_kernel(ctx, PAIR_KERNELS.get(which, which) if isinstance(which, str) else int(which)))
 
 
 def nc_pair_kernel_used(ctx) -> str:
-    return {0: "none", 1: "cell", 2: "segment", 3: "sparse"}[load().nc_pair_kernel_used(ctx)]
+    return {0: "none", 1: "cell", 2: "segment", 3: "sparse", 4: "rows"}[load().nc_pair_kernel_used(ctx)]
 
 
 def nc_profile(ctx, enable) -> None:

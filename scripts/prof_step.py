@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--scale", type=int, default=1)
     ap.add_argument("--input", default="lattice", choices=["lattice", "fluid"])
+    ap.add_argument("--pair-kernel", default="auto")
     ap.add_argument("--cache", default="gpurun_out/fluid_cache.npy",
                     help="fluid positions are computed once (run without ncu first) and loaded from here")
     a = ap.parse_args()
@@ -40,6 +41,8 @@ def main():
         q = W.positions(w, dtype=dt, k=a.config)
     p = W.momenta(w, dtype=dt, k=a.config)
     cl = CellList(a.variant, a.prec, rc=w.rc, u_shift=w.ushift, capacity=w.n, max_cells=0)
+    if a.pair_kernel != "auto":
+        cl.pair_kernel(a.pair_kernel)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]

@@ -102,7 +102,7 @@ def test_pair_list_cap_reports_the_count():
 
 def _edge_case(kind, prec, variant, kernel):
     # the sparse-cell kernel gets the same pairs in a box 8x the volume (~2 particles per cell, its regime)
-    a = 20.0 if kernel in ("segment", "sparse") else 10.0
+    a = 20.0 if kernel in ("segment", "sparse", "rows") else 10.0
     L, rc, q, d0 = edges.edge_pairs(kind, npairs=6000, seed={"le": 1, "kr": 2, "gkr": 3}[kind], a=a)
     qs = q.astype(np.float32 if prec == "f32" else np.float64)
     cl = _cl(variant, prec, rc, len(qs), sigma=0.1, kernel=kernel)
@@ -120,6 +120,7 @@ def _edge_case(kind, prec, variant, kernel):
 @pytest.mark.parametrize("prec, variant, kernel", [("f32", "do", "cell"), ("f32", "ds", "cell"),
                                                    ("f32", "do", "segment"), ("f32", "ds", "segment"),
                                                    ("f32", "do", "sparse"), ("f32", "ds", "sparse"),
+                                                   ("f32", "do", "rows"), ("f32", "ds", "rows"),
                                                    ("f64", "do", "cell"), ("f64", "ds", "cell")])
 def test_pairs_on_the_cutoff(kind, prec, variant, kernel):
     r, counts, cnt, hs, hx, st, n_on, n_edge = _edge_case(kind, prec, variant, kernel)
@@ -154,7 +155,8 @@ def test_cutoff_at_the_last_bit_fp64(variant):
     assert max(seen[k] for k in ks if k <= 0) < min(seen[k] for k in ks if k > 0), seen
 
 
-@pytest.mark.parametrize("prec, kernel", [("f32", "cell"), ("f32", "segment"), ("f32", "sparse"), ("f64", "cell")])
+@pytest.mark.parametrize("prec, kernel", [("f32", "cell"), ("f32", "segment"), ("f32", "sparse"), ("f32", "rows"),
+                                          ("f64", "cell")])
 def test_truncated_stencil_is_caught(prec, kernel):
     """Negative control: with the last entry of every neighborhood dropped (nc_debug), the same
     checks must fail -- the parity tests can see a missing stencil cell."""

@@ -97,7 +97,7 @@ def test_c1_shear(variant, prec):
     check_against_oracle(w, q, variant, prec)
 
 
-@pytest.mark.parametrize("kernel", ["cell", "segment", "sparse"])
+@pytest.mark.parametrize("kernel", ["cell", "segment", "sparse", "rows"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
 def test_c1_both_pair_kernels(variant, kernel):
     """Sparse WCA cells (C1, ~1.3 per cell): the warp-per-cell, the row-segment and the
@@ -107,20 +107,21 @@ def test_c1_both_pair_kernels(variant, kernel):
     assert g["kernel"] == kernel
 
 
+@pytest.mark.parametrize("kernel", ["sparse", "rows"])
 @pytest.mark.parametrize("scale", [3, 4])
 @pytest.mark.parametrize("variant", ["ds", "do"])
-def test_sparse_kernel_tiny_grid_many_rows_per_warp(variant, scale):
+def test_sparse_kernel_tiny_grid_many_rows_per_warp(variant, scale, kernel):
     """k_pairs_sparse on a tiny WCA grid (C1 scaled to 7-10 cells a side, ~9-13 particles a cell
     row): a warp's 32 particles span 3-5 cell rows, so most lanes build their own row data instead of
     reading the warp's two shared rows -- both paths must give the oracle's pair set and forces."""
     w, q = inputs(1, "f32", scale=scale)
-    g, _ = check_against_oracle(w, q, variant, "f32", kernel="sparse")
-    assert g["kernel"] == "sparse"
+    g, _ = check_against_oracle(w, q, variant, "f32", kernel=kernel)
+    assert g["kernel"] == kernel
     dims = g["dims"]
     assert 32 > 2 * dims[0] * 1.0  # rows of < 16 cells: a warp spans >= 3 cell rows
 
 
-@pytest.mark.parametrize("kernel", ["segment", "sparse"])
+@pytest.mark.parametrize("kernel", ["segment", "sparse", "rows"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
 def test_segment_kernel_on_dense_lj_cells(variant, kernel):
     """The sparse-cell kernels forced onto dense LJ cells (~13 per cell; the segment kernel's
@@ -130,7 +131,7 @@ def test_segment_kernel_on_dense_lj_cells(variant, kernel):
     check_against_oracle(w, q, variant, "f32", kernel=kernel)
 
 
-@pytest.mark.parametrize("kernel", ["segment", "sparse"])
+@pytest.mark.parametrize("kernel", ["segment", "sparse", "rows"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
 def test_segment_kernel_deterministic_and_equal_pair_set(kernel, variant):
     w, q = inputs(3, "f32", scale=2)
@@ -153,6 +154,8 @@ def test_pair_kernel_option_errors():
         cl.pair_kernel("segment")
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel("sparse")
+    with pytest.raises(NcError, match="NC_E_ARG"):
+        cl.pair_kernel("rows")
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel(7)
     cl.close()
@@ -400,7 +403,7 @@ def test_minimal_grids(variant, prec, tilt):
     check_against_oracle(w, q, variant, prec)
 
 
-@pytest.mark.parametrize("kernel", ["cell", "segment", "sparse"])
+@pytest.mark.parametrize("kernel", ["cell", "segment", "sparse", "rows"])
 def test_user_order_force_output_host_device_async_agree(kernel):
     """The pair kernels write F straight into the caller's order (no unsort pass): device q / F, host
     q / F (staged) and the pipelined host-buffer calls give bitwise the same F, in the caller's own
@@ -430,3 +433,20 @@ def test_user_order_force_output_host_device_async_agree(kernel):
     # differ in their last bits before the fp32 rounding)
     Fo = Fo.cpu().numpy()[perm]
     assert np.abs(Fd - Fo).max() <= 1e-6 * np.sqrt(np.mean(Fo ** 2))
+
+
+@pytest.mark.parametrize("cfg, scale", [(1, 1), (3, 4), (3, 2)])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_rows_kernel_bitwise_equals_sparse_kernel(cfg, scale, variant):
+    """k_pairs_rows evaluates every lane's candidates in k_pairs_sparse's order with its fp64
+    arithmetic: per-particle forces, counts and pair digests are bitwise equal; U and W differ only
+    by the block partition of their fixed-order sums."""
+    w, q = inputs(cfg, "f32", scale=scale)
+    a = gpu_eval(w, q, variant, "f32", kernel="rows")
+    b = gpu_eval(w, q, variant, "f32", kernel="sparse")
+    assert np.array_equal(a["F"], b["F"])
+    for x, y in zip(a["dig"], b["dig"]):
+        assert np.array_equal(x, y)
+    for k in ("candidates", "interactions", "stencil_cells", "rechecks"):
+        assert a["stats"][k] == b["stats"][k], k
+    assert abs(a["U"] - b["U"]) <= 1e-12 * abs(b["U"])

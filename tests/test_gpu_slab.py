@@ -220,9 +220,10 @@ def test_slab_repartition_when_l3_changes(P, variant, dev):
         r.close()
 
 
+@pytest.mark.parametrize("kernel", ["sparse", "rows"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("dev", [False, True])
-def test_slab_forces_bitwise_particle_per_thread_kernel(P, dev):
+def test_slab_forces_bitwise_particle_per_thread_kernel(P, dev, kernel):
     """The particle-per-thread sparse kernel (NC_PK_SPARSE) on every rank and on one device: its
     block partials are fixed particle ranges of one layer, so U and W stay bitwise P-invariant."""
     import torch
@@ -232,16 +233,16 @@ def test_slab_forces_bitwise_particle_per_thread_kernel(P, dev):
     q = W.positions(w, dtype=np.float32, k=1)
     p = W.momenta(w, dtype=np.float32, k=1)
     one = CellList("do", "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
-    one.pair_kernel("sparse")
+    one.pair_kernel(kernel)
     one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
     F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
     st1 = one.stats()
     one.close()
     sysm = make_system(w, q, p, P, "do", "f32", dev=dev)
     for r in sysm.ranks:
-        r.cl.pair_kernel("sparse")
+        r.cl.pair_kernel(kernel)
     U, Wv, st = sysm.forces(True)
-    assert all(r.cl.pair_kernel_used() == "sparse" for r in sysm.ranks)
+    assert all(r.cl.pair_kernel_used() == kernel for r in sysm.ranks)
     _, _, F = gather_state(sysm, len(q), np.float32)
     assert np.array_equal(F, F1.cpu().numpy())
     assert U == U1 and np.array_equal(Wv, W1)
