@@ -208,3 +208,27 @@ def test_pair_sets_every_sllod_step(prec):
         assert np.array_equal(counts, r.cnt), step
     cl.close()
     assert np.any(np.diff(gammas) < 0)  # a Lees-Edwards reset happened inside the run
+
+
+def test_rows_kernel_overfull_neighbour_row_fails_loudly():
+    """k_pairs_rows stages a batch's neighbour rows in a fixed shared-memory buffer; a row it cannot
+    stage even for a single particle (one cell holding > 512 particles) is reported as NC_E_OOM, never
+    evaluated from a truncated buffer.  The particle-per-thread kernel streams its rows from global
+    memory and still reproduces the oracle's pair set on the same input."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import NcError
+
+    rng = np.random.default_rng([1412, 3784, 77])
+    L = np.eye(3) * 12.0
+    rc = 2.5
+    q = np.concatenate([rng.uniform(0.1, 2.9, size=(600, 3)), rng.uniform(0.0, 12.0, size=(400, 3))])
+    cl = _cl("do", "f32", rc, len(q), sigma=0.1, kernel="rows")
+    cl.set_box(L)
+    with pytest.raises(NcError, match="NC_E_OOM"):
+        cl.compute_forces(torch.from_numpy(q.astype(np.float32)).cuda())
+    cl.close()
+    cl = _cl("do", "f32", rc, len(q), sigma=0.1, kernel="sparse")
+    counts, wq, (cnt, hs, hx), st = _eval(cl, L, q.astype(np.float32), "f32")
+    cl.close()
+    r = oracle.evaluate(oracle.DO, wq, L, rc, 1.0, 0.1, 0.0)
+    assert np.array_equal(cnt, r.cnt) and np.array_equal(hs, r.hsum) and np.array_equal(counts, r.cnt)
