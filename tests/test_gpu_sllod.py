@@ -19,7 +19,7 @@ from paper_1412_3784_b200 import workloads as W
 pytestmark = pytest.mark.gpu
 
 
-def run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=None):
+def run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=None, kernel="auto"):
     """SLLOD on the GPU on a side (non-default) stream: one nc_step_sllod call of nsteps or, with
     per_call = k, nsteps / k calls."""
     import torch
@@ -29,6 +29,7 @@ def run_gpu(w, q, p, prec, variant, dt, nsteps, per_call=None):
     torch.cuda.synchronize()
     cl = CellList(variant, prec, rc=w.rc, eps=w.eps, sigma=w.sigma, u_shift=w.ushift, mass=w.mass,
                   capacity=len(q), max_cells=4 * len(q) + 4096, stream=side.cuda_stream)
+    cl.pair_kernel(kernel)
     kw = dict(L0=w.L0)
     if w.policy == "kr":
         kw["tstar"] = w.extra["tstar"]
@@ -241,3 +242,16 @@ def test_deferred_kick_dropped_by_set_state():
     cl.get_state(None, po)
     cl.close()
     assert torch.equal(po, pd)
+
+
+@pytest.mark.parametrize("k,scale,flow,variant", [(1, 1, "uniaxial", "do"), (1, 1, "uniaxial", "ds"),
+                                                  (3, 4, "uniaxial", "do"), (3, 4, "biaxial", "ds")])
+def test_rows_kernel_trajectory_bitwise_equals_sparse(k, scale, flow, variant):
+    """k_pairs_rows gives bitwise k_pairs_sparse's per-particle forces, so whole fp32 SLLOD trajectories
+    (Lees-Edwards / generalized KR resets inside the run) are bitwise the same with either kernel."""
+    w = near_reset(W.make(k, flow=flow, scale=scale), 20, W.make(k, flow=flow, scale=scale).dt)
+    q = W.positions(w, dtype=np.float32, k=k)
+    p = W.momenta(w, dtype=np.float32, k=k)
+    a = run_gpu(w, q, p, "f32", variant, w.dt, 20, kernel="rows")
+    b = run_gpu(w, q, p, "f32", variant, w.dt, 20, kernel="sparse")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
