@@ -31,6 +31,10 @@ constexpr int SP_QCAP = 16;   // per-thread hit queue (flushed when some lane co
 #define NC_SP_MINB 4
 #endif
 constexpr int SP_UNR = NC_SP_UNR;
+#ifndef NC_SP_LPP_CELLS
+#define NC_SP_LPP_CELLS 8192  // grids below this many cells use 4 threads per particle (host sparse_lpp)
+#endif
+constexpr int64_t SP_LPP_CELLS = NC_SP_LPP_CELLS;
 constexpr int SP_QD = SP_QCAP * SP_NT * 4;  // byte offset of qd from qj
 constexpr int SP_CPB = 96 * SP_NT / 128;  // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
 
@@ -254,7 +258,7 @@ __device__ __forceinline__ void sp_eval(const Geom& g, SpSmem& sm, const double4
 // grid = nlay layers x bpl blocks; block b of layer L takes the layer's particles
 // [b SP_NT, (b+1) SP_NT) + k bpl SP_NT, k = 0, 1, ... (a fixed partition of the layer).  The cells of
 // the layer are walked the same way for the stencil-size statistic (empty cells included).
-template <bool DIGEST>
+template <bool DIGEST, int LPP = 1>
 __global__ void __launch_bounds__(SP_NT, NC_SP_MINB)
 k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, const uint32_t* __restrict__ cs,
                const uint4* __restrict__ rec, const float4* __restrict__ qs, const uint32_t* __restrict__ nh,
@@ -322,8 +326,13 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     if (cv) tS += (uint32_t)(ns - g.dbg_drop);
   }
 
-  for (uint32_t base = P0 + (uint32_t)b * SP_NT; base < P1; base += (uint32_t)bpl * SP_NT) {
-    const uint32_t i = base + (uint32_t)tid;
+  // LPP > 1 (small systems: more warps, a shorter chain per warp): LPP consecutive threads share one
+  // particle, thread `sub` walking the stencil rows sub, sub + LPP, ...; their partial sums are combined
+  // in fixed order (sub 0 + 1 + ... ) by the owner (sub 0)
+  constexpr int NPB = SP_NT / LPP;  // particles per block pass
+  const int sub = LPP > 1 ? tid % LPP : 0;
+  for (uint32_t base = P0 + (uint32_t)b * NPB; base < P1; base += (uint32_t)bpl * NPB) {
+    const uint32_t i = base + (uint32_t)(LPP > 1 ? tid / LPP : tid);
     const bool act = i < P1;
     const uint32_t me = act ? i : P0;
     const uint32_t c = rec[me].z;  // the cell of sorted slot me (bucket records: same cell order)
@@ -355,7 +364,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     // queue slot addresses of this thread: qj[k][tid] at qa0 + 4 SP_NT k, qd[k][tid] SP_QD bytes further
     const uint32_t qa0 = smem_u32(&sm.qj[0][tid]);
     uint32_t qa = qa0;
-    for (int ri = 0; ri < 12; ++ri) {
+    for (int ri = sub; ri < 12; ri += LPP) {  // (the same trip count for every lane of the warp)
       SpSmem::RowW w;
       if (grp >= 0) w = sm.rw[wid][grp][ri];
       else sp_row_inv(g, ri, a1, layer, w);
@@ -438,7 +447,22 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     acc.w3 = sm.acc[7][tid]; acc.w4 = sm.acc[8][tid]; acc.w5 = sm.acc[9][tid];
     acc.cnt = sm.cnt[tid]; acc.nrc = sm.nrc[tid];
     if (DIGEST) { acc.hs = sm.hs[tid]; acc.hx = sm.hx[tid]; }
-    if (act) {
+    if (LPP > 1) {  // the owner adds its siblings' partial sums in fixed order (sp_eval ended in __syncwarp)
+      if (act && sub == 0) {
+#pragma unroll
+        for (int k = 1; k < LPP; ++k) {
+          const int o = tid + k;
+          acc.fx += sm.acc[0][o]; acc.fy += sm.acc[1][o]; acc.fz += sm.acc[2][o]; acc.u += sm.acc[3][o];
+          acc.w0 += sm.acc[4][o]; acc.w1 += sm.acc[5][o]; acc.w2 += sm.acc[6][o];
+          acc.w3 += sm.acc[7][o]; acc.w4 += sm.acc[8][o]; acc.w5 += sm.acc[9][o];
+          acc.cnt += sm.cnt[o]; acc.nrc += sm.nrc[o];
+          if (DIGEST) { acc.hs += sm.hs[o]; acc.hx ^= sm.hx[o]; }
+        }
+      }
+      if (act) tC += ncand;  // every thread its own rows' candidates (the self pair subtracted below)
+      __syncwarp();  // the siblings' sums are read before the next batch clears them
+    }
+    if (act && sub == 0) {
       const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
       const float4 fv = make_float4((float)(g.Q[0] * acc.fx + g.Q[1] * acc.fy + g.Q[2] * acc.fz),
                                     (float)(g.Q[3] * acc.fx + g.Q[4] * acc.fy + g.Q[5] * acc.fz),
@@ -452,7 +476,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
       sm.tuw[4][tid] += 0.5 * acc.w3; sm.tuw[5][tid] += 0.5 * acc.w4; sm.tuw[6][tid] += 0.5 * acc.w5;
       tI += acc.cnt;
       tR += acc.nrc;
-      tC += ncand - 1u;
+      tC += (LPP > 1 ? 0u : ncand) - 1u;
       tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0u : 1u;
     }
   }

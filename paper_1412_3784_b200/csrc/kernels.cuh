@@ -298,26 +298,43 @@ __global__ void k_scan_apply(const uint32_t* __restrict__ in, int64_t m, const u
 }
 
 // Small inputs (m <= SCAN_SMALL): the whole exclusive scan in one block, one launch instead of
-// three (C1's 24k cells, slab migration blocks, ...): rows of 1024 coalesced elements, each a
-// block scan, with a running carry.  out[m] = total.
+// three (C1's 24k cells, C2's 20k, slab migration blocks, ...).  One SM does all of it, so it is bound by
+// that SM's instruction issue: each thread scans its own run of R consecutive counts (R a multiple of 4,
+// loaded / stored as 16-byte vectors, kept in registers), then one warp scan of the run totals and one of
+// the warp totals.  out[m] = total.  (A shared-memory copy with strided runs was bound by bank conflicts,
+// and a 32-wide shuffle scan per step by issue: ~10 us for C1's 24k cells either way.)
 constexpr int SCAN_SMALL_T = 1024, SCAN_SMALL_R = 32, SCAN_SMALL = SCAN_SMALL_R * SCAN_SMALL_T;
-// m <= SCAN_SMALL in one block with three barriers: coalesced loads into shared memory (padded one word
-// per 32), each thread scans its own contiguous run of R = ceil(m / T) entries, one block scan of the
-// T run totals, each thread writes its run's exclusive prefixes back, coalesced stores.
-__host__ __device__ constexpr int scan_pad(int i) { return i + (i >> 5); }
 __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __restrict__ in, int64_t m,
                                                              uint32_t* __restrict__ out) {
   PDL_ENTRY();
-  extern __shared__ uint32_t sbuf[];  // scan_pad(SCAN_SMALL) words
   __shared__ uint32_t wsum[SCAN_SMALL_T / 32];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int mm = (int)m;
-  for (int i = tid; i < mm; i += SCAN_SMALL_T) sbuf[scan_pad(i)] = in[i];
-  __syncthreads();
-  const int R = (mm + SCAN_SMALL_T - 1) / SCAN_SMALL_T;
-  const int b = tid * R, e = min(b + R, mm);
+  const int R = ((mm + SCAN_SMALL_T - 1) / SCAN_SMALL_T + 3) & ~3;  // run length, a multiple of 4
+  const int b0 = tid * R;
+  uint32_t v[SCAN_SMALL_R];
+#pragma unroll
+  for (int q = 0; q < SCAN_SMALL_R / 4; ++q) {
+    const int i = b0 + 4 * q;
+    uint4 x = make_uint4(0u, 0u, 0u, 0u);
+    if (4 * q < R) {
+      if (i + 4 <= mm) {
+        x = *reinterpret_cast<const uint4*>(in + i);
+      } else {
+        if (i < mm) x.x = in[i];
+        if (i + 1 < mm) x.y = in[i + 1];
+        if (i + 2 < mm) x.z = in[i + 2];
+      }
+    }
+    v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+  }
   uint32_t run = 0;
-  for (int i = b; i < e; ++i) run += sbuf[scan_pad(i)];
+#pragma unroll
+  for (int k = 0; k < SCAN_SMALL_R; ++k) {  // exclusive prefixes inside the run (zeros past R / m)
+    const uint32_t c = v[k];
+    v[k] = run;
+    run += c;
+  }
   uint32_t x = run;  // inclusive scan of the run totals: warp, then warp sums
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -336,14 +353,21 @@ __global__ void __launch_bounds__(SCAN_SMALL_T) k_scan_small(const uint32_t* __r
     wsum[lane] = w;  // inclusive over warps
   }
   __syncthreads();
-  uint32_t pre = (wid > 0 ? wsum[wid - 1] : 0u) + x - run;  // exclusive prefix of this run
-  for (int i = b; i < e; ++i) {
-    const uint32_t v = sbuf[scan_pad(i)];
-    sbuf[scan_pad(i)] = pre;
-    pre += v;
+  const uint32_t pre = (wid > 0 ? wsum[wid - 1] : 0u) + x - run;  // exclusive prefix of this run
+#pragma unroll
+  for (int q = 0; q < SCAN_SMALL_R / 4; ++q) {
+    const int i = b0 + 4 * q;
+    if (4 * q < R) {
+      const uint4 y = make_uint4(pre + v[4 * q], pre + v[4 * q + 1], pre + v[4 * q + 2], pre + v[4 * q + 3]);
+      if (i + 4 <= mm) {
+        *reinterpret_cast<uint4*>(out + i) = y;
+      } else {
+        if (i < mm) out[i] = y.x;
+        if (i + 1 < mm) out[i + 1] = y.y;
+        if (i + 2 < mm) out[i + 2] = y.z;
+      }
+    }
   }
-  __syncthreads();
-  for (int i = tid; i < mm; i += SCAN_SMALL_T) out[i] = sbuf[scan_pad(i)];
   if (tid == 0) out[m] = wsum[31];
 }
 

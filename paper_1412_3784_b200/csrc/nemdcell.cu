@@ -282,8 +282,21 @@ int sparse_kind(nc_ctx* ctx, const Geom& g) {
                                           : (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (env_mode == 0 || occ >= 4.0) return 0;
   // thread-per-particle wins once the grid fills the GPU (C3 DO 0.68 vs 0.72 ms, DS 0.67 vs 0.86 ms);
-  // on small systems (C1, 32k) the row-segment kernel's fewer, fuller blocks are ~10% faster
+  // on small systems (C1, 32k) the row-segment kernel's fewer, fuller blocks are ~10% faster; on tiny
+  // grids (the paper's E2 system, 1,728 particles) the particle-per-thread kernel with four threads per
+  // particle is (29.6 -> 26.1 us per DO step)
+  if (g.ncells < SP_LPP_CELLS) return 2;
   return ctx->n_last >= (1 << 18) ? 2 : 1;
+}
+
+// Threads per particle of k_pairs_sparse: 4 on small grids (the kernel's chain per warp, not the
+// GPU's throughput, bounds them), else 1.  NC_SP_LPP=1/4 forces either (A/B runs).  A function of the
+// grid only, so slab ranks and one device agree.
+int sparse_lpp(nc_ctx* ctx, const Geom& g) {
+  (void)ctx;
+  static int env = [] { const char* e = getenv("NC_SP_LPP"); return e ? atoi(e) : 0; }();
+  if (env == 1 || env == 4) return env;
+  return g.ncells < SP_LPP_CELLS ? 4 : 1;
 }
 
 nc_status apply_box(nc_ctx* ctx, const double* L) {
@@ -356,8 +369,7 @@ nc_status apply_box(nc_ctx* ctx, const double* L) {
 nc_status launch_scan_raw(nc_ctx* ctx, const uint32_t* in, int64_t m, uint32_t* out) {
   cudaStream_t s = ctx->stream;
   if (m <= SCAN_SMALL) {
-    launch_pdl(k_scan_small, dim3(1), dim3(SCAN_SMALL_T), sizeof(uint32_t) * (size_t)scan_pad((int)m + 32), s, in, m,
-               out);
+    launch_pdl(k_scan_small, dim3(1), dim3(SCAN_SMALL_T), 0, s, in, m, out);
     LAUNCHED();
   } else {
     const int64_t nb = (m + SCAN_TILE - 1) / SCAN_TILE;
@@ -451,13 +463,21 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                  (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const float4*)qs, (const uint32_t*)ctx->nh, gid,
                  (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
     } else if (sparse_kind(ctx, g) == 2) {  // sparse cells: one thread per particle (k3_sparse.cuh)
-      bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + SP_CPB - 1) / SP_CPB);  // a function of the grid only (P-invariant)
+      // small systems: four threads per particle (more warps, a quarter of the rows each)
+      const int lpp = sparse_lpp(ctx, g);
+      const int cpb = SP_CPB / lpp;
+      bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + cpb - 1) / cpb);  // a function of the grid only (P-invariant)
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      launch_pdl(k_pairs_sparse<DIGEST>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
-                 (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
-                 (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+      if (lpp == 4)
+        launch_pdl(k_pairs_sparse<DIGEST, 4>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
+                   (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+      else
+        launch_pdl(k_pairs_sparse<DIGEST, 1>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
+                   (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
     } else if (Gseg > 0) {  // sparse cells: one warp per row segment of Gseg cells (k3_seg.cuh)
       const int nseg = (g.dims[0] + Gseg - 1) / Gseg;
       const int bpl_s = nseg * g.dims[1];
@@ -1197,9 +1217,10 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_seg<true, 2>, sizeof(SgSmem<2>)},
         {(const void*)k_pairs_seg<false, 4>, sizeof(SgSmem<4>)},
         {(const void*)k_pairs_seg<true, 4>, sizeof(SgSmem<4>)},
-        {(const void*)k_scan_small, sizeof(uint32_t) * (size_t)scan_pad(SCAN_SMALL + 32)},
         {(const void*)k_pairs_sparse<false>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<false, 4>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<true, 4>, sizeof(SpSmem)},
         {(const void*)k_pairs_rows<false>, sizeof(RwSmem)},
         {(const void*)k_pairs_rows<true>, sizeof(RwSmem)}};
     for (const KA& a : ka) {
