@@ -464,7 +464,10 @@ k_rank_gather(int64_t n, const uint4* __restrict__ rec, const uint32_t* __restri
 #define NC_F64_SPLIT_B 8
 #endif
 constexpr int K3_F64_SPLIT_B = NC_F64_SPLIT_B;  // NC_F64 small grids: particles per i-batch when blocks share a cell
-constexpr int K3_CAP = 448;     // staged neighbor particles per warp per chunk
+#ifndef K3_CAP_OVR
+#define K3_CAP_OVR 448
+#endif
+constexpr int K3_CAP = K3_CAP_OVR;  // staged neighbor particles per warp per chunk
 constexpr int K3_DUMMY = K3_CAP + 64;  // permanent far element (padding slot of the evaluation)
 constexpr int K3_STAGE = K3_CAP + 66;  // fp64 mode: + up to S far sentinels so the filter needs no bounds checks
 #ifndef K3_QCAP_OVR
@@ -508,7 +511,7 @@ constexpr double K3_BAND64 = 1e-12;
 // fp32 mode: staged x, y, z (image bracket applied, centred on the center cell) and |v|^2 as four
 // arrays of stride K3_SSTR floats.  K3_SSTR = 8 (mod 32): the four words one mma B fragment takes
 // (lane (g, t) reads component t of element 8k + g) fall in four disjoint bank octets.
-constexpr int K3_SSTR = 520;
+constexpr int K3_SSTR = ((K3_CAP + 64 + 1 + 23) / 32) * 32 + 8;  // > K3_DUMMY, = 8 (mod 32): 520 for 448
 constexpr int K3_HW = (K3_CAP + 127) / 128;  // hit words per (row, MMA stream): 16 column blocks each
 static_assert(K3_SSTR % 32 == 8 && K3_SSTR > K3_DUMMY && 128 * K3_HW <= K3_DUMMY, "staging stride / padding");
 template <typename T>
