@@ -15,7 +15,10 @@ import subprocess
 import sys
 
 FLOP = {"FFMA2": (4, 32), "FADD2": (2, 32), "FMUL2": (2, 32), "FFMA": (2, 32), "FADD": (1, 32), "FMUL": (1, 32),
-        "DFMA": (2, 64), "DADD": (1, 64), "DMUL": (1, 64)}
+        "DFMA": (2, 64), "DADD": (1, 64), "DMUL": (1, 64),
+        # tensor cores: HMMA.1684 (mma.sync m16n8k4 tf32) = 2 x 16 x 8 x 4 = 1024 flop per warp instruction,
+        # i.e. 32 per predicated-on thread
+        "HMMA": (32, 19)}
 
 
 def main(rep):
@@ -23,7 +26,7 @@ def main(rep):
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
     hdr = rows[1]
-    tot = {32: 0.0, 64: 0.0}
+    tot = {32: 0.0, 64: 0.0, 19: 0.0}
     per = {}
     for r in rows[2:]:
         if len(r) != len(hdr):
@@ -56,6 +59,11 @@ def main(rep):
         rate = tot[bits] / sec
         print(f"fp{bits}: {tot[bits]:.4e} flop executed, {rate / 1e12:.2f} TFLOP/s = {rate / peak:.3f} of "
               f"{peak / 1e12:.1f}")
+    if tot[19]:
+        # dense tf32 tensor peak: half the bf16 one (B200_PROFILING: 2.25 PFLOP/s bf16 nominal)
+        rate = tot[19] / sec
+        print(f"tf32 (tensor cores): {tot[19]:.4e} flop executed, {rate / 1e12:.2f} TFLOP/s = {rate / 1.125e15:.4f} "
+              f"of the nominal 1125 TFLOP/s dense tf32")
 
 
 if __name__ == "__main__":
