@@ -421,7 +421,7 @@ nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *m
  *  NC_PK_AUTO    (default) per cell when the mean occupancy is at least 4 particles per
  *                cell; below that (WCA at rho = 0.8442: ~1.3) per particle from 2^18
  *                particles on and on grids of fewer than 8,192 cells (there with four
- *                threads per particle), per row segment otherwise;
+ *                or eight threads per particle), per row segment otherwise;
  *  NC_PK_CELL    one warp per center cell (k_pairs);
  *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
  *                union of their neighborhoods (k_pairs_seg, round 1), fp64 pair forces;

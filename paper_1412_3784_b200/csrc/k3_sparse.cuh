@@ -364,11 +364,13 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
     // queue slot addresses of this thread: qj[k][tid] at qa0 + 4 SP_NT k, qd[k][tid] SP_QD bytes further
     const uint32_t qa0 = smem_u32(&sm.qj[0][tid]);
     uint32_t qa = qa0;
-    for (int ri = sub; ri < 12; ri += LPP) {  // (the same trip count for every lane of the warp)
+    for (int it = 0; it < (12 + LPP - 1) / LPP; ++it) {  // (the same trip count for every lane of the warp)
+      const int rs = sub + it * LPP;  // this thread's stencil row (none past row 11 when LPP does not divide 12)
+      const int ri = rs < 12 ? rs : 11;
       SpSmem::RowW w;
       if (grp >= 0) w = sm.rw[wid][grp][ri];
       else sp_row_inv(g, ri, a1, layer, w);
-      const bool has = act && (w.meta & 1u);
+      const bool has = act && rs < 12 && (w.meta & 1u);
       if (!__any_sync(0xffffffffu, has)) continue;
       // columns [c0, c1) in <= 2 pieces of constant x shift n1 (the row wraps at most once:
       // c1 - c0 <= 4 <= l1) and the pieces' cell starts

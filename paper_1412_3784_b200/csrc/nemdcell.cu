@@ -289,14 +289,14 @@ int sparse_kind(nc_ctx* ctx, const Geom& g) {
   return ctx->n_last >= (1 << 18) ? 2 : 1;
 }
 
-// Threads per particle of k_pairs_sparse: 4 on small grids (the kernel's chain per warp, not the
-// GPU's throughput, bounds them), else 1.  NC_SP_LPP=1/4 forces either (A/B runs).  A function of the
+// Threads per particle of k_pairs_sparse: 8 below 2,048 cells, 4 below 8,192 (the kernel's chain per
+// warp, not the GPU's throughput, bounds such grids), else 1.  NC_SP_LPP=1/4/8 forces one (A/B runs).  A function of the
 // grid only, so slab ranks and one device agree.
 int sparse_lpp(nc_ctx* ctx, const Geom& g) {
   (void)ctx;
   static int env = [] { const char* e = getenv("NC_SP_LPP"); return e ? atoi(e) : 0; }();
-  if (env == 1 || env == 4) return env;
-  return g.ncells < SP_LPP_CELLS ? 4 : 1;
+  if (env == 1 || env == 4 || env == 8) return env;
+  return g.ncells < SP_LPP_CELLS / 4 ? 8 : (g.ncells < SP_LPP_CELLS ? 4 : 1);  // E2 (1,331 cells): 8 threads
 }
 
 nc_status apply_box(nc_ctx* ctx, const double* L) {
@@ -470,7 +470,11 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      if (lpp == 4)
+      if (lpp == 8)
+        launch_pdl(k_pairs_sparse<DIGEST, 8>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
+                   (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+      else if (lpp == 4)
         launch_pdl(k_pairs_sparse<DIGEST, 4>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
                    (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
                    (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
@@ -1221,6 +1225,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<false, 4>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true, 4>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<false, 8>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<true, 8>, sizeof(SpSmem)},
         {(const void*)k_pairs_rows<false>, sizeof(RwSmem)},
         {(const void*)k_pairs_rows<true>, sizeof(RwSmem)}};
     for (const KA& a : ka) {
