@@ -415,9 +415,10 @@ nc_status nc_sd_forces_end(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, 
 nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, const void *p, void *q_out,
                                   void *p_out, uint32_t *gid_out, void *F, double *parts);
 
-/* Choice of the K3 pair kernel (NC_F32 only; NC_F64 always uses the warp-per-cell
- * kernel).  Both evaluate the same neighborhoods, the same
- * candidates and the same pair set; they differ in how work maps to warps:
+/* Choice of the K3 pair kernel.  All evaluate the same neighborhoods, the
+ * same candidates and the same pair set; they differ in how work maps to warps.  NC_F64 has two:
+ * the warp-per-cell kernel and a particle-per-thread one (NC_PK_SPARSE, k_pairs_sparse64; AUTO
+ * below 4 particles per cell), both with the canonical fp64 test on every candidate.  NC_F32:
  *  NC_PK_AUTO    (default) per cell when the mean occupancy is at least 4 particles per
  *                cell; below that (WCA at rho = 0.8442: ~1.3) per particle from 2^18
  *                particles on and on grids of fewer than 8,192 cells (there with four
@@ -430,7 +431,7 @@ nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *m
  *  NC_PK_ROWS    one warp per cell row, batches of 32 consecutive particles whose neighbour rows
  *                are staged once in shared memory (k_pairs_rows, round 2), fp64 pair forces
  *                bitwise those of NC_PK_SPARSE.
- * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT / NC_PK_SPARSE / NC_PK_ROWS on an NC_F64 context).
+ * Errors: NC_E_ARG (bad value, or NC_PK_SEGMENT / NC_PK_ROWS on an NC_F64 context).
  * nc_pair_kernel_used returns the kernel of the last evaluation (1, 2, 3 or 4, 0 = none). */
 typedef enum { NC_PK_AUTO = 0, NC_PK_CELL = 1, NC_PK_SEGMENT = 2, NC_PK_SPARSE = 3, NC_PK_ROWS = 4 } nc_pair_kernel;
 nc_status nc_set_pair_kernel(nc_ctx *ctx, int which);

@@ -2017,3 +2017,4 @@ __global__ void k_unsort_idx(int64_t n, const typename V4<T>::t* __restrict__ sr
 #include "k3_seg.cuh"
 #include "k3_sparse.cuh"
 #include "k3_rows.cuh"
+#include "k3_sparse64.cuh"

@@ -270,7 +270,15 @@ int seg_cells(nc_ctx* ctx, const Geom& g) {
 // thread per particle (k_pairs_sparse).  AUTO takes the row-segment kernel below 4 particles per cell
 // (C3 DO: 0.70 ms vs 0.84 ms for the particle-per-thread kernel).
 int sparse_kind(nc_ctx* ctx, const Geom& g) {
-  if (ctx->cfg.prec != NC_F32 || ctx->pair_kernel == NC_PK_CELL) return 0;
+  if (ctx->cfg.prec != NC_F32) {  // NC_F64: the warp-per-cell kernel or k_pairs_sparse64
+    if (ctx->pair_kernel == NC_PK_SPARSE) return 2;
+    if (ctx->pair_kernel != NC_PK_AUTO) return 0;
+    // sparse cells (C1 in fp64: pair kernel 0.106 -> 0.027 ms, DO) get one thread per particle
+    const double occ64 = ctx->occ_hint >= 0.0 ? ctx->occ_hint
+                                              : (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
+    return occ64 < 4.0 ? 2 : 0;
+  }
+  if (ctx->pair_kernel == NC_PK_CELL) return 0;
   if (ctx->pair_kernel == NC_PK_SEGMENT) return 1;
   if (ctx->pair_kernel == NC_PK_SPARSE) return 2;
   if (ctx->pair_kernel == NC_PK_ROWS) return 3;
@@ -510,6 +518,14 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                    (const float4*)ctx->u32, (const uint32_t*)ctx->cs, qs, (const uint32_t*)ctx->nh, gid, F, bp,
                    ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
     }
+  } else if (sparse_kind(ctx, g) == 2) {  // NC_F64 sparse cells: one thread per particle (k3_sparse64.cuh)
+    bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + SP_CPB - 1) / SP_CPB);  // a function of the grid only
+    nblocks = bpl * nlay;
+    bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
+    ctx->pair_kernel_used = NC_PK_SPARSE;
+    launch_pdl(k_pairs_sparse64<DIGEST>, dim3(nblocks), dim3(SP_NT), sizeof(Sp64Smem), s, (const uint32_t*)ctx->cs,
+               (const uint4*)ctx->srec, (const double4*)qs, (const uint32_t*)ctx->nh, gid, (double4*)F, bp, ctx->dcnt,
+               ctx->dhs, ctx->dhx, g, bpl, layer0, po);
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
     bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
@@ -1106,8 +1122,8 @@ nc_status nc_set_pair_kernel(nc_ctx* ctx, int which) {
   if (which != NC_PK_AUTO && which != NC_PK_CELL && which != NC_PK_SEGMENT && which != NC_PK_SPARSE &&
       which != NC_PK_ROWS)
     return fail(ctx, NC_E_ARG, "pair kernel must be NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE or NC_PK_ROWS");
-  if ((which == NC_PK_SEGMENT || which == NC_PK_SPARSE || which == NC_PK_ROWS) && ctx->cfg.prec != NC_F32)
-    return fail(ctx, NC_E_ARG, "the segment pair kernel is NC_F32 only");
+  if ((which == NC_PK_SEGMENT || which == NC_PK_ROWS) && ctx->cfg.prec != NC_F32)
+    return fail(ctx, NC_E_ARG, "the segment and row-window pair kernels are NC_F32 only");
   ctx->pair_kernel = which;
   return NC_OK;
 }
@@ -1227,6 +1243,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_sparse<true, 4>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<false, 8>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true, 8>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse64<false>, sizeof(Sp64Smem)},
+        {(const void*)k_pairs_sparse64<true>, sizeof(Sp64Smem)},
         {(const void*)k_pairs_rows<false>, sizeof(RwSmem)},
         {(const void*)k_pairs_rows<true>, sizeof(RwSmem)}};
     for (const KA& a : ka) {

@@ -121,7 +121,8 @@ def _edge_case(kind, prec, variant, kernel):
                                                    ("f32", "do", "segment"), ("f32", "ds", "segment"),
                                                    ("f32", "do", "sparse"), ("f32", "ds", "sparse"),
                                                    ("f32", "do", "rows"), ("f32", "ds", "rows"),
-                                                   ("f64", "do", "cell"), ("f64", "ds", "cell")])
+                                                   ("f64", "do", "cell"), ("f64", "ds", "cell"),
+                                                   ("f64", "do", "sparse"), ("f64", "ds", "sparse")])
 def test_pairs_on_the_cutoff(kind, prec, variant, kernel):
     r, counts, cnt, hs, hx, st, n_on, n_edge = _edge_case(kind, prec, variant, kernel)
     assert 2 * n_edge >= 10000 and n_on >= 200  # >= 10^4 ordered pairs at the edge, hundreds exactly on it
@@ -132,8 +133,9 @@ def test_pairs_on_the_cutoff(kind, prec, variant, kernel):
         assert st["rechecks"] > 0  # the canonical fp64 test decided the pairs on the cutoff
 
 
+@pytest.mark.parametrize("kernel", ["cell", "sparse"])
 @pytest.mark.parametrize("variant", ["ds", "do"])
-def test_cutoff_at_the_last_bit_fp64(variant):
+def test_cutoff_at_the_last_bit_fp64(variant, kernel):
     """r_c^2 = X0 + k ulp(X0) around the exact squares X0 of the constructed pairs: pairs at r^2 = X0
     are inside for k > 0 and outside for k <= 0, decided by the canonical fp64 comparison."""
     L, rc0, q, d0 = edges.edge_pairs("le", npairs=3000, seed=4)
@@ -143,7 +145,7 @@ def test_cutoff_at_the_last_bit_fp64(variant):
         rc = edges.rc_with_square(X0, k)
         if rc is None:
             continue
-        cl = _cl(variant, "f64", rc, len(q), sigma=0.1)
+        cl = _cl(variant, "f64", rc, len(q), sigma=0.1, kernel=kernel)
         counts, wq, (cnt, hs, hx), st = _eval(cl, L, q, "f64")
         cl.close()
         r = oracle.evaluate(VAR[variant], wq, L, rc, 1.0, 0.1, 0.0)
@@ -156,7 +158,7 @@ def test_cutoff_at_the_last_bit_fp64(variant):
 
 
 @pytest.mark.parametrize("prec, kernel", [("f32", "cell"), ("f32", "segment"), ("f32", "sparse"), ("f32", "rows"),
-                                          ("f64", "cell")])
+                                          ("f64", "cell"), ("f64", "sparse")])
 def test_truncated_stencil_is_caught(prec, kernel):
     """Negative control: with the last entry of every neighborhood dropped (nc_debug), the same
     checks must fail -- the parity tests can see a missing stencil cell."""

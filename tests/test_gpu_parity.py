@@ -152,8 +152,7 @@ def test_pair_kernel_option_errors():
     cl = CellList("do", "f64", rc=2.5, capacity=16)
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel("segment")
-    with pytest.raises(NcError, match="NC_E_ARG"):
-        cl.pair_kernel("sparse")
+    cl.pair_kernel("sparse")  # NC_F64 has a particle-per-thread kernel too (k_pairs_sparse64)
     with pytest.raises(NcError, match="NC_E_ARG"):
         cl.pair_kernel("rows")
     with pytest.raises(NcError, match="NC_E_ARG"):
@@ -450,3 +449,18 @@ def test_rows_kernel_bitwise_equals_sparse_kernel(cfg, scale, variant):
     for k in ("candidates", "interactions", "stencil_cells", "rechecks"):
         assert a["stats"][k] == b["stats"][k], k
     assert abs(a["U"] - b["U"]) <= 1e-12 * abs(b["U"])
+
+
+@pytest.mark.parametrize("cfg, scale", [(1, 1), (1, 3), (3, 4), (0, 1)])
+@pytest.mark.parametrize("variant", ["ds", "do"])
+def test_sparse_kernel_fp64(cfg, scale, variant):
+    """NC_F64 on the particle-per-thread kernel (k_pairs_sparse64): the canonical fp64 test on every
+    candidate and error-free displacements, as the warp-per-cell kernel, mapped one thread per particle --
+    the oracle's cells, pair set (bit-exact), candidate counts and forces within 1e-12 RMS(F); C0's dense
+    LJ cells included (long stencil rows, frequent queue flushes)."""
+    w, q = inputs(cfg, "f64", scale=scale)
+    g, _ = check_against_oracle(w, q, variant, "f64", kernel="sparse")
+    assert g["kernel"] == "sparse"
+    c = gpu_eval(w, q, variant, "f64", kernel="cell")
+    assert g["stats"]["candidates"] == c["stats"]["candidates"]
+    assert g["stats"]["stencil_cells"] == c["stats"]["stencil_cells"]

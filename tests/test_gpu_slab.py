@@ -337,3 +337,31 @@ def test_slab_fp64_forces_and_steps_bitwise(variant, dev):
     assert out[0] == Us and np.array_equal(out[1], Ws)
     for r in sysm.ranks:
         r.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_slab_forces_bitwise_fp64_sparse_kernel(P):
+    """NC_F64 on the particle-per-thread kernel (k_pairs_sparse64) on every rank and on one device:
+    F, U and W bitwise P-invariant (block partials are fixed particle ranges of one layer)."""
+    import torch
+    from paper_1412_3784_b200.nemdcell import CellList
+
+    w = W.make(1, scale=2)
+    q = W.positions(w, dtype=np.float64, k=1)
+    p = W.momenta(w, dtype=np.float64, k=1)
+    one = CellList("do", "f64", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    one.pair_kernel("sparse")
+    one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
+    F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
+    assert one.pair_kernel_used() == "sparse"
+    one.close()
+    sysm = make_system(w, q, p, P, "do", "f64")
+    for r in sysm.ranks:
+        r.cl.pair_kernel("sparse")
+    U, Wv, st = sysm.forces(True)
+    assert all(r.cl.pair_kernel_used() == "sparse" for r in sysm.ranks)
+    _, _, F = gather_state(sysm, len(q), np.float64)
+    assert np.array_equal(F, F1.cpu().numpy())
+    assert U == U1 and np.array_equal(Wv, W1)
+    for r in sysm.ranks:
+        r.close()
