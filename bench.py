@@ -296,7 +296,14 @@ def run_slab(args):
 
     # N > 1: the library's own NCCL data plane (whole fixed-capacity messages, nc_sd_exchange_start /
     # nc_slab_allgather); torch only broadcasts the unique id.  No host synchronization inside a step.
-    sysm = SlabSystem([sr], NcclTransport(sr, rank, ws) if ws > 1 else LoopbackTransport())
+    if ws == 1:
+        tr = LoopbackTransport()
+    elif args.transport == "ipc":  # the packing kernels write the neighbours' receive buffers (peer memory)
+        from paper_1412_3784_b200.slab import IpcTransport
+        tr = IpcTransport(sr, rank, ws)
+    else:
+        tr = NcclTransport(sr, rank, ws)
+    sysm = SlabSystem([sr], tr)
     with torch.cuda.stream(stream):
         sysm.forces(False)
         for _ in range(args.warmup):
@@ -437,9 +444,9 @@ def run_slab(args):
                        "box": box_text(w), "potential": pot_text(w),
                        "precision": "fp32 storage + fp32 filter, fp32/fp64 two-tier interactions",
                        "l2": "inputs >> L2; no flush", "parallelism": f"slabs x{ws} (cell layers along lambda_3), "
-                                                                   "NCCL P2P halo + migration inside "
-                                                                   "libnemdcell, host-synchronization-free "
-                                                                   "step (fixed-capacity messages, nc_sd_*)"},
+                       + ("peer-memory halo + migration written by the packing kernels (CUDA IPC)"
+                          if args.transport == "ipc" and ws > 1 else "NCCL P2P halo + migration inside libnemdcell")
+                       + ", host-synchronization-free step (fixed-capacity messages, nc_sd_*)"},
             "particle_steps_per_s": w.n * args.steps / (ms_max * 1e-3),
             "kernel_ms_per_step_rank0": {k: v[0] / nprof for k, v in prof_all.items() if v[1]},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(t[3]), "clocks": clocks,
@@ -705,6 +712,9 @@ def main():
     ap.add_argument("--input", default="fluid", choices=["fluid", "lattice"],
                     help="fluid: BASELINE's relaxed uniform positions (default); lattice: the jittered crystal")
     ap.add_argument("--t0", type=float, default=None, help="KR configs: start at t0 = this fraction of t*")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N > 1 data plane: NCCL send/recv of whole messages (default) or peer-memory stores from "
+                         "the packing kernels (CUDA IPC, NVLink)")
     ap.add_argument("--pair-kernel", default="auto", choices=["auto", "cell", "segment", "sparse", "rows"],
                     help="force one K3 pair kernel (A/B runs; default: the library's choice)")
     ap.add_argument("--weak", action="store_true",

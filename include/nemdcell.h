@@ -415,6 +415,29 @@ nc_status nc_sd_forces_end(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, 
 nc_status nc_sd_forces_end_sorted(nc_ctx *ctx, const void *msg_lo, const void *msg_hi, const void *p, void *q_out,
                                   void *p_out, uint32_t *gid_out, void *F, double *parts);
 
+/* Peer-memory data plane of the slab step (the halo of P:445's cell layers and the migration
+ * of particles between slabs, written by the packing kernels STRAIGHT into the neighbour ranks' receive
+ * buffers -- pack and transfer in one pass over NVLink peer memory, no send buffer, copy or collective):
+ *  nc_ipc_alloc       a zeroed device buffer of `bytes` owned by ctx (freed by nc_destroy), and its
+ *                     64-byte cudaIpcMemHandle for the neighbours; pass *dptr as the RECEIVE buffer of
+ *                     nc_sd_absorb / nc_sd_forces_end(_sorted);
+ *  nc_ipc_open        map a neighbour's buffer from its handle (unmapped by nc_destroy); pass *dptr as
+ *                     the msg_lo / msg_hi argument of nc_sd_halo / nc_sd_migrate, which then write the
+ *                     neighbour's receive buffer directly;
+ *  nc_ipc_event       an interprocess event of ctx (64-byte handle), returned as an id;
+ *  nc_ipc_event_open  a neighbour's event from its handle, returned as an id;
+ *  nc_ipc_record      record event `id` after the work queued on cfg.stream;
+ *  nc_ipc_wait        cfg.stream waits for the latest record of event `id` (a stream wait: no kernel
+ *                     spins).  A wait binds to the record that precedes it on the host, so the caller
+ *                     separates neighbours' records from its waits by a host barrier (slab.IpcTransport).
+ * Errors: NC_E_ARG (null / bad id), NC_E_CUDA (IPC not available, e.g. no peer access). */
+nc_status nc_ipc_alloc(nc_ctx *ctx, int64_t bytes, void **dptr, void *handle);
+nc_status nc_ipc_open(nc_ctx *ctx, const void *handle, void **dptr);
+nc_status nc_ipc_event(nc_ctx *ctx, void *handle, int *id);
+nc_status nc_ipc_event_open(nc_ctx *ctx, const void *handle, int *id);
+nc_status nc_ipc_record(nc_ctx *ctx, int id);
+nc_status nc_ipc_wait(nc_ctx *ctx, int id);
+
 /* Choice of the K3 pair kernel.  All evaluate the same neighborhoods, the
  * same candidates and the same pair set; they differ in how work maps to warps.  NC_F64 has two:
  * the warp-per-cell kernel and a particle-per-thread one (NC_PK_SPARSE, k_pairs_sparse64; AUTO

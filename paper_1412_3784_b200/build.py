@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC_DIR = os.path.join(HERE, "csrc")
 SOURCES = [os.path.join(SRC_DIR, "nemdcell.cu")]
-DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("kernels.cuh", "k3_seg.cuh", "k3_sparse.cuh", "k3_rows.cuh", "k3_sparse64.cuh", "geom.hpp", "nccl_slab.cuh", "slab_dc.cuh")] + [
+DEPS = SOURCES + [os.path.join(SRC_DIR, f) for f in ("kernels.cuh", "k3_seg.cuh", "k3_sparse.cuh", "k3_rows.cuh", "k3_sparse64.cuh", "geom.hpp", "nccl_slab.cuh", "slab_dc.cuh", "ipc_slab.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "nemdcell.h")]
 LIB = os.path.join(HERE, "libnemdcell.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

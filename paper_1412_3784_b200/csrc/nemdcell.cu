@@ -20,6 +20,10 @@ using namespace nc;
 
 struct nc_ctx {
   nc_config cfg;
+  // peer-memory data plane (nc_ipc_*): buffers this context exported, peer buffers it mapped, and the
+  // interprocess events it created or opened
+  std::vector<void*> ipc_own, ipc_open;
+  std::vector<cudaEvent_t> ipc_ev;
   cudaStream_t stream = nullptr;
   std::string err;
   int64_t launches = 0;
@@ -1291,6 +1295,9 @@ void nc_destroy(nc_ctx* ctx) {
     cudaEventDestroy(p.second.second);
   }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (void* p : ctx->ipc_open) cudaIpcCloseMemHandle(p);
+  for (void* p : ctx->ipc_own) cudaFree(p);
+  for (auto e : ctx->ipc_ev) cudaEventDestroy(e);
   nc_comm_release(ctx);
   delete ctx;
 }
@@ -1784,6 +1791,7 @@ nc_status nc_slab_reduce(nc_ctx* ctx, const double* parts, int nlayers, double* 
 
 #include "nccl_slab.cuh"
 #include "slab_dc.cuh"
+#include "ipc_slab.cuh"
 
 void nc_comm_release(nc_ctx* ctx) {
   if (!ctx->comm) return;

@@ -36,7 +36,9 @@ EXPORTS = ["nc_create", "nc_destroy", "nc_set_box", "nc_set_flow", "nc_build_cel
            # host-synchronization-free slab step (csrc/slab_dc.cuh)
            "nc_sd_load", "nc_sd_status", "nc_sd_kick_drift", "nc_sd_kick", "nc_sd_migrate", "nc_sd_absorb",
            "nc_sd_halo", "nc_sd_exchange_start", "nc_sd_forces_begin", "nc_sd_forces_end",
-           "nc_sd_forces_end_sorted"]
+           "nc_sd_forces_end_sorted",
+           # peer-memory data plane (csrc/ipc_slab.cuh)
+           "nc_ipc_alloc", "nc_ipc_open", "nc_ipc_event", "nc_ipc_event_open", "nc_ipc_record", "nc_ipc_wait"]
 NC_DBG_DROP_ENTRIES = 1
 NC_PK_AUTO, NC_PK_CELL, NC_PK_SEGMENT, NC_PK_SPARSE, NC_PK_ROWS = 0, 1, 2, 3, 4
 PAIR_KERNELS = {"auto": NC_PK_AUTO, "cell": NC_PK_CELL, "segment": NC_PK_SEGMENT, "sparse": NC_PK_SPARSE, "rows": NC_PK_ROWS}
@@ -142,6 +144,12 @@ def load(build_if_missing: bool = True) -> ctypes.CDLL:
         L.nc_sd_forces_begin.argtypes = [vp, vp, vp, i64, i64, i32, i32]
         L.nc_sd_forces_end.argtypes = [vp, vp, vp, vp, vp]
         L.nc_sd_forces_end_sorted.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.nc_ipc_alloc.argtypes = [vp, i64, ctypes.POINTER(vp), vp]
+        L.nc_ipc_open.argtypes = [vp, vp, ctypes.POINTER(vp)]
+        L.nc_ipc_event.argtypes = [vp, vp, ctypes.POINTER(i32)]
+        L.nc_ipc_event_open.argtypes = [vp, vp, ctypes.POINTER(i32)]
+        L.nc_ipc_record.argtypes = [vp, i32]
+        L.nc_ipc_wait.argtypes = [vp, i32]
         L.nc_launch_count.argtypes = [vp]
         L.nc_launch_count.restype = i64
         L.nc_set_pair_kernel.argtypes = [vp, i32]
@@ -462,6 +470,40 @@ def nc_slab_reduce(ctx, parts: np.ndarray):
     st = np.zeros(4)
     _check(ctx, load().nc_slab_reduce(ctx, _ptr(parts), int(parts.shape[0]), ctypes.byref(U), _ptr(W), _ptr(st)))
     return U.value, W, {"interactions": st[0], "candidates": st[1], "stencil_cells": st[2], "rechecks": st[3]}
+
+
+def nc_ipc_alloc(ctx, nbytes: int):
+    """A zeroed device buffer owned by ctx, exported: (raw pointer as c_void_p, 64-byte handle)."""
+    p, h = ctypes.c_void_p(), (ctypes.c_uint8 * 64)()
+    _check(ctx, load().nc_ipc_alloc(ctx, int(nbytes), ctypes.byref(p), h))
+    return p, bytes(h)
+
+
+def nc_ipc_open(ctx, handle: bytes):
+    p, h = ctypes.c_void_p(), (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    _check(ctx, load().nc_ipc_open(ctx, h, ctypes.byref(p)))
+    return p
+
+
+def nc_ipc_event(ctx):
+    """An interprocess event of ctx: (id, 64-byte handle)."""
+    i, h = ctypes.c_int(), (ctypes.c_uint8 * 64)()
+    _check(ctx, load().nc_ipc_event(ctx, h, ctypes.byref(i)))
+    return i.value, bytes(h)
+
+
+def nc_ipc_event_open(ctx, handle: bytes) -> int:
+    i, h = ctypes.c_int(), (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    _check(ctx, load().nc_ipc_event_open(ctx, h, ctypes.byref(i)))
+    return i.value
+
+
+def nc_ipc_record(ctx, eid: int) -> None:
+    _check(ctx, load().nc_ipc_record(ctx, int(eid)))
+
+
+def nc_ipc_wait(ctx, eid: int) -> None:
+    _check(ctx, load().nc_ipc_wait(ctx, int(eid)))
 
 
 def nc_nccl_unique_id() -> bytes:

@@ -449,6 +449,105 @@ class HostStagedTransport(DistTransport):
         return pending
 
 
+class IpcTransport(DistTransport):
+    """The peer-memory data plane (csrc/ipc_slab.cuh) for the host-synchronization-free step (SlabRankDev,
+    P >= 2): every rank exports double-buffered receive buffers for the halo and migration messages and
+    maps its neighbours', and the packing kernels (nc_sd_halo, nc_sd_migrate) write their messages
+    straight into the neighbours' receive buffers -- pack and transfer in one pass over peer memory
+    (NVLink between GPUs), no send buffer, copy or collective.  An exchange is then ordering only:
+    interprocess events recorded after the packing ("sent") and after the reads of the previous messages
+    ("consumed"), a host barrier (a stream wait binds to the record issued before it), and stream waits
+    on the neighbours' events -- no kernel ever spins on another rank.  The energy partials and the rare
+    repartition go through torch.distributed like DistTransport."""
+
+    KINDS = ("h", "m")  # halo (4 words per record), migration (8 words per record)
+
+    def __init__(self, slab_rank, rank: int, nranks: int):
+        import torch
+        import torch.distributed as dist
+
+        assert nranks >= 2, "the peer-memory data plane needs neighbour ranks (P >= 2)"
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        super().__init__(rank, nranks, dev)
+        sr = self.sr = slab_rank
+        isz = sr.torch.empty(0, dtype=sr.dtype).element_size()
+        nbytes = {"h": (1 + sr.hcap) * 4 * isz, "m": (1 + sr.mcap) * 8 * isz}
+        self.words = {"h": 4, "m": 8}
+        own, blob = {}, b""
+        for k in self.KINDS:                      # receive buffers: [kind][side: from r-1, from r+1][parity]
+            for side in (0, 1):
+                for par in (0, 1):
+                    own[(k, side, par)], h = nc.nc_ipc_alloc(sr.ctx, nbytes[k])
+                    blob += h
+        self.ev = {}
+        for k in self.KINDS:
+            for e in ("S", "C"):
+                self.ev[(k, e)], h = nc.nc_ipc_event(sr.ctx)
+                blob += h
+        # handles and the per-exchange barrier on the host (gloo): an NCCL barrier would synchronize the
+        # device, which the host-synchronization-free step never does
+        self.cpu_group = dist.new_group(backend="gloo") if dist.get_backend() == "nccl" else None
+        t = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+        allb = [torch.zeros_like(t) for _ in range(nranks)]
+        dist.all_gather(allb, t, group=self.cpu_group)
+        allb = [bytes(x.numpy().tobytes()) for x in allb]
+
+        def mem_handle(r, k, side, par):
+            i = (self.KINDS.index(k) * 2 + side) * 2 + par
+            return allb[r][64 * i:64 * (i + 1)]
+
+        def ev_handle(r, k, e):
+            i = 8 + self.KINDS.index(k) * 2 + ("S", "C").index(e)
+            return allb[r][64 * i:64 * (i + 1)]
+
+        lo, hi = (rank - 1) % nranks, (rank + 1) % nranks
+        # our low message lands in r-1's "from r+1" buffer, our high message in r+1's "from r-1" buffer
+        self.send = {k: [[nc.nc_ipc_open(sr.ctx, mem_handle(lo, k, 1, par)),
+                          nc.nc_ipc_open(sr.ctx, mem_handle(hi, k, 0, par))] for par in (0, 1)] for k in self.KINDS}
+        self.recv = {k: [[own[(k, 0, par)], own[(k, 1, par)]] for par in (0, 1)] for k in self.KINDS}
+        peers = [lo] if lo == hi else [lo, hi]
+        self.pev = {(k, e): [nc.nc_ipc_event_open(sr.ctx, ev_handle(r, k, e)) for r in peers]
+                    for k in self.KINDS for e in ("S", "C")}
+        self.par = {k: 0 for k in self.KINDS}
+        self._point("h", send_par=0, recv_par=0)
+        self._point("m", send_par=0, recv_par=0)
+
+    def _point(self, k, send_par, recv_par):
+        """The rank's message pointers: the next packing writes parity send_par of the neighbours'
+        buffers, the next reads take parity recv_par of its own."""
+        if k == "h":
+            self.sr.hsend, self.sr.hrecv = self.send[k][send_par], self.recv[k][recv_par]
+        else:
+            self.sr.msend, self.sr.mrecv = self.send[k][send_par], self.recv[k][recv_par]
+
+    def _records(self, k):
+        ctx = self.sr.ctx
+        nc.nc_ipc_record(ctx, self.ev[(k, "C")])  # the reads of the previous messages are queued before
+        nc.nc_ipc_record(ctx, self.ev[(k, "S")])  # our messages are in the neighbours' buffers
+        self.dist.barrier(group=self.cpu_group)   # every record is issued before any neighbour's wait
+
+    def _waits(self, k):
+        ctx = self.sr.ctx
+        for i in self.pev[(k, "S")]:   # the neighbours' messages to us have landed
+            nc.nc_ipc_wait(ctx, i)
+        for i in self.pev[(k, "C")]:   # they are done with the parity our next packing writes
+            nc.nc_ipc_wait(ctx, i)
+        p = self.par[k]
+        self._point(k, send_par=1 - p, recv_par=p)
+        self.par[k] = 1 - p
+
+    def exchange_msgs(self, sends, recv_bufs):   # migration: packed by nc_sd_migrate into the neighbours
+        self._records("m")
+        self._waits("m")
+
+    def start_msgs(self, sends, recv_bufs):      # halo: the interior layers' K3 runs between start and finish
+        self._records("h")
+        self._pending = "h"
+
+    def finish_msgs(self):
+        self._waits(self._pending)
+
+
 class NcclTransport:
     """The data plane inside libnemdcell.so (nc_slab_exchange*, nc_slab_allgather over NCCL, on the
     library's communication stream): one rank per process, the host only broadcasts rank 0's NCCL

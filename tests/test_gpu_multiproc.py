@@ -1,6 +1,8 @@
 """Two processes, one GPU: real SlabRank contexts (libnemdcell.so on cuda:0 in each process) exchanging
 halo and migration records through torch.distributed gloo with every buffer staged through host memory
-(HostStagedTransport: no rank's kernels ever wait on another's on the device).  Forces, energy, virial
+(HostStagedTransport: no rank's kernels ever wait on another's on the device), or through the
+peer-memory data plane (IpcTransport: the packing kernels write the other process's receive buffers
+through CUDA IPC, ordered by interprocess events -- stream waits, no spinning kernels).  Forces, energy, virial
 and a short SLLOD run must be BITWISE equal to the single-device path -- the
 multi-process slab protocol end to end on the hardware this box has."""
 import os
@@ -27,7 +29,7 @@ def _flow_kw(w):
     return kw
 
 
-def _worker(rank, P, port, variant, out_dir, dev=False):
+def _worker(rank, P, port, variant, out_dir, dev=False, transport="host"):
     import torch
     import torch.distributed as dist
 
@@ -36,7 +38,8 @@ def _worker(rank, P, port, variant, out_dir, dev=False):
     dist.init_process_group("gloo", rank=rank, world_size=P)
     from paper_1412_3784_b200 import workloads as W
     from paper_1412_3784_b200.nemdcell import CellList
-    from paper_1412_3784_b200.slab import HostStagedTransport, SlabRank, SlabRankDev, SlabSystem, own_particles
+    from paper_1412_3784_b200.slab import (HostStagedTransport, IpcTransport, SlabRank, SlabRankDev, SlabSystem,
+                                           own_particles)
 
     w = W.make(2, scale=2)
     q = W.positions(w, dtype=np.float32, k=2)
@@ -50,7 +53,10 @@ def _worker(rank, P, port, variant, out_dir, dev=False):
                                             capacity=len(q), max_cells=4 * len(q) + 4096)
     sr.set_flow(w.A, w.policy, w.t0, **_flow_kw(w))
     sr.load(q[idx], p[idx], idx.astype(np.int32))
-    sysm = SlabSystem([sr], HostStagedTransport(rank, P))
+    # host: every buffer staged through host memory (gloo); ipc: the packing kernels write the neighbour's
+    # receive buffers through CUDA IPC peer memory, ordered by interprocess events (no kernel spins)
+    tr = IpcTransport(sr, rank, P) if transport == "ipc" else HostStagedTransport(rank, P)
+    sysm = SlabSystem([sr], tr)
     U0, W0, _ = sysm.forces(True)
     out = None
     for _ in range(3):
@@ -64,16 +70,16 @@ def _worker(rank, P, port, variant, out_dir, dev=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("dev", [False, True])
+@pytest.mark.parametrize("dev, transport, P", [(False, "host", 2), (True, "host", 2), (True, "ipc", 2),
+                                               (True, "ipc", 3)])
 @pytest.mark.parametrize("variant", ["do", "ds"])
-def test_two_processes_share_one_gpu_bitwise(variant, dev, tmp_path):
+def test_two_processes_share_one_gpu_bitwise(variant, dev, transport, P, tmp_path):
     import torch
     import torch.multiprocessing as mp
     from paper_1412_3784_b200 import workloads as W
     from paper_1412_3784_b200.nemdcell import CellList
 
-    P = 2
-    mp.start_processes(_worker, args=(P, _free_port(), variant, str(tmp_path), dev), nprocs=P, join=True,
+    mp.start_processes(_worker, args=(P, _free_port(), variant, str(tmp_path), dev, transport), nprocs=P, join=True,
                        start_method="spawn")
     w = W.make(2, scale=2)
     q = W.positions(w, dtype=np.float32, k=2)
