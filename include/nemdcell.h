@@ -444,8 +444,8 @@ nc_status nc_ipc_wait(nc_ctx *ctx, int id);
  * below 4 particles per cell), both with the canonical fp64 test on every candidate.  NC_F32:
  *  NC_PK_AUTO    (default) per cell when the mean occupancy is at least 4 particles per
  *                cell; below that (WCA at rho = 0.8442: ~1.3) per particle from 2^18
- *                particles on and on grids of fewer than 8,192 cells (there with four
- *                or eight threads per particle), per row segment otherwise;
+ *                particles on and on grids of fewer than 65,536 cells (there with two,
+ *                four or eight threads per particle), per row segment otherwise;
  *  NC_PK_CELL    one warp per center cell (k_pairs);
  *  NC_PK_SEGMENT one 2-warp block per row segment of cells sharing one staged
  *                union of their neighborhoods (k_pairs_seg, round 1), fp64 pair forces;

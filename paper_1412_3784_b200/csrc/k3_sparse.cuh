@@ -35,6 +35,7 @@ constexpr int SP_UNR = NC_SP_UNR;
 #define NC_SP_LPP_CELLS 8192  // grids below this many cells use 4 threads per particle (host sparse_lpp)
 #endif
 constexpr int64_t SP_LPP_CELLS = NC_SP_LPP_CELLS;
+constexpr int64_t SP_LPP2_CELLS = 65536;  // grids below this many cells: 2 threads per particle (AUTO)
 constexpr int SP_QD = SP_QCAP * SP_NT * 4;  // byte offset of qd from qj
 constexpr int SP_CPB = 96 * SP_NT / 128;  // cells of a layer per block (~1.3 particles each: ~one pass of SP_NT)  // candidates per iteration (their loads in flight together)
 

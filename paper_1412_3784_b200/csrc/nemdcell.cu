@@ -294,21 +294,23 @@ int sparse_kind(nc_ctx* ctx, const Geom& g) {
                                           : (double)ctx->n_last / (double)std::max<int64_t>(g.ncells, 1);
   if (env_mode == 0 || occ >= 4.0) return 0;
   // thread-per-particle wins once the grid fills the GPU (C3 DO 0.68 vs 0.72 ms, DS 0.67 vs 0.86 ms);
-  // on small systems (C1, 32k) the row-segment kernel's fewer, fuller blocks are ~10% faster; on tiny
-  // grids (the paper's E2 system, 1,728 particles) the particle-per-thread kernel with four threads per
-  // particle is (29.6 -> 26.1 us per DO step)
-  if (g.ncells < SP_LPP_CELLS) return 2;
+  // below 65,536 cells the particle-per-thread kernel with 2-8 threads per particle beats the row-segment
+  // kernel (C1: 36.9 vs 40.8 us per DO step; the paper's E2 system: 24.0 vs 29.0 us)
+  if (g.ncells < SP_LPP2_CELLS) return 2;  // with 2 / 4 / 8 threads per particle (sparse_lpp)
   return ctx->n_last >= (1 << 18) ? 2 : 1;
 }
 
-// Threads per particle of k_pairs_sparse: 8 below 2,048 cells, 4 below 8,192 (the kernel's chain per
-// warp, not the GPU's throughput, bounds such grids), else 1.  NC_SP_LPP=1/4/8 forces one (A/B runs).  A function of the
+// Threads per particle of k_pairs_sparse: 8 below 2,048 cells, 4 below 8,192, 2 below 65,536 (the
+// kernel's chain per warp, not the GPU's throughput, bounds such grids: C1 36.9 vs 42.0 us per step with
+// one thread, C3's 1.7M cells 0.72 vs 0.52 ms the other way), else 1.  NC_SP_LPP=1/2/4/8 forces one.  A function of the
 // grid only, so slab ranks and one device agree.
 int sparse_lpp(nc_ctx* ctx, const Geom& g) {
   (void)ctx;
   static int env = [] { const char* e = getenv("NC_SP_LPP"); return e ? atoi(e) : 0; }();
-  if (env == 1 || env == 4 || env == 8) return env;
-  return g.ncells < SP_LPP_CELLS / 4 ? 8 : (g.ncells < SP_LPP_CELLS ? 4 : 1);  // E2 (1,331 cells): 8 threads
+  if (env == 1 || env == 2 || env == 4 || env == 8) return env;
+  if (g.ncells < SP_LPP_CELLS / 4) return 8;  // E2 (1,331 cells)
+  if (g.ncells < SP_LPP_CELLS) return 4;
+  return g.ncells < SP_LPP2_CELLS ? 2 : 1;    // C1 (24,389 cells): 2 threads per particle
 }
 
 nc_status apply_box(nc_ctx* ctx, const double* L) {
@@ -482,7 +484,11 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
       nblocks = bpl * nlay;
       bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
       ctx->pair_kernel_used = NC_PK_SPARSE;
-      if (lpp == 8)
+      if (lpp == 2)
+        launch_pdl(k_pairs_sparse<DIGEST, 2>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
+                   (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
+                   (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+      else if (lpp == 8)
         launch_pdl(k_pairs_sparse<DIGEST, 8>, dim3(nblocks), dim3(SP_NT), sizeof(SpSmem), s, (const double4*)ctx->u,
                    (const float4*)ctx->u32, (const uint32_t*)ctx->cs, (const uint4*)ctx->srec, (const float4*)qs,
                    (const uint32_t*)ctx->nh, gid, (float4*)F, bp, ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
@@ -1245,6 +1251,8 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_sparse<true>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<false, 4>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true, 4>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<false, 2>, sizeof(SpSmem)},
+        {(const void*)k_pairs_sparse<true, 2>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<false, 8>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true, 8>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse64<false>, sizeof(Sp64Smem)},

@@ -109,12 +109,14 @@ def test_slab_sllod_bitwise(P, dev):
         r.close()
 
 
+@pytest.mark.parametrize("kernel", ["auto", "segment"])
 @pytest.mark.parametrize("P", [2, 3])
 @pytest.mark.parametrize("variant", ["do", "ds"])
 @pytest.mark.parametrize("dev", [False, True])
-def test_slab_forces_bitwise_sparse_cells(P, variant, dev):
-    """Sparse WCA cells (C1, ~1.3 per cell): every rank and the single device run
-    the row-segment pair kernel; forces, U, W and counts stay bitwise equal."""
+def test_slab_forces_bitwise_sparse_cells(P, variant, dev, kernel):
+    """Sparse WCA cells (C1, ~1.3 per cell): every rank and the single device run the same pair kernel
+    -- AUTO's choice (a function of the grid: the particle-per-thread kernel with two threads per particle
+    on C1's 24k cells) or the row-segment kernel; forces, U, W and counts stay bitwise equal."""
     import torch
     from paper_1412_3784_b200.nemdcell import CellList
 
@@ -122,14 +124,18 @@ def test_slab_forces_bitwise_sparse_cells(P, variant, dev):
     q = W.positions(w, dtype=np.float32, k=1)
     p = W.momenta(w, dtype=np.float32, k=1)
     one = CellList(variant, "f32", rc=w.rc, u_shift=w.ushift, capacity=len(q))
+    one.pair_kernel(kernel)
     one.set_flow(w.A, w.policy, w.t0, **flow_kw(w))
     F1, U1, W1 = one.compute_forces(torch.from_numpy(q).cuda())
     st1 = one.stats()
-    assert one.pair_kernel_used() == "segment"
+    used = one.pair_kernel_used()
+    assert used == ("sparse" if kernel == "auto" else kernel)
     one.close()
     sysm = make_system(w, q, p, P, variant, "f32", dev=dev)
+    for r in sysm.ranks:
+        r.cl.pair_kernel(kernel)
     U, Wv, st = sysm.forces(True)
-    assert all(r.cl.pair_kernel_used() == "segment" for r in sysm.ranks)
+    assert all(r.cl.pair_kernel_used() == used for r in sysm.ranks)
     _, _, F = gather_state(sysm, len(q), np.float32)
     assert np.array_equal(F, F1.cpu().numpy())
     assert U == U1 and np.array_equal(Wv, W1)
