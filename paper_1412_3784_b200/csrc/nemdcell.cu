@@ -271,8 +271,10 @@ int seg_cells(nc_ctx* ctx, const Geom& g) {
 }
 
 // Pair kernel for this grid: 0 = warp per cell (k_pairs), 1 = row segments (k_pairs_seg), 2 = one
-// thread per particle (k_pairs_sparse).  AUTO takes the row-segment kernel below 4 particles per cell
-// (C3 DO: 0.70 ms vs 0.84 ms for the particle-per-thread kernel).
+// thread per particle (k_pairs_sparse; k_pairs_sparse64 in NC_F64), 3 = row windows (k_pairs_rows).
+// AUTO below 4 particles per cell: the particle-per-thread kernel from 2^18 particles on and on grids
+// below 65,536 cells (sparse_lpp: 2-8 threads per particle there), the row-segment kernel otherwise
+// (DESIGN.md sections 5 and 7).
 int sparse_kind(nc_ctx* ctx, const Geom& g) {
   if (ctx->cfg.prec != NC_F32) {  // NC_F64: the warp-per-cell kernel or k_pairs_sparse64
     if (ctx->pair_kernel == NC_PK_SPARSE) return 2;
