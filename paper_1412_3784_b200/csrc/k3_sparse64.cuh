@@ -53,7 +53,7 @@ __device__ __forceinline__ void sp64_eval(const Geom& g, const Sp64Smem& sm, con
 // grid = nlay layers x bpl blocks, bpl = ceil(l1 l2 / SP_CPB): block b of layer L takes the layer's
 // particles [b SP_NT, (b+1) SP_NT) + k bpl SP_NT, k = 0, 1, ... and the layer's cells the same way
 // for the stencil-size statistic (empty cells included).
-template <bool DIGEST>
+template <bool DIGEST, int LPP = 1>
 __global__ void __launch_bounds__(SP_NT, 4)
 k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec, const double4* __restrict__ qs,
                  const uint32_t* __restrict__ nh, const uint32_t* __restrict__ gid, double4* __restrict__ Fout,
@@ -83,8 +83,12 @@ k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec,
     tS += (uint32_t)(ns - g.dbg_drop);
   }
 
-  for (uint32_t base = P0 + (uint32_t)b * SP_NT; base < P1; base += (uint32_t)bpl * SP_NT) {
-    const uint32_t i = base + (uint32_t)tid;
+  // LPP > 1 (small grids): LPP consecutive threads share one particle, thread `sub` walking the stencil
+  // rows sub, sub + LPP, ...; the owner (sub 0) adds the others' sums in fixed order (shuffles)
+  constexpr int NPB = SP_NT / LPP;
+  const int sub = LPP > 1 ? tid % LPP : 0;
+  for (uint32_t base = P0 + (uint32_t)b * NPB; base < P1; base += (uint32_t)bpl * NPB) {
+    const uint32_t i = base + (uint32_t)(LPP > 1 ? tid / LPP : tid);
     const bool act = i < P1;
     const uint32_t me = act ? i : P0;
     const uint32_t c = rec[me].z;  // the cell of sorted slot me
@@ -101,9 +105,10 @@ k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec,
         SpRow r;
         if (sp_row(g, ri, a0, a1, layer, r)) last_ri = ri;
       }
-    for (int ri = 0; ri < 12; ++ri) {
+    for (int it = 0; it < (12 + LPP - 1) / LPP; ++it) {  // (the same trip count for every lane)
+      const int ri = sub + it * LPP;
       SpRow r;
-      const bool has = act && sp_row(g, ri, a0, a1, layer, r);
+      const bool has = act && ri < 12 && sp_row(g, ri, a0, a1, layer, r);
       if (!__any_sync(0xffffffffu, has)) continue;
       if (!has) { r.c0 = r.c1 = a0; r.base = 0u; r.n2 = r.n3 = 0; }
       if (has && g.dbg_drop && ri == last_ri) r.c1 -= 1;
@@ -154,7 +159,26 @@ k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec,
       }
     }
     sp64_eval<DIGEST>(g, sm, qs, gid, nq, tid, qi, acc, po, gi);
-    if (act) {
+    if (LPP > 1) {
+      if (act) tC += ncand;  // each thread its own rows' candidates (the self pair subtracted by the owner)
+#pragma unroll
+      for (int k = 1; k < LPP; ++k) {  // the owner adds sub 1, 2, ... in order
+        const double fx = __shfl_down_sync(0xffffffffu, acc.fx, k), fy = __shfl_down_sync(0xffffffffu, acc.fy, k),
+                     fz = __shfl_down_sync(0xffffffffu, acc.fz, k), uu = __shfl_down_sync(0xffffffffu, acc.u, k);
+        const double w0 = __shfl_down_sync(0xffffffffu, acc.w0, k), w1 = __shfl_down_sync(0xffffffffu, acc.w1, k),
+                     w2 = __shfl_down_sync(0xffffffffu, acc.w2, k), w3 = __shfl_down_sync(0xffffffffu, acc.w3, k),
+                     w4 = __shfl_down_sync(0xffffffffu, acc.w4, k), w5 = __shfl_down_sync(0xffffffffu, acc.w5, k);
+        const uint32_t cn = __shfl_down_sync(0xffffffffu, acc.cnt, k);
+        const uint64_t h1 = __shfl_down_sync(0xffffffffu, acc.hs, k), h2 = __shfl_down_sync(0xffffffffu, acc.hx, k);
+        if (sub == 0) {
+          acc.fx += fx; acc.fy += fy; acc.fz += fz; acc.u += uu;
+          acc.w0 += w0; acc.w1 += w1; acc.w2 += w2; acc.w3 += w3; acc.w4 += w4; acc.w5 += w5;
+          acc.cnt += cn;
+          if (DIGEST) { acc.hs += h1; acc.hx ^= h2; }
+        }
+      }
+    }
+    if (act && sub == 0) {
       const double Ui = 2.0 * g.eps * acc.u - 0.5 * g.ushift * (double)acc.cnt;
       const double4 fv = make_double4(acc.fx, acc.fy, acc.fz, (double)acc.cnt);  // lab frame
       Fout[me] = fv;
@@ -164,7 +188,7 @@ k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec,
       tW[0] += 0.5 * acc.w0; tW[1] += 0.5 * acc.w1; tW[2] += 0.5 * acc.w2;
       tW[3] += 0.5 * acc.w3; tW[4] += 0.5 * acc.w4; tW[5] += 0.5 * acc.w5;
       tI += acc.cnt;
-      tC += ncand - 1u;
+      tC += (LPP > 1 ? 0u : ncand) - 1u;
       tNF += isfinite(acc.fx + acc.fy + acc.fz + Ui) ? 0.0 : 1.0;
     }
   }

@@ -531,13 +531,20 @@ nc_status launch_pairs(nc_ctx* ctx, const typename V4<T>::t* qs, const uint32_t*
                    ctx->dcnt, ctx->dhs, ctx->dhx, g, cpb, bpl, layer0, po);
     }
   } else if (sparse_kind(ctx, g) == 2) {  // NC_F64 sparse cells: one thread per particle (k3_sparse64.cuh)
-    bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + SP_CPB - 1) / SP_CPB);  // a function of the grid only
+    const int lpp = sparse_lpp(ctx, g) >= 2 ? 2 : 1;  // two threads per particle on small grids
+    const int cpb64 = SP_CPB / lpp;
+    bpl = (int)(((int64_t)g.dims[0] * g.dims[1] + cpb64 - 1) / cpb64);  // a function of the grid only
     nblocks = bpl * nlay;
     bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
     ctx->pair_kernel_used = NC_PK_SPARSE;
-    launch_pdl(k_pairs_sparse64<DIGEST>, dim3(nblocks), dim3(SP_NT), sizeof(Sp64Smem), s, (const uint32_t*)ctx->cs,
-               (const uint4*)ctx->srec, (const double4*)qs, (const uint32_t*)ctx->nh, gid, (double4*)F, bp, ctx->dcnt,
-               ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+    if (lpp == 2)
+      launch_pdl(k_pairs_sparse64<DIGEST, 2>, dim3(nblocks), dim3(SP_NT), sizeof(Sp64Smem), s, (const uint32_t*)ctx->cs,
+                 (const uint4*)ctx->srec, (const double4*)qs, (const uint32_t*)ctx->nh, gid, (double4*)F, bp,
+                 ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
+    else
+      launch_pdl(k_pairs_sparse64<DIGEST, 1>, dim3(nblocks), dim3(SP_NT), sizeof(Sp64Smem), s, (const uint32_t*)ctx->cs,
+                 (const uint4*)ctx->srec, (const double4*)qs, (const uint32_t*)ctx->nh, gid, (double4*)F, bp,
+                 ctx->dcnt, ctx->dhs, ctx->dhx, g, bpl, layer0, po);
   } else {
     ctx->pair_kernel_used = NC_PK_CELL;
     bp = ctx->bpart + (int64_t)(layer0 - part_layer0) * bpl * NPART;
@@ -1257,8 +1264,10 @@ nc_status nc_create(const nc_config* cfg, nc_ctx** out) {
         {(const void*)k_pairs_sparse<true, 2>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<false, 8>, sizeof(SpSmem)},
         {(const void*)k_pairs_sparse<true, 8>, sizeof(SpSmem)},
-        {(const void*)k_pairs_sparse64<false>, sizeof(Sp64Smem)},
-        {(const void*)k_pairs_sparse64<true>, sizeof(Sp64Smem)},
+        {(const void*)k_pairs_sparse64<false, 1>, sizeof(Sp64Smem)},
+        {(const void*)k_pairs_sparse64<true, 1>, sizeof(Sp64Smem)},
+        {(const void*)k_pairs_sparse64<false, 2>, sizeof(Sp64Smem)},
+        {(const void*)k_pairs_sparse64<true, 2>, sizeof(Sp64Smem)},
         {(const void*)k_pairs_rows<false>, sizeof(RwSmem)},
         {(const void*)k_pairs_rows<true>, sizeof(RwSmem)}};
     for (const KA& a : ka) {
