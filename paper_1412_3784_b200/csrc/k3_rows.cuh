@@ -346,6 +346,7 @@ k_pairs_rows(const double4* __restrict__ u, const float4* __restrict__ u32, cons
                 const float bx = fmaf((float)(colw - (inb ? 0 : sm.cwa[r])), w0x, inb ? sm.bxb[r] : sm.bxa[r]);
                 const SpSmem::RowW& w = sm.rw[r];
                 const int off = sm.S[r] - gbase + (int)t;
+                NC_CHECK(off >= 0 && off < RW_CAP);
                 sm.st[off] = make_float4(v[h].x + bx, v[h].y + w.byf, v[h].z + w.bzf, __uint_as_float(jv[h]));
                 // unwrapped column - Aref (16 bits), stencil row, piece (its x image: n1a + inb)
                 sm.code[off] = (uint32_t)(colw + (inb ? sm.cut[r] : sm.nla[r]) - Aref + 32768) | ((uint32_t)r << 16) |
@@ -373,6 +374,7 @@ k_pairs_rows(const double4* __restrict__ u, const float4* __restrict__ u32, cons
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               t[h] = k + h < len ? s0 + k + h : 0;
+              NC_CHECK(t[h] >= 0 && t[h] < RW_CAP);
               v[h] = lds128(st0 + 16u * (uint32_t)t[h]);
             }
 #pragma unroll
@@ -380,6 +382,7 @@ k_pairs_rows(const double4* __restrict__ u, const float4* __restrict__ u32, cons
               const float dx = v[h].x - xi, dy = v[h].y - yi, dz = v[h].z - zi;
               const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
               const bool hit = (k + h < len) && (r2 < hi32) && (__float_as_uint(v[h].w) != me);
+              NC_CHECK(nq < RW_QCAP);
               sts16(qa0 + 64u * (uint32_t)nq, (uint32_t)t[h]);  // nq <= RW_QCAP - 1 here
               nq += hit ? 1 : 0;
             }

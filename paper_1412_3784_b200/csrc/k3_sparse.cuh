@@ -455,6 +455,7 @@ k_pairs_sparse(const double4* __restrict__ u, const float4* __restrict__ u32, co
 #pragma unroll
         for (int k = 1; k < LPP; ++k) {
           const int o = tid + k;
+          NC_CHECK(o < SP_NT && (o >> 5) == (tid >> 5));
           acc.fx += sm.acc[0][o]; acc.fy += sm.acc[1][o]; acc.fz += sm.acc[2][o]; acc.u += sm.acc[3][o];
           acc.w0 += sm.acc[4][o]; acc.w1 += sm.acc[5][o]; acc.w2 += sm.acc[6][o];
           acc.w3 += sm.acc[7][o]; acc.w4 += sm.acc[8][o]; acc.w5 += sm.acc[9][o];

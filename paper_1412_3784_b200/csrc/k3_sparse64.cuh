@@ -152,6 +152,7 @@ k_pairs_sparse64(const uint32_t* __restrict__ cs, const uint4* __restrict__ rec,
           }
           const double r2 = canonical_r2(g, qj[h].x, qj[h].y, qj[h].z, qi.x, qi.y, qi.z, n0, n1, n2);
           const bool hit = valid && jv[h] != me && r2 < g.rc2;
+          NC_CHECK(nq < SP64_QCAP);
           sm.qj[nq][tid] = jv[h];  // (slot nq <= SP64_QCAP - 1 here)
           sm.qn[nq][tid] = pack_n3(n0, n1, n2);
           nq += hit ? 1 : 0;

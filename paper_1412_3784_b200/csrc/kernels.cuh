@@ -41,6 +41,13 @@ namespace nc {
 #define PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
 #define PDL_LAUNCH() asm volatile("griddepcontrol.launch_dependents;" :::)
 #define PDL_ENTRY() do { PDL_WAIT(); PDL_LAUNCH(); } while (0)
+// bounds checks of shared-memory indices in the newer pair kernels (a debug build: -DNC_BOUNDS; a failed
+// check traps the kernel, which the host reports as NC_E_CUDA)
+#ifdef NC_BOUNDS
+#define NC_CHECK(c) do { if (!(c)) __trap(); } while (0)
+#else
+#define NC_CHECK(c) do { } while (0)
+#endif
 
 template <typename T> struct V4;
 template <> struct V4<float> { using t = float4; };
