@@ -1178,8 +1178,10 @@ __device__ __forceinline__ void eval_hits(const Geom& g, const PairCtx<float>& p
       // the MMA margin beyond it (the fp64 tier rejects those) -- goes to the close queue
       const bool fa = r2a >= split2 && r2a < lo32, fb = r2b >= split2 && r2b < lo32;
       const bool qa = va && !fa, qb = vb && !fb;  // predicated stores: no wavefront otherwise
+      NC_CHECK(!qa || qc < qc0 + K3_QSTRIDE * K3_CQ);
       if (qa) stsq(qc, aa);
       qc += qa ? K3_QSTRIDE : 0u;
+      NC_CHECK(!qb || qc < qc0 + K3_QSTRIDE * K3_CQ);
       if (qb) stsq(qc, ab);
       qc += qb ? K3_QSTRIDE : 0u;
       float ia, ib;
@@ -1391,7 +1393,9 @@ k_pairs(const double4* __restrict__ u, const float4* __restrict__ u32, const uin
             continue;
           }
           const uint32_t ctot = (e1 < nst ? sm.e_off[e1] : tot) - base_off;
+          NC_CHECK(ctot <= (uint32_t)K3_CAP);
           const int W = (int)((ctot + 127) / 128);  // hit words: 16 column blocks of 8 elements each
+          NC_CHECK(128 * W <= K3_DUMMY && 2 * W <= K3_MW);
           // (a vote: the compiler then knows the branch is warp-uniform and keeps the shuffles of the
           // rest of the kernel free of divergence handling)
           if (__any_sync(0xffffffffu, e0 != staged0 || e1 != staged1)) {
